@@ -1,0 +1,181 @@
+/* include/lsmgnn.h — C-ABI of the B200-native LSM-GNN feature-gather hot path.
+ *
+ * Method: LSM-GNN (arXiv 2407.15264), PAPER.md (= /root/reference/PAPER.md, cited
+ * "P:n" = line n). The library gathers the feature rows of sampled nodes through
+ * per-GPU software caches that a home-GPU directory turns into one box-wide shared
+ * cache (§4.1 "Communication Layer"), with the hybrid eviction policy
+ * (§4.2), a victim buffer in pinned host memory and its Preemptive
+ * Victim-buffer Prefetcher (§4.3), and a host-resident backing table that
+ * stands in for the SSD tier. DESIGN.md states every reading taken where the
+ * paper is silent (R1..R25) and the data layout.
+ *
+ * Process model: one process per GPU ("DDP leverages multi-processing");
+ * rank r of G is the home of every node v with v mod G == r (R1).
+ * All calls are made from the thread that owns the rank's CUDA device.
+ *
+ * Conventions (all entry points):
+ *   - return 0 on success or a negative LSMGNN_E* code; lsmgnn_last_error() gives
+ *     a one-line message. No C++ exception crosses the ABI.
+ *   - pointers documented "device" must be CUDA device (or managed) addresses of the
+ *     calling rank's device; "host" pointers are ordinary (or pinned) host memory.
+ *   - stream arguments are cudaStream_t values passed as void* (0 = legacy default).
+ *   - the library owns every buffer it allocates (cache, window mask, staging,
+ *     inboxes on the device; victim queues in pinned host memory). It references but
+ *     does not own the backing table registered with lsmgnn_attach_storage.
+ *   - errors detected on the device (a node ID >= num_nodes) set a sticky flag; the
+ *     next call (or lsmgnn_stats) returns LSMGNN_ERANGE and the out rows of those
+ *     IDs are zero-filled.
+ */
+#ifndef LSMGNN_H
+#define LSMGNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSMGNN_ABI_VERSION 1
+
+/* ---- return codes */
+#define LSMGNN_OK 0
+#define LSMGNN_EINVAL (-1)  /* bad argument, alignment (R % 16 != 0) or n > max_batch_ids */
+#define LSMGNN_ERANGE (-2)  /* a node ID >= num_nodes (sticky, device-detected)             */
+#define LSMGNN_ENOMEM (-3)  /* device or pinned-host allocation failed                      */
+#define LSMGNN_ECUDA (-4)   /* a CUDA runtime/driver call failed                            */
+#define LSMGNN_ESTATE (-5)  /* call order (not initialised, iterations out of order, ...)   */
+#define LSMGNN_ECOMM (-6)   /* peer mapping / exchange failure                              */
+
+typedef enum { LSMGNN_F32 = 0, LSMGNN_F16 = 1, LSMGNN_BF16 = 2 } lsmgnn_dtype;
+
+/* Replacement policy. HYBRID is the paper's; STATIC and DYNAMIC are the
+ * single-information ablations of P:645; RR is the M-GIDS baseline policy;
+ * LRU is the north-star comparison policy. */
+typedef enum {
+  LSMGNN_HYBRID = 0,
+  LSMGNN_STATIC = 1,
+  LSMGNN_LRU = 2,
+  LSMGNN_RR = 3,
+  LSMGNN_DYNAMIC = 4
+} lsmgnn_policy;
+
+/* Options (optional; call lsmgnn_set_options before lsmgnn_init, defaults otherwise).
+ *   policy          default HYBRID
+ *   pvp             1 = victim buffer + PVP on; default 0
+ *   window          W, iterations of look-ahead (W = 256 in P:607); default 256
+ *   threshold       T; 0 => max(1, W/8) ("by default ... 1/8 of the window")
+ *   update_period   P; only 1 (exact dynamic information) is implemented (R6)
+ *   reinsert_victims 1 = a victim-buffer hit is re-inserted into the cache (R15); default 1
+ *   max_batch_ids   capacity: the largest n any rank passes to gather/prefetch; default 1<<20 */
+typedef struct {
+  int32_t version; /* LSMGNN_ABI_VERSION */
+  lsmgnn_policy policy;
+  int32_t pvp;
+  int32_t window;
+  int32_t threshold;
+  int32_t update_period;
+  int32_t reinsert_victims;
+  int64_t max_batch_ids;
+} lsmgnn_options;
+
+/* Per-home counters, one record per gather iteration (scope 0) or summed (scope 1).
+ * Every count except `requests`/`peer_requests` is over UNIQUE nodes of the batch at
+ * this home (R11). hits + victim_hits + storage_reads == unique (I2).
+ *   evict_by_class[c]: c = 0 NoReuse, 1 Far (d > T), 2 Fresh, 3 Near (d <= T)
+ *   victim_admitted/_dropped: eviction candidates with a next reuse (pvp = 1) that did /
+ *     did not find room in victim queue reuse mod W
+ *   evicted_no_reuse: evictions that were not victim candidates (discarded)
+ *   pvp_prefetched: rows the PVP staged for this iteration; pvp_unused: staged rows this
+ *     iteration did not request
+ *   bytes_*: the per-tier algorithmic bytes (R = row bytes): out = requests*R,
+ *     nvlink = peer_requests*R, h2d_storage = storage_reads*R, h2d_pvp = pvp_prefetched*R,
+ *     d2h_victim = victim_admitted*R. */
+typedef struct {
+  uint64_t iter, requests, peer_requests, unique, hits, victim_hits, storage_reads, inserted,
+      bypassed, evictions, evict_by_class[4], victim_admitted, victim_dropped, evicted_no_reuse,
+      pvp_prefetched, pvp_unused;
+  uint64_t bytes_out, bytes_nvlink, bytes_h2d_storage, bytes_h2d_pvp, bytes_d2h_victim;
+} lsmgnn_stats_t;
+
+/* Bind this process to (rank, world, device) before lsmgnn_init. The binding takes
+ * them from its torch.distributed process group. Default (0, 1, current device). */
+int lsmgnn_bind(int32_t rank, int32_t world, int32_t device);
+
+int lsmgnn_set_options(const lsmgnn_options* opt);
+
+/* Allocate this rank's home: a `ways`-way set-associative cache of lines_per_gpu rows
+ * ("32-way set associative GPU software cache"; S = lines_per_gpu / ways sets,
+ * set(v) = floor(v / G) mod S, R2), the window reuse mask, staging areas and, when
+ * pvp = 1, W victim queues of floor(victim_lines / W) rows in pinned host memory
+ * ("data ... victim buffers", "16K cache-lines" each; R13).
+ *   num_nodes      N; node IDs are 0 .. N-1
+ *   feat_dim, dtype  row bytes R = feat_dim * sizeof(dtype); R % 16 must be 0
+ *   lines_per_gpu  L (> 0, multiple of ways), ways A in 1..32
+ *   victim_lines   V (ignored when pvp = 0)
+ *   static_scores  host u8[num_nodes], higher = hotter (one byte P:322 draft);
+ *                  copied (caller may free after the call). NULL => all zero.
+ * Collective in the sense that every rank must call it with identical arguments. */
+int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t lines_per_gpu,
+                int32_t ways, int64_t victim_lines, const uint8_t* static_scores);
+
+/* Register this home's partition of the backing "storage" table: host memory holding
+ * the rows of nodes v = rank, rank+G, rank+2G, ... in that order (row k = node
+ * rank + k*G), ceil((N - rank)/G) rows of R bytes. The library page-locks it with
+ * cudaHostRegister unless it is already pinned, and reads it with zero-copy loads from
+ * its fill kernel (features "directly fetched by GPU threads").
+ * nvme_path must be NULL (an NVMe tier is not implemented). */
+int lsmgnn_attach_storage(const void* host_rows_for_my_home, const char* nvme_path);
+
+/* G > 1 bootstrap. lsmgnn_export_handle writes this rank's shareable handle blob
+ * (cudaIpcMemHandle of its shared arena + layout) into buf (cap >= lsmgnn_handle_bytes()).
+ * The binding all-gathers the blobs over the torch process group and passes the
+ * concatenation (world * lsmgnn_handle_bytes() bytes, rank order) to lsmgnn_connect,
+ * which opens every peer mapping. Not needed when world == 1. */
+size_t lsmgnn_handle_bytes(void);
+int lsmgnn_export_handle(void* buf, size_t cap);
+int lsmgnn_connect(const void* peer_handles, int32_t world);
+
+/* gather(t): collective, lockstep — every rank calls it once per iteration t.
+ * Stream-ordered on `stream`: node_ids (device int64[n]) and out (device, n*R bytes,
+ * row-major, tightly packed) are caller-owned and must stay valid until the stream
+ * reaches the end of this call. Result: out[i] = table[node_ids[i]] (R bytes), routed
+ * through the shared cache and the hit / victim-buffer / storage tiers.
+ * n may be 0. Asynchronous: no host synchronisation in steady state. */
+int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream);
+
+/* Same as lsmgnn_gather but node_ids and out are HOST pointers (pinned or pageable);
+ * the host->device copy of the IDs and the device->host copy of the rows are done
+ * on `stream` inside the call (used for the end-to-end measurement). Synchronous. */
+int lsmgnn_gather_host(const int64_t* host_ids, int64_t n, void* host_out, void* stream);
+
+/* prefetch: collective. Feeds this rank's future batches to the window buffer
+ * (P:249): batch b = ids[offsets[b] .. offsets[b+1]) (device int64 arrays;
+ * offsets has num_batches + 1 entries, offsets[0] == 0 and the offsets array is a
+ * HOST pointer) for iterations first_iter .. first_iter + num_batches - 1.
+ *  - The bootstrap call (before the first gather) feeds iterations 1 .. W.
+ *  - Each later call, after gather(t), feeds the single batch t + 1 + W (an empty
+ *    batch past the end of the trace) and launches the PVP copy of victim queue
+ *    (t+1) mod W into home staging on a side stream (R17); gather(t+1)
+ *    waits for it with an event. */
+int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batches,
+                    int64_t first_iter, void* stream);
+
+/* Counters of this home: scope 0 = the last completed gather, 1 = cumulative.
+ * Synchronises with the last stream used. */
+int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope);
+
+/* Per-iteration records for iterations [first, first+count) (kept on the device in a
+ * ring of the last 4096 iterations). Synchronous. */
+int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count);
+
+/* Number of kernels the library has launched since init (launch accounting). */
+int64_t lsmgnn_kernel_launches(void);
+
+int lsmgnn_finalize(void);
+const char* lsmgnn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSMGNN_H */

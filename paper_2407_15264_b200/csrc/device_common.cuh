@@ -1,0 +1,167 @@
+// device_common.cuh — small device helpers for the LSM-GNN gather path (sm_100a).
+//
+// Nothing here is shared with oracle/: the two implement the paper independently.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lsm {
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // empty cache way / "no victim slot"
+constexpr uint32_t kHostBit = 0x80000000u;  // FillEnt::src: bit 31 set => backing-table row q
+
+// Dynamic-information classes; index of evict_by_class[].
+enum Cls : int { kNoReuse = 0, kFar = 1, kFresh = 2, kNear = 3 };
+// Probe outcome per unique request.
+enum Kind : uint32_t { kStorage = 0, kHit = 1, kVHit = 2 };
+
+// Counter fields, in lsmgnn_stats_t order.
+enum Field : int {
+  F_ITER = 0, F_REQ, F_PEER, F_UNIQUE, F_HIT, F_VHIT, F_STOR, F_INS, F_BYP, F_EVICT,
+  F_EV0, F_EV1, F_EV2, F_EV3, F_VADM, F_VDROP, F_ENR, F_PREF, F_UNUSED,
+  F_BOUT, F_BNVL, F_BH2D, F_BPVP, F_BD2H, F_NFIELDS
+};
+
+// One row copy the fill kernel performs.
+struct FillEnt {
+  uint32_t src;     // kHostBit|q: backing-table row q; else a pool row (PVP staging)
+  uint32_t dst;     // pool row (cache slot or bypass staging)
+  uint32_t victim;  // host victim-queue row the OLD content of dst goes to first, or kInvalid
+  uint32_t pad;
+};
+// One victim-buffer candidate.
+struct Cand {
+  uint32_t x;      // evicted node
+  uint32_t reuse;  // its next reuse iteration
+  uint32_t fill;   // index of the FillEnt overwriting its slot
+  uint32_t pad;
+};
+
+// Per-batch scratch counters (u32, device).
+struct Scratch {
+  uint32_t nuniq;      // unique nodes at this home
+  uint32_t nfill;      // FillEnt entries
+  uint32_t ncand;      // victim candidates
+  uint32_t nbypass;    // bypass-staging rows used
+  uint32_t bad_ids;    // sticky count of node IDs >= N (ERANGE)
+  uint32_t nreq;       // requests routed to this home
+  uint32_t staged[2];  // rows the PVP staged, by iteration parity
+  uint32_t pvp_done;   // grid-completion counter of the PVP kernel
+  uint32_t pad[7];
+};
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+// Warp-aggregated atomicAdd of `inc` per lane: one atomic per warp. Must be called
+// by all 32 lanes (inactive lanes pass inc = 0). Returns this lane's base offset.
+__device__ __forceinline__ uint32_t warp_reserve(uint32_t* ctr, uint32_t inc) {
+  const uint32_t lane = lane_id();
+  uint32_t incl = inc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= (uint32_t)o) incl += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  uint32_t base = 0;
+  if (lane == 31 && total) base = atomicAdd(ctr, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + incl - inc;
+}
+
+// First set bit in [lo, hi) of a bitmask row; -1 if none.
+__device__ __forceinline__ int first_bit_in(const uint32_t* row, int lo, int hi) {
+  if (lo >= hi) return -1;
+  int w = lo >> 5, wl = (hi - 1) >> 5;
+  uint32_t bits = row[w] & (~0u << (lo & 31));
+  while (true) {
+    if (w == wl) {
+      int top = hi - (w << 5);  // 1..32 valid bits in this word
+      if (top < 32) bits &= (1u << top) - 1u;
+    }
+    if (bits) return (w << 5) + __ffs(bits) - 1;
+    if (++w > wl) return -1;
+    bits = row[w];
+  }
+}
+
+// Next reuse distance d in 1..W of a node from its window mask row, 0 = none.
+// Bit position of iteration k is k mod (W+1); at gather(t) the window is t+1..t+W
+// (PAPER.md P:352-354 window buffer; R5). p0 = (t+1) mod (W+1).
+__device__ __forceinline__ int next_reuse_d(const uint32_t* row, int p0, int W) {
+  const int Wp1 = W + 1;
+  int end1 = p0 + W < Wp1 ? p0 + W : Wp1;
+  int pos = first_bit_in(row, p0, end1);
+  if (pos >= 0) return pos - p0 + 1;
+  int end2 = p0 + W - Wp1;  // wrapped part [0, p0-1)
+  pos = first_bit_in(row, 0, end2);
+  if (pos >= 0) return (Wp1 - p0) + pos + 1;
+  return 0;
+}
+
+// 16-byte vector copies.
+// Device-memory rows are streamed (.nc, no L1 allocation, .cs stores); rows in host
+// memory mapped over PCIe use plain ld/st (cache-policy qualifiers are not valid on
+// the system address space).
+enum Mem : int { kDev = 0, kHost = 1 };
+template <int M>
+__device__ __forceinline__ uint4 ld16(const uint4* p) {
+  uint4 r;
+  if (M == kDev)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  else
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+  return r;
+}
+template <int M>
+__device__ __forceinline__ void st16(uint4* p, uint4 v) {
+  if (M == kDev)
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+  else
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// Warp copies one row of `nvec` 16-byte vectors, UNROLL vectors in flight per lane.
+template <int UNROLL, int SRC, int DST>
+__device__ __forceinline__ void warp_copy_row(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                              int nvec) {
+  const int lane = (int)lane_id();
+  int i = lane;
+  for (; i + 32 * (UNROLL - 1) < nvec; i += 32 * UNROLL) {
+    uint4 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) v[u] = ld16<SRC>(src + i + 32 * u);
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) st16<DST>(dst + i + 32 * u, v[u]);
+  }
+  for (; i < nvec; i += 32) st16<DST>(dst + i, ld16<SRC>(src + i));
+}
+
+template <typename T>
+__device__ __forceinline__ void warp_bitonic_sort(T* a, int P) {
+  const int lane = (int)lane_id();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < P; i += 32) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          bool up = (i & k) == 0;
+          T x = a[i], y = a[ixj];
+          if ((x > y) == up) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace lsm

@@ -1,0 +1,736 @@
+// kernels.cuh — sm_100a kernels of the LSM-GNN gather hot path.
+//
+// Step names follow SURVEY.md §8(a) (S1..S11) and DESIGN.md §"Kernels":
+//   k_route      S1   requester: validate IDs, bucket by home (v mod G), write home inboxes
+//   k_dedup      S3   home: unique nodes of the batch (node-indexed stamp table) + per-set counts
+//   k_scan       S3   home: exclusive scan of per-set counts; PVP "unused" accounting
+//   k_bucket     S3   home: scatter unique nodes into set buckets
+//   k_set        S4+S5 home: warp per touched set — tag probe, staging probe, bypass selection,
+//                     way assignment by the policy key, eviction classes, victim candidates
+//   k_qhist/k_qscatter/k_admit  S5  victim admission per queue (PVP)
+//   k_fill       S6   home: victim row D2H (old slot content) then new row -> slot / staging
+//   k_pull       S7+S8 requester: location lookup at the home + row copy into `out`
+//   k_begin/k_end S9  per-iteration counters
+//   k_mask_*     S10  window feed: reuse bitmask update
+//   k_pvp        S11  PVP copy of victim queue (t+1) mod W into home staging (side stream)
+#pragma once
+#include "device_common.cuh"
+
+namespace lsm {
+
+// ------------------------------------------------------------------------------ S9
+// Zero this iteration's record and the per-batch scratch counters.
+__global__ void k_begin(unsigned long long* rec, Scratch* scr, uint64_t t) {
+  const int i = threadIdx.x;
+  if (i < F_NFIELDS) rec[i] = 0;
+  __syncthreads();
+  if (i == 0) {
+    rec[F_ITER] = t;
+    rec[F_PREF] = scr->staged[t & 1];
+    scr->nuniq = 0;
+    scr->nfill = 0;
+    scr->ncand = 0;
+    scr->nbypass = 0;
+    scr->nreq = 0;
+  }
+}
+
+// Close the record: algorithmic bytes per tier, cumulative sums; the staging count of
+// the next parity is reset so that a missing PVP call stages nothing.
+__global__ void k_end(unsigned long long* rec, unsigned long long* cum, Scratch* scr, uint64_t t,
+                      uint32_t R) {
+  if (threadIdx.x != 0) return;
+  rec[F_UNIQUE] = scr->nuniq;
+  rec[F_REQ] = scr->nreq;
+  rec[F_BOUT] = rec[F_REQ] * R;
+  rec[F_BNVL] = rec[F_PEER] * R;
+  rec[F_BH2D] = rec[F_STOR] * R;
+  rec[F_BPVP] = rec[F_PREF] * R;
+  rec[F_BD2H] = rec[F_VADM] * R;
+  for (int f = 1; f < F_NFIELDS; ++f) cum[f] += rec[f];
+  cum[F_ITER] = t;
+  scr->staged[(t + 1) & 1] = 0;
+}
+
+// ------------------------------------------------------------------------------ S1 (G = 1)
+// Validate the caller's int64 IDs and write them (u32) into this home's inbox.
+__global__ void k_route_local(const int64_t* __restrict__ ids, int64_t n, uint64_t N,
+                              uint32_t* __restrict__ inbox, uint32_t* __restrict__ inbox_cnt,
+                              Scratch* scr) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool ok = false;
+    uint32_t v = 0;
+    if (i < n) {
+      const int64_t x = ids[i];
+      ok = x >= 0 && (uint64_t)x < N;
+      v = (uint32_t)x;
+      if (!ok) atomicAdd(&scr->bad_ids, 1u);
+    }
+    const uint32_t pos = warp_reserve(inbox_cnt, ok ? 1u : 0u);
+    if (ok) inbox[pos] = v;
+  }
+}
+
+// ------------------------------------------------------------------------------ S1 (G > 1)
+// Requester side of the communication layer: bucket each valid ID by its
+// home g = v mod G and store it straight into home g's inbox slot [me] through the
+// peer mapping. Counts go to route_cnt[g] (local) and are published by k_route_publish.
+struct RouteArgs {
+  uint32_t* inbox[8];  // inbox base of each home (peer-mapped), slot [me] already applied
+  uint32_t* route_cnt; // [G] local counters
+  uint32_t G;
+};
+__global__ void k_route_peer(const int64_t* __restrict__ ids, int64_t n, uint64_t N, RouteArgs a,
+                             Scratch* scr) {
+  __shared__ uint32_t s_cnt[8], s_base[8];
+  const int64_t tile = blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * tile; base < n; base += (int64_t)gridDim.x * tile) {
+    if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i = base + threadIdx.x;
+    bool ok = false;
+    uint32_t v = 0, g = 0, local = 0;
+    if (i < n) {
+      const int64_t x = ids[i];
+      ok = x >= 0 && (uint64_t)x < N;
+      if (!ok) atomicAdd(&scr->bad_ids, 1u);
+      v = (uint32_t)x;
+      g = v % a.G;
+      if (ok) local = atomicAdd(&s_cnt[g], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < a.G) s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(&a.route_cnt[threadIdx.x], s_cnt[threadIdx.x]) : 0;
+    __syncthreads();
+    if (ok) a.inbox[g][s_base[g] + local] = v;
+    __syncthreads();
+  }
+}
+// Publish this requester's per-home counts into every home's inbox header [me].
+struct PublishArgs {
+  uint32_t* peer_cnt[8];  // inbox_cnt array of each home (peer-mapped)
+  uint32_t G, me;
+};
+__global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
+  const uint32_t g = threadIdx.x;
+  if (g < a.G) {
+    a.peer_cnt[g][a.me] = route_cnt[g];
+    __threadfence_system();
+  }
+}
+
+// ------------------------------------------------------------------------------ S3
+// Home: one representative per distinct node (stamp table indexed by q = v / G),
+// appended to uniq[]; per-set counts for the bucket pass. Requests and peer requests
+// are counted here (every count but `requests` is over unique nodes, R11).
+__global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
+                        uint32_t nsrc, uint32_t cap, uint32_t me, uint32_t G, uint32_t S,
+                        uint32_t stamp, uint32_t* __restrict__ mark, uint32_t* __restrict__ uniq,
+                        uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* rec) {
+  uint32_t nreq = 0, npeer = 0;
+  for (uint32_t r = 0; r < nsrc; ++r) {
+    const uint32_t n = inbox_cnt[r];
+    const uint32_t* in = inbox + (size_t)r * cap;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+      const uint32_t i = base + threadIdx.x;
+      bool first = false;
+      uint32_t v = 0;
+      if (i < n) {
+        v = in[i];
+        const uint32_t q = v / G;
+        first = atomicExch(&mark[q], stamp) != stamp;
+        if (first) atomicAdd(&set_cnt[q % S], 1u);
+        ++nreq;
+        if (r != me) ++npeer;
+      }
+      const uint32_t pos = warp_reserve(&scr->nuniq, first ? 1u : 0u);
+      if (first) uniq[pos] = v;
+    }
+  }
+  nreq = __reduce_add_sync(0xffffffffu, nreq);
+  npeer = __reduce_add_sync(0xffffffffu, npeer);
+  if (lane_id() == 0) {
+    if (nreq) atomicAdd(&scr->nreq, nreq);
+    if (npeer) atomicAdd(&rec[F_PEER], (unsigned long long)npeer);
+  }
+}
+
+// Exclusive scan of set_cnt[0..S) into set_off[0..S] by one CTA (1024 threads).
+// The same CTA counts staged PVP rows that this batch did not request (pvp_unused).
+__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off,
+                                               uint32_t n, const uint32_t* __restrict__ stg_nodes,
+                                               const uint32_t* staged_count, const uint32_t* __restrict__ mark,
+                                               uint32_t stamp, uint32_t G, unsigned long long* rec) {
+  __shared__ uint32_t s_warp[32];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (n + 1023) / 1024;
+  const uint32_t lo = tid * per, hi = min(n, lo + per);
+  uint32_t sum = 0;
+  for (uint32_t i = lo; i < hi; ++i) sum += cnt[i];
+  // block exclusive scan of `sum`
+  uint32_t x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((tid & 31) >= (uint32_t)o) x += y;
+  }
+  if ((tid & 31) == 31) s_warp[tid >> 5] = x;
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t w = s_warp[tid];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (tid >= (uint32_t)o) w += y;
+    }
+    s_warp[tid] = w;
+  }
+  __syncthreads();
+  uint32_t run = x - sum + ((tid >> 5) ? s_warp[(tid >> 5) - 1] : 0);
+  for (uint32_t i = lo; i < hi; ++i) {
+    off[i] = run;
+    run += cnt[i];
+  }
+  if (tid == 1023) off[n] = run;
+  // pvp_unused: staged rows whose node this batch did not request
+  if (stg_nodes) {
+    const uint32_t ns = *staged_count;
+    uint32_t unused = 0;
+    for (uint32_t j = tid; j < ns; j += 1024) unused += mark[stg_nodes[j] / G] != stamp;
+    unused = __reduce_add_sync(0xffffffffu, unused);
+    if ((tid & 31) == 0 && unused) atomicAdd(&rec[F_UNUSED], (unsigned long long)unused);
+  }
+}
+
+// Scatter unique nodes into their set's bucket. set_cnt is decremented back to zero.
+__global__ void k_bucket(const uint32_t* __restrict__ uniq, const Scratch* scr, uint32_t G, uint32_t S,
+                         const uint32_t* __restrict__ off, uint32_t* __restrict__ set_cnt,
+                         uint32_t* __restrict__ bucket) {
+  const uint32_t n = scr->nuniq;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t v = uniq[i];
+    const uint32_t s = (v / G) % S;
+    const uint32_t pos = off[s] + atomicSub(&set_cnt[s], 1u) - 1u;
+    bucket[pos] = v;
+  }
+}
+
+// ------------------------------------------------------------------------------ S4 + S5
+struct SetParams {
+  const uint32_t* set_off;
+  const uint32_t* bucket;
+  uint32_t* tags;
+  uint32_t* last_use;
+  uint32_t* rr;
+  const uint8_t* score;
+  const uint32_t* mask;
+  uint32_t* node_loc;
+  const uint32_t* vst_stamp;
+  const uint32_t* vst_idx;
+  FillEnt* fills;
+  Cand* cands;
+  Scratch* scr;
+  unsigned long long* rec;
+  uint32_t S, A, G, W, T, MW;
+  uint32_t policy, pvp, reinsert;
+  uint32_t t, stamp, p0;
+  uint32_t P;            // per-warp capacity (power of two >= max bucket)
+  uint32_t warp_bytes;   // per-warp shared memory
+  uint32_t stage_base;   // pool row of this iteration's PVP staging buffer
+  uint32_t bypass_base;  // pool row of the bypass staging area
+};
+
+enum { C_HIT, C_VHIT, C_STOR, C_INS, C_BYP, C_EVICT, C_EV0, C_EV1, C_EV2, C_EV3, C_ENR, C_N };
+__device__ __constant__ int kCtrField[C_N] = {F_HIT, F_VHIT, F_STOR, F_INS, F_BYP, F_EVICT,
+                                              F_EV0, F_EV1, F_EV2, F_EV3, F_ENR};
+
+// Priority level of a class: NoReuse 0, Far 1, Fresh 2, Near 3; with PVP the
+// two lowest are swapped: Far 0, NoReuse 1.
+__device__ __forceinline__ uint64_t level_of(int cls, uint32_t pvp) {
+  if (cls == kNoReuse) return pvp ? 1 : 0;
+  if (cls == kFar) return pvp ? 0 : 1;
+  return (uint64_t)cls;  // Fresh 2, Near 3
+}
+__device__ __forceinline__ int class_of(int d, uint32_t T) {
+  return d == 0 ? kNoReuse : ((uint32_t)d <= T ? kNear : kFar);
+}
+// 64-bit eviction key, smallest evicted first; the node ID in the low 32 bits makes
+// every key unique (tie-break by node, R8).
+__device__ __forceinline__ uint64_t policy_key(const SetParams& p, uint32_t v, uint32_t lu, int d) {
+  switch (p.policy) {
+    case 0:  // HYBRID: (level, static score, node)
+      return (level_of(class_of(d, p.T), p.pvp) << 40) | ((uint64_t)p.score[v / p.G] << 32) | v;
+    case 1:  // STATIC: (score, node)
+      return ((uint64_t)p.score[v / p.G] << 32) | v;
+    case 2:  // LRU: (last use, node)
+      return ((uint64_t)lu << 32) | v;
+    case 4:  // DYNAMIC: no reuse first, then farthest reuse
+      return d == 0 ? (uint64_t)v : ((2ull << 48) | ((uint64_t)(p.W - d) << 32) | v);
+    default:  // RR: bypass order only
+      return v;
+  }
+}
+
+__global__ void k_set(SetParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long s_ctr[C_N];
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  if (threadIdx.x < C_N) s_ctr[threadIdx.x] = 0;
+  __syncthreads();
+
+  unsigned char* wbase = smem + (size_t)wib * p.warp_bytes;
+  uint32_t* sv = reinterpret_cast<uint32_t*>(wbase);  // sorted nodes of the set
+  uint32_t* sk = sv + p.P;                           // per node: kind | way<<2 | inM<<10 | byp<<11
+  uint32_t* sidx = sk + p.P;                         // M list, then insert list (indices into sv)
+  unsigned long long* skey = reinterpret_cast<unsigned long long*>(sidx + p.P);
+  uint32_t* stag = reinterpret_cast<uint32_t*>(skey + p.P);
+  uint32_t* svict = stag + 32;
+  int* sd = reinterpret_cast<int*>(svict + 32);
+
+  uint32_t ctr[C_N];
+#pragma unroll
+  for (int c = 0; c < C_N; ++c) ctr[c] = 0;
+  const uint32_t A = p.A, G = p.G;
+
+  for (uint32_t s = blockIdx.x * nwb + wib; s < p.S; s += gridDim.x * nwb) {
+    const uint32_t off = p.set_off[s];
+    const uint32_t m = p.set_off[s + 1] - off;
+    if (m == 0) continue;
+    uint32_t Pm = 32;
+    while (Pm < m) Pm <<= 1;
+    for (uint32_t j = lane; j < Pm; j += 32) sv[j] = j < m ? p.bucket[off + j] : kInvalid;
+    // resident lines of the set: lane w holds way w
+    uint32_t tg = kInvalid, lu = 0;
+    if (lane < A) {
+      tg = p.tags[s * A + lane];
+      lu = p.last_use[s * A + lane];
+    }
+    stag[lane] = tg;
+    int d = 0;  // next reuse distance of the resident node (0 = none in the window)
+    if (tg != kInvalid) d = next_reuse_d(p.mask + (size_t)(tg / G) * p.MW, p.p0, p.W);
+    sd[lane] = d;
+    __syncwarp();
+    warp_bitonic_sort(sv, (int)Pm);  // nodes ascending (R10: misses installed in node order)
+
+    // ---- probe (S4): tag compare, then the PVP staging directory
+    uint32_t protm = 0;
+    const uint32_t mr = (m + 31) & ~31u;
+    for (uint32_t j = lane; j < mr; j += 32) {
+      if (j < m) {
+        const uint32_t v = sv[j], q = v / G;
+        int way = -1;
+        for (uint32_t w = 0; w < A; ++w)
+          if (stag[w] == v) way = (int)w;
+        uint32_t kind, inM;
+        if (way >= 0) {
+          kind = kHit;
+          protm |= 1u << way;
+          p.node_loc[q] = s * A + (uint32_t)way;
+          ++ctr[C_HIT];
+        } else if (p.vst_stamp[q] == p.stamp) {
+          kind = kVHit;
+          ++ctr[C_VHIT];
+        } else {
+          kind = kStorage;
+          ++ctr[C_STOR];
+        }
+        inM = kind != kHit && (kind == kStorage || p.reinsert);
+        sk[j] = kind | ((uint32_t)(way & 0xff) << 2) | (inM << 10);
+      }
+    }
+    protm = __reduce_or_sync(0xffffffffu, protm);
+    __syncwarp();
+    const uint32_t nH = __popc(protm);
+    if ((protm >> lane) & 1u) p.last_use[s * A + lane] = p.t;  // hits are protected, last use = t
+
+    // ---- M = misses to insert, ascending node order
+    uint32_t nM = 0;
+    for (uint32_t j0 = 0; j0 < mr; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const bool f = j < m && ((sk[j] >> 10) & 1u);
+      const uint32_t b = __ballot_sync(0xffffffffu, f);
+      if (f) sidx[nM + __popc(b & ((1u << lane) - 1u))] = j;
+      nM += __popc(b);
+    }
+    __syncwarp();
+    const uint32_t avail = A - nH;
+    const uint32_t nbyp = nM > avail ? nM - avail : 0;
+    if (nbyp) {
+      // more misses than unprotected ways: bypass the nbyp smallest incoming keys (R10)
+      uint32_t PM = 32;
+      while (PM < nM) PM <<= 1;
+      for (uint32_t k = lane; k < PM; k += 32) {
+        unsigned long long key = ~0ull;
+        if (k < nM) {
+          const uint32_t v = sv[sidx[k]];
+          const int dv = (p.policy == 0 || p.policy == 4)
+                             ? next_reuse_d(p.mask + (size_t)(v / G) * p.MW, p.p0, p.W) : 0;
+          key = policy_key(p, v, p.t, dv);
+        }
+        skey[k] = key;
+      }
+      __syncwarp();
+      warp_bitonic_sort(skey, (int)PM);
+      for (uint32_t k = lane; k < nbyp; k += 32) {
+        const uint32_t v = (uint32_t)skey[k];
+        uint32_t lo = 0, hi = m;  // lower_bound in sv
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (sv[mid] < v) lo = mid + 1; else hi = mid;
+        }
+        sk[lo] |= 1u << 11;
+      }
+      __syncwarp();
+      // drop bypassed entries from the insert list (stable, in place)
+      uint32_t nI = 0;
+      const uint32_t nMr = (nM + 31) & ~31u;
+      for (uint32_t k0 = 0; k0 < nMr; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        uint32_t j = 0;
+        bool keep = false;
+        if (k < nM) {
+          j = sidx[k];
+          keep = !((sk[j] >> 11) & 1u);
+        }
+        const uint32_t b = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) sidx[nI + __popc(b & ((1u << lane) - 1u))] = j;
+        nI += __popc(b);
+        __syncwarp();
+      }
+      ctr[C_BYP] += lane == 0 ? nbyp : 0;
+    }
+    const uint32_t nI = nM - nbyp;
+
+    // ---- way assignment (S5): free ways first (ascending), then victims by policy key
+    const bool cand = lane < A && tg != kInvalid && !((protm >> lane) & 1u);
+    const uint32_t freem = __ballot_sync(0xffffffffu, lane < A && tg == kInvalid);
+    const uint32_t candm = __ballot_sync(0xffffffffu, cand);
+    const uint32_t nF = __popc(freem);
+    const uint32_t e = nI > nF ? nI - nF : 0;
+    if (e) {
+      uint32_t rank;
+      if (p.policy == 3) {  // RR: candidates in cyclic order from the cursor
+        const uint32_t c0 = p.rr[s];
+        const uint32_t pos = (lane + A - c0) % A;
+        uint32_t before = 0;
+        for (uint32_t w = 0; w < A; ++w)
+          if (((candm >> w) & 1u) && ((w + A - c0) % A) < pos) ++before;
+        rank = before;
+      } else {
+        const unsigned long long key = cand ? policy_key(p, tg, lu, d) : ~0ull;
+        rank = 0;
+        for (int w = 0; w < 32; ++w) {
+          const unsigned long long kw = __shfl_sync(0xffffffffu, key, w);
+          if (((candm >> w) & 1u) && kw < key) ++rank;
+        }
+      }
+      if (cand && rank < e) svict[rank] = lane;
+      __syncwarp();
+      if (p.policy == 3 && lane == 0) p.rr[s] = (svict[e - 1] + 1) % A;
+    }
+    __syncwarp();
+
+    // ---- install the kept misses; evicted lines become victim candidates
+    const uint32_t nIr = (nI + 31) & ~31u;
+    for (uint32_t k0 = 0; k0 < nIr; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const bool act = k < nI;
+      uint32_t v = 0, q = 0, way = 0, kind = 0, x = kInvalid;
+      if (act) {
+        const uint32_t j = sidx[k];
+        v = sv[j];
+        q = v / G;
+        kind = sk[j] & 3u;
+        if (k < nF) {
+          uint32_t fm = freem;
+          for (uint32_t z = 0; z < k; ++z) fm &= fm - 1u;  // k-th free way
+          way = __ffs(fm) - 1;
+        } else {
+          way = svict[k - nF];
+        }
+        x = stag[way];
+      }
+      bool is_cand = false;
+      uint32_t reuse = 0;
+      if (act && x != kInvalid) {
+        const int dx = sd[way];
+        ++ctr[C_EVICT];
+        ++ctr[C_EV0 + class_of(dx, p.T)];
+        if (p.pvp && dx) {
+          is_cand = true;
+          reuse = p.t + (uint32_t)dx;
+        } else {
+          ++ctr[C_ENR];
+        }
+      }
+      const uint32_t fidx = warp_reserve(&p.scr->nfill, act ? 1u : 0u);
+      const uint32_t cidx = warp_reserve(&p.scr->ncand, is_cand ? 1u : 0u);
+      if (act) {
+        const uint32_t slot = s * A + way;
+        FillEnt f;
+        f.src = kind == kVHit ? p.stage_base + p.vst_idx[q] : (kHostBit | q);
+        f.dst = slot;
+        f.victim = kInvalid;
+        f.pad = 0;
+        p.fills[fidx] = f;
+        p.node_loc[q] = slot;
+        p.tags[slot] = v;
+        p.last_use[slot] = p.t;
+        ++ctr[C_INS];
+        if (is_cand) {
+          Cand c;
+          c.x = x;
+          c.reuse = reuse;
+          c.fill = fidx;
+          c.pad = 0;
+          p.cands[cidx] = c;
+        }
+      }
+    }
+
+    // ---- rows not installed: bypassed storage misses go to bypass staging; victim-buffer
+    // hits not installed are served from the PVP staging buffer
+    for (uint32_t j0 = 0; j0 < mr; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      bool bs = false;
+      uint32_t v = 0;
+      if (j < m) {
+        const uint32_t info = sk[j];
+        const uint32_t kind = info & 3u;
+        const bool inM = (info >> 10) & 1u, byp = (info >> 11) & 1u;
+        v = sv[j];
+        if (kind == kVHit && (!inM || byp)) p.node_loc[v / G] = p.stage_base + p.vst_idx[v / G];
+        bs = kind == kStorage && byp;
+      }
+      const uint32_t b = warp_reserve(&p.scr->nbypass, bs ? 1u : 0u);
+      const uint32_t fidx = warp_reserve(&p.scr->nfill, bs ? 1u : 0u);
+      if (bs) {
+        FillEnt f;
+        f.src = kHostBit | (v / G);
+        f.dst = p.bypass_base + b;
+        f.victim = kInvalid;
+        f.pad = 0;
+        p.fills[fidx] = f;
+        p.node_loc[v / G] = p.bypass_base + b;
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---- counters: warp -> CTA -> global
+#pragma unroll
+  for (int c = 0; c < C_N; ++c) {
+    const uint32_t x = __reduce_add_sync(0xffffffffu, ctr[c]);
+    if (lane == 0 && x) atomicAdd(&s_ctr[c], (unsigned long long)x);
+  }
+  __syncthreads();
+  if (threadIdx.x < C_N && s_ctr[threadIdx.x]) atomicAdd(&p.rec[kCtrField[threadIdx.x]], s_ctr[threadIdx.x]);
+}
+
+// ------------------------------------------------------------------------------ S5: admission
+// Histogram of victim candidates per queue k = reuse mod W ("fourth victim buffer").
+__global__ void k_qhist(const Cand* __restrict__ cands, const Scratch* scr, uint32_t W,
+                        uint32_t* __restrict__ qcnt) {
+  const uint32_t n = scr->ncand;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAdd(&qcnt[cands[i].reuse % W], 1u);
+}
+__global__ void k_qscatter(const Cand* __restrict__ cands, const Scratch* scr, uint32_t W,
+                           const uint32_t* __restrict__ qoff, uint32_t* __restrict__ qcnt,
+                           uint32_t* __restrict__ qb) {
+  const uint32_t n = scr->ncand;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t k = cands[i].reuse % W;
+    qb[qoff[k] + atomicSub(&qcnt[k], 1u) - 1u] = i;
+  }
+}
+// One CTA per queue: admit the candidates with the smallest node IDs into the free slots
+// (R14), slot = queue counter before the increment. Admitted rows are copied to
+// the pinned host queue by k_fill before their slot is overwritten.
+__global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, const uint32_t* __restrict__ qoff,
+                                               const uint32_t* __restrict__ qb, uint32_t* __restrict__ qlen,
+                                               uint32_t* __restrict__ qnode, uint32_t* __restrict__ qreuse,
+                                               FillEnt* __restrict__ fills, uint32_t C, unsigned long long* rec) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_prefix, s_want, s_taken;
+  const uint32_t k = blockIdx.x;
+  const uint32_t lo = qoff[k], nk = qoff[k + 1] - lo;
+  if (nk == 0) return;
+  const uint32_t len0 = qlen[k];
+  const uint32_t room = len0 < C ? C - len0 : 0;
+  uint32_t thresh = 0xFFFFFFFFu;  // admit x <= thresh
+  bool none = room == 0;
+  if (!none && nk > room) {
+    // radix select: the room-th smallest node ID (IDs of one batch's victims are distinct)
+    if (threadIdx.x == 0) {
+      s_prefix = 0;
+      s_want = room;
+    }
+    uint32_t pmask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      const uint32_t prefix = s_prefix;
+      for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) {
+        const uint32_t x = cands[qb[lo + i]].x;
+        if ((x & pmask) == prefix) atomicAdd(&hist[(x >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t want = s_want, dd = 0;
+        for (; dd < 256; ++dd) {
+          if (hist[dd] >= want) break;
+          want -= hist[dd];
+        }
+        s_want = want;
+        s_prefix = prefix | (dd << shift);
+      }
+      pmask |= 255u << shift;
+      __syncthreads();
+    }
+    thresh = s_prefix;
+  }
+  if (threadIdx.x == 0) s_taken = 0;
+  __syncthreads();
+  uint32_t adm = 0;
+  for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) {
+    const Cand c = cands[qb[lo + i]];
+    if (!none && c.x <= thresh) {
+      const uint32_t slot = len0 + atomicAdd(&s_taken, 1u);
+      qnode[(size_t)k * C + slot] = c.x;
+      qreuse[(size_t)k * C + slot] = c.reuse;
+      fills[c.fill].victim = k * C + slot;
+      ++adm;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    qlen[k] = len0 + s_taken;
+    atomicAdd(&rec[F_VADM], (unsigned long long)s_taken);
+    atomicAdd(&rec[F_VDROP], (unsigned long long)(nk - s_taken));
+  }
+  (void)adm;
+}
+
+// ------------------------------------------------------------------------------ S6
+// Warp per fill entry: first the victim row (old slot content) to the pinned host queue
+// (eviction D2H), then the new row from the backing table (zero-copy over PCIe,
+// P:249 "directly fetched by GPU threads") or from PVP staging into the slot.
+template <int UNROLL>
+__global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
+                       const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec) {
+  const uint32_t n = scr->nfill;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t e = warp; e < n; e += nwarps) {
+    const FillEnt f = fills[e];
+    uint4* dst = pool + (size_t)f.dst * nvec;
+    if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, dst, nvec);
+    if (f.src & kHostBit)
+      warp_copy_row<UNROLL, kHost, kDev>(dst, table + (size_t)(f.src & ~kHostBit) * nvec, nvec);
+    else
+      warp_copy_row<UNROLL, kDev, kDev>(dst, pool + (size_t)f.src * nvec, nvec);
+  }
+}
+
+// ------------------------------------------------------------------------------ S7 + S8
+// Requester: out[i] = row of ids[i] at its home. The location (cache slot, staging row)
+// is looked up in the home's node_loc table (peer-mapped when home != me) — the
+// "respond" step as a one-sided read — and the row is copied with 16-byte vectors.
+struct PullArgs {
+  const uint4* pool[8];
+  const uint32_t* node_loc[8];
+  uint32_t G;
+};
+template <int UNROLL>
+__global__ void k_pull(const int64_t* __restrict__ ids, int64_t n, uint64_t N, PullArgs a,
+                       uint4* __restrict__ out, uint32_t nvec) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const int64_t x = ids[i];
+    uint4* dst = out + (size_t)i * nvec;
+    if (x < 0 || (uint64_t)x >= N) {  // ERANGE: zero-filled row
+      for (uint32_t k = lane_id(); k < nvec; k += 32) dst[k] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint32_t v = (uint32_t)x, g = v % a.G, q = v / a.G;
+    const uint32_t loc = a.node_loc[g][q];
+    warp_copy_row<UNROLL, kDev, kDev>(dst, a.pool[g] + (size_t)loc * nvec, nvec);
+  }
+}
+
+// ------------------------------------------------------------------------------ S10
+// Window feed. Bit (k mod (W+1)) of mask[q] is set when node q*G+me is in B_k.
+// k_mask_clear drops iteration k's bits (the list stored in its ring slot); k_win_store
+// stores the new batch (u32) into the slot and sets its bits.
+__global__ void k_mask_clear(const uint32_t* __restrict__ list, const uint32_t* len, uint32_t G,
+                             uint32_t MW, uint32_t bit, uint32_t* __restrict__ mask) {
+  const uint32_t n = *len;
+  const uint32_t m = ~(1u << (bit & 31));
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicAnd(&mask[(size_t)(list[i] / G) * MW + (bit >> 5)], m);
+}
+__global__ void k_mask_set(const uint32_t* __restrict__ list, const uint32_t* len, uint32_t G,
+                           uint32_t MW, uint32_t bit, uint32_t* __restrict__ mask) {
+  const uint32_t n = *len;
+  const uint32_t m = 1u << (bit & 31);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    atomicOr(&mask[(size_t)(list[i] / G) * MW + (bit >> 5)], m);
+}
+// Copy the inboxes of all sources (window IDs routed to this home) into one ring slot.
+__global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
+                             uint32_t nsrc, uint32_t cap, uint32_t* __restrict__ slot, uint32_t* slot_len) {
+  uint32_t base = 0;
+  for (uint32_t r = 0; r < nsrc; ++r) {
+    const uint32_t n = inbox_cnt[r];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+      slot[base + i] = inbox[(size_t)r * cap + i];
+    base += n;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *slot_len = base;
+}
+
+// ------------------------------------------------------------------------------ S11
+// PVP: copy victim queue k = (t+1) mod W (pinned host) into this iteration's
+// staging buffer and publish the staging directory (vst_stamp/vst_idx) for gather(t+1).
+// Entries whose recorded reuse is not t+1 are dropped (R17). The last CTA empties the queue.
+template <int UNROLL>
+__global__ void k_pvp(uint32_t k, uint32_t t1, uint32_t stamp1, uint32_t C, uint32_t G,
+                      uint32_t* __restrict__ qlen, const uint32_t* __restrict__ qnode,
+                      const uint32_t* __restrict__ qreuse, const uint4* __restrict__ hostq,
+                      uint4* __restrict__ pool, uint32_t stage_base, uint32_t* __restrict__ stg_nodes,
+                      uint32_t* __restrict__ vst_stamp, uint32_t* __restrict__ vst_idx, Scratch* scr,
+                      uint32_t par, uint32_t nvec) {
+  const uint32_t n = qlen[k];
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t j = warp; j < n; j += nwarps) {
+    const size_t e = (size_t)k * C + j;
+    if (qreuse[e] != t1) continue;
+    uint32_t m = 0;
+    if (lane_id() == 0) m = atomicAdd(&scr->staged[par], 1u);
+    m = __shfl_sync(0xffffffffu, m, 0);
+    const uint32_t x = qnode[e];
+    warp_copy_row<UNROLL, kHost, kDev>(pool + (size_t)(stage_base + m) * nvec, hostq + e * nvec, nvec);
+    if (lane_id() == 0) {
+      stg_nodes[m] = x;
+      vst_idx[x / G] = m;
+      vst_stamp[x / G] = stamp1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&scr->pvp_done, 1u) == gridDim.x - 1) {
+      qlen[k] = 0;
+      scr->pvp_done = 0;
+    }
+  }
+}
+
+}  // namespace lsm

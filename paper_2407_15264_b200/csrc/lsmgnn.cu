@@ -1,0 +1,737 @@
+// lsmgnn.cu — host runtime + C-ABI of the B200-native LSM-GNN gather hot path.
+//
+// Declared in include/lsmgnn.h (argument meaning, layout, ownership, errors).
+// DESIGN.md §"Data layout" and §"Kernels" describe what lives where; kernels.cuh holds
+// the sm_100a kernels. One process per GPU; peers are reached through CUDA IPC
+// mappings (NVLink P2P on a real 8-GPU box) and stream-ordered 32-bit flags written
+// and awaited with cuStreamWriteValue32 / cuStreamWaitValue32 (no SM spins, no host
+// synchronisation in steady state).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lsmgnn.h"
+#include "kernels.cuh"
+
+using namespace lsm;
+
+namespace {
+
+constexpr int kMaxG = 8;
+constexpr int64_t kHist = 4096;  // per-iteration records kept on the device
+
+struct Handle {  // exported per rank for lsmgnn_connect
+  cudaIpcMemHandle_t ipc;
+  uint64_t arena_bytes;
+  uint64_t layout_sig;
+  int32_t rank, world;
+};
+
+struct Ctx {
+  // binding
+  int rank = 0, world = 1, device = -1;
+  lsmgnn_options opt{};
+  bool opt_set = false;
+  bool inited = false, connected = false;
+  std::string err;
+  int sticky = 0;
+
+  // config
+  uint64_t N = 0;
+  uint32_t R = 0, nvec = 0, A = 0, W = 0, T = 0, MW = 0, Wp1 = 0;
+  uint64_t L = 0, S = 0, Q = 0, C = 0, cap = 0, ucap = 0, bcap = 0;
+  uint64_t pool_rows = 0, stage_base0 = 0, bypass_base = 0;
+  uint32_t P = 32, warp_bytes = 0, set_warps = 8;
+  int sms = 148;
+
+  // shared arena (exported to peers): [flags | inbox_cnt | win_cnt | inbox | win_inbox | node_loc | pool]
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  size_t off_flags = 0, off_icnt = 0, off_wcnt = 0, off_inbox = 0, off_win = 0, off_loc = 0, off_pool = 0;
+  char* peer_arena[kMaxG] = {};
+
+  // local device state
+  uint32_t *tags = nullptr, *last_use = nullptr, *rr = nullptr, *mask = nullptr, *mark = nullptr;
+  uint32_t *vst_stamp = nullptr, *vst_idx = nullptr, *set_cnt = nullptr, *set_off = nullptr;
+  uint32_t *bucket = nullptr, *uniq = nullptr, *ring = nullptr, *ring_len = nullptr;
+  uint32_t *qcnt = nullptr, *qoff = nullptr, *qb = nullptr, *qlen = nullptr, *qnode = nullptr;
+  uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr, *local_inbox_cnt = nullptr;
+  uint8_t* score = nullptr;
+  FillEnt* fills = nullptr;
+  Cand* cands = nullptr;
+  Scratch* scr = nullptr;
+  unsigned long long *hist = nullptr, *cum = nullptr;
+
+  // host tiers
+  uint8_t* qrows_host = nullptr;  // pinned victim queues [W*C][R]
+  uint8_t* qrows_dev = nullptr;   // its device mapping
+  const uint8_t* table_host = nullptr;
+  const uint8_t* table_dev = nullptr;
+  bool table_registered = false;
+  volatile uint32_t* bad_host = nullptr;  // pinned mirror of scr->bad_ids
+  uint32_t* bad_dev = nullptr;
+
+  // streams / events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
+  bool pvp_pending = false;
+  cudaStream_t last_stream = nullptr;
+  int64_t* tmp_ids = nullptr;  // for lsmgnn_gather_host
+  void* tmp_out = nullptr;
+
+  // iteration state
+  int64_t t_next = 0;      // next gather iteration
+  int64_t feed_next = 1;   // next window iteration to feed
+  uint32_t win_seq = 0;    // window batches exchanged (G > 1)
+  int64_t launches = 0;
+
+  // driver entry points (stream memory operations)
+  PFN_cuStreamWaitValue32_v2 waitv = nullptr;
+  PFN_cuStreamWriteValue32_v2 writev = nullptr;
+};
+
+Ctx g;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g.err = buf;
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(e_ == cudaErrorMemoryAllocation ? LSMGNN_ENOMEM : LSMGNN_ECUDA,     \
+                     "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                     __LINE__);                                                         \
+  } while (0)
+
+#define LAUNCHED()                                                                  \
+  do {                                                                              \
+    ++g.launches;                                                                   \
+    cudaError_t e_ = cudaPeekAtLastError();                                         \
+    if (e_ != cudaSuccess)                                                          \
+      return set_err(LSMGNN_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                           \
+  } while (0)
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+  CK(cudaMemset(*p, 0, count * sizeof(T)));
+  return 0;
+}
+
+// arena views (local or peer)
+uint32_t* flags_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_flags); }
+// flag slots: [0,G) route from r; [G,2G) served by home g; [2G,3G) window from r; [3G,4G) window ack from g
+uint32_t* icnt_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_icnt); }
+uint32_t* wcnt_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_wcnt); }
+uint32_t* inbox_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_inbox); }
+uint32_t* win_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_win); }
+uint32_t* loc_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_loc); }
+uint8_t* pool_of(char* base) { return reinterpret_cast<uint8_t*>(base + g.off_pool); }
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int grid_for(int64_t work, int threads, int per_sm = 8) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)std::min<int64_t>(b, (int64_t)g.sms * per_sm);
+}
+
+int check_sticky() {
+  if (g.bad_host && *g.bad_host) g.sticky = LSMGNN_ERANGE;
+  if (g.sticky) return set_err(g.sticky, "a node id >= num_nodes was passed (sticky)");
+  return 0;
+}
+
+// ---- stream-ordered flags (G > 1)
+int flag_write(cudaStream_t st, uint32_t* addr, uint32_t value) {
+  CUresult r = g.writev(st, (CUdeviceptr)addr, value, 0);
+  if (r != CUDA_SUCCESS) return set_err(LSMGNN_ECOMM, "cuStreamWriteValue32 failed (%d)", (int)r);
+  return 0;
+}
+int flag_wait(cudaStream_t st, uint32_t* addr, uint32_t value) {
+  CUresult r = g.waitv(st, (CUdeviceptr)addr, value, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return set_err(LSMGNN_ECOMM, "cuStreamWaitValue32 failed (%d)", (int)r);
+  return 0;
+}
+
+// Route `n` int64 IDs of this requester to the homes' inboxes (gather: win=false) and run the
+// flag exchange so that, on return (stream order), every home's inbox for this round is full.
+int exchange_ids(const int64_t* ids, int64_t n, bool win, uint32_t seq, cudaStream_t st) {
+  const int G = g.world;
+  uint32_t* myflags = flags_of(g.arena);
+  if (win) {  // the homes must have consumed the previous window round
+    for (int h = 0; h < G; ++h)
+      if (int rc = flag_wait(st, &myflags[3 * G + h], seq - 1)) return rc;
+  }
+  CK(cudaMemsetAsync(g.route_cnt, 0, sizeof(uint32_t) * G, st));
+  RouteArgs ra{};
+  PublishArgs pa{};
+  for (int h = 0; h < G; ++h) {
+    char* base = g.peer_arena[h];
+    ra.inbox[h] = (win ? win_of(base) : inbox_of(base)) + (size_t)g.rank * g.cap;
+    pa.peer_cnt[h] = win ? wcnt_of(base) : icnt_of(base);
+  }
+  ra.route_cnt = g.route_cnt;
+  ra.G = (uint32_t)G;
+  pa.G = (uint32_t)G;
+  pa.me = (uint32_t)g.rank;
+  if (n > 0) {
+    k_route_peer<<<grid_for(n, 256, 4), 256, 0, st>>>(ids, n, g.N, ra, g.scr);
+    LAUNCHED();
+  }
+  k_route_publish<<<1, 32, 0, st>>>(g.route_cnt, pa);
+  LAUNCHED();
+  const int slot = win ? 2 : 0;
+  for (int h = 0; h < G; ++h)
+    if (int rc = flag_write(st, &flags_of(g.peer_arena[h])[slot * G + g.rank], seq)) return rc;
+  for (int r = 0; r < G; ++r)
+    if (int rc = flag_wait(st, &myflags[slot * G + r], seq)) return rc;
+  return 0;
+}
+
+int free_all() {
+  cudaDeviceSynchronize();
+  void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off,
+                  g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
+                  g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.score, g.fills, g.cands, g.scr, g.hist,
+                  g.cum, g.arena, g.tmp_ids, g.tmp_out};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (int h = 0; h < kMaxG; ++h)
+    if (g.peer_arena[h] && g.peer_arena[h] != g.arena) cudaIpcCloseMemHandle(g.peer_arena[h]);
+  if (g.qrows_host) cudaFreeHost(g.qrows_host);
+  if (g.bad_host) cudaFreeHost((void*)g.bad_host);
+  if (g.table_registered) cudaHostUnregister((void*)g.table_host);
+  if (g.side) cudaStreamDestroy(g.side);
+  if (g.ev_main) cudaEventDestroy(g.ev_main);
+  if (g.ev_pvp) cudaEventDestroy(g.ev_pvp);
+  const int rank = g.rank, world = g.world, dev = g.device;
+  const lsmgnn_options opt = g.opt;
+  const bool opt_set = g.opt_set;
+  g = Ctx();
+  g.rank = rank;
+  g.world = world;
+  g.device = dev;
+  g.opt = opt;
+  g.opt_set = opt_set;
+  return 0;
+}
+
+lsmgnn_options default_options() {
+  lsmgnn_options o{};
+  o.version = LSMGNN_ABI_VERSION;
+  o.policy = LSMGNN_HYBRID;
+  o.pvp = 0;
+  o.window = 256;
+  o.threshold = 0;
+  o.update_period = 1;
+  o.reinsert_victims = 1;
+  o.max_batch_ids = 1 << 20;
+  return o;
+}
+
+}  // namespace
+
+// ====================================================================================== C-ABI
+extern "C" {
+
+const char* lsmgnn_last_error(void) { return g.err.c_str(); }
+int64_t lsmgnn_kernel_launches(void) { return g.launches; }
+size_t lsmgnn_handle_bytes(void) { return sizeof(Handle); }
+
+int lsmgnn_bind(int32_t rank, int32_t world, int32_t device) {
+  if (g.inited) return set_err(LSMGNN_ESTATE, "bind after init");
+  if (world < 1 || world > kMaxG || rank < 0 || rank >= world)
+    return set_err(LSMGNN_EINVAL, "bad rank/world (%d/%d); world must be 1..%d", rank, world, kMaxG);
+  g.rank = rank;
+  g.world = world;
+  g.device = device;
+  return 0;
+}
+
+int lsmgnn_set_options(const lsmgnn_options* opt) {
+  if (g.inited) return set_err(LSMGNN_ESTATE, "set_options after init");
+  if (!opt || opt->version != LSMGNN_ABI_VERSION) return set_err(LSMGNN_EINVAL, "bad options/version");
+  if (opt->policy < 0 || opt->policy > 4) return set_err(LSMGNN_EINVAL, "bad policy");
+  if (opt->window < 1 || opt->window > 65534) return set_err(LSMGNN_EINVAL, "window must be 1..65534");
+  if (opt->threshold < 0 || opt->threshold > opt->window) return set_err(LSMGNN_EINVAL, "bad threshold");
+  if (opt->update_period != 1 && opt->update_period != 0)
+    return set_err(LSMGNN_EINVAL, "only update_period = 1 is implemented (DESIGN.md R6)");
+  if (opt->max_batch_ids < 1 || opt->max_batch_ids > (1ll << 30)) return set_err(LSMGNN_EINVAL, "bad max_batch_ids");
+  g.opt = *opt;
+  g.opt_set = true;
+  return 0;
+}
+
+int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t lines_per_gpu, int32_t ways,
+                int64_t victim_lines, const uint8_t* static_scores) {
+  if (g.inited) return set_err(LSMGNN_ESTATE, "already initialised");
+  if (!g.opt_set) g.opt = default_options();
+  const int esz = dtype == LSMGNN_F32 ? 4 : (dtype == LSMGNN_F16 || dtype == LSMGNN_BF16) ? 2 : 0;
+  if (esz == 0) return set_err(LSMGNN_EINVAL, "bad dtype");
+  if (num_nodes < 1 || num_nodes > 0xFFFFFFF0ll) return set_err(LSMGNN_EINVAL, "num_nodes must be 1..2^32-16");
+  if (feat_dim < 1) return set_err(LSMGNN_EINVAL, "bad feat_dim");
+  const int64_t R = (int64_t)feat_dim * esz;
+  if (R % 16) return set_err(LSMGNN_EINVAL, "row bytes %lld not a multiple of 16 (DESIGN.md R22)", (long long)R);
+  if (ways < 1 || ways > 32) return set_err(LSMGNN_EINVAL, "ways must be 1..32");
+  if (lines_per_gpu < ways || lines_per_gpu % ways) return set_err(LSMGNN_EINVAL, "lines_per_gpu must be a positive multiple of ways");
+  if (lines_per_gpu >= (1ll << 31)) return set_err(LSMGNN_EINVAL, "lines_per_gpu too large");
+  if (g.device < 0) CK(cudaGetDevice(&g.device));
+  CK(cudaSetDevice(g.device));
+  CK(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, g.device));
+
+  const int G = g.world;
+  g.N = (uint64_t)num_nodes;
+  g.R = (uint32_t)R;
+  g.nvec = (uint32_t)(R / 16);
+  g.A = (uint32_t)ways;
+  g.L = (uint64_t)lines_per_gpu;
+  g.S = g.L / g.A;
+  g.Q = (g.N + G - 1) / G;
+  g.W = (uint32_t)g.opt.window;
+  g.Wp1 = g.W + 1;
+  g.T = g.opt.threshold ? (uint32_t)g.opt.threshold : std::max<uint32_t>(1, g.W / 8);
+  g.MW = (g.Wp1 + 31) / 32;
+  g.C = g.opt.pvp ? (uint64_t)victim_lines / g.W : 0;
+  if (g.opt.pvp && g.C < 1) return set_err(LSMGNN_EINVAL, "pvp needs victim_lines >= window");
+  g.cap = (uint64_t)g.opt.max_batch_ids;
+  g.ucap = std::min<uint64_t>(g.cap * G, g.Q);  // unique nodes per batch at a home
+  g.bcap = g.ucap;                              // bypass staging rows
+  g.stage_base0 = g.L;
+  g.bypass_base = g.L + 2 * g.C;
+  g.pool_rows = g.L + 2 * g.C + g.bcap;
+  if (g.pool_rows >= (uint64_t)kHostBit) return set_err(LSMGNN_EINVAL, "pool too large for 31-bit rows");
+  // k_set per-warp shared memory: the largest possible bucket of one set
+  const uint64_t maxm = std::min<uint64_t>((g.Q + g.S - 1) / g.S, g.ucap);
+  g.P = 32;
+  while (g.P < maxm) g.P <<= 1;
+  g.warp_bytes = (uint32_t)align_up(20ull * g.P + 3 * 32 * 4, 16);
+  g.set_warps = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(8, (160 * 1024) / g.warp_bytes));
+  if ((uint64_t)g.warp_bytes * g.set_warps > 200 * 1024)
+    return set_err(LSMGNN_EINVAL, "a cache set can receive %llu distinct nodes per batch; use more sets",
+                   (unsigned long long)maxm);
+
+  // ---- shared arena
+  size_t o = 0;
+  g.off_flags = o; o = align_up(o + 4 * G * sizeof(uint32_t), 256);
+  g.off_icnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
+  g.off_wcnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
+  g.off_inbox = o; o = align_up(o + (size_t)G * g.cap * sizeof(uint32_t), 256);
+  g.off_win = o;   o = align_up(o + (G > 1 ? (size_t)G * g.cap * sizeof(uint32_t) : 0), 256);
+  g.off_loc = o;   o = align_up(o + g.Q * sizeof(uint32_t), 4096);
+  g.off_pool = o;  o = align_up(o + g.pool_rows * (size_t)g.R, 4096);
+  g.arena_bytes = o;
+  CK(cudaMalloc(&g.arena, g.arena_bytes));
+  CK(cudaMemset(g.arena, 0, g.off_pool));
+  for (int h = 0; h < kMaxG; ++h) g.peer_arena[h] = nullptr;
+  g.peer_arena[g.rank] = g.arena;
+
+  int rc = 0;
+#define DA(p, n) if ((rc = dalloc(&(p), (n)))) return rc
+  DA(g.tags, g.L);
+  CK(cudaMemset(g.tags, 0xFF, g.L * sizeof(uint32_t)));
+  DA(g.last_use, g.L);
+  DA(g.rr, g.S);
+  DA(g.mask, g.Q * g.MW);
+  DA(g.mark, g.Q);
+  DA(g.vst_stamp, g.Q);
+  DA(g.vst_idx, g.Q);
+  DA(g.set_cnt, g.S);
+  DA(g.set_off, g.S + 1);
+  DA(g.bucket, g.ucap);
+  DA(g.uniq, g.ucap);
+  DA(g.ring, (size_t)g.Wp1 * g.cap * G);
+  DA(g.ring_len, g.Wp1);
+  DA(g.qcnt, g.W);
+  DA(g.qoff, g.W + 1);
+  DA(g.qb, g.ucap);
+  DA(g.qlen, g.W);
+  DA(g.qnode, std::max<uint64_t>(1, g.W * g.C));
+  DA(g.qreuse, std::max<uint64_t>(1, g.W * g.C));
+  DA(g.stg_nodes, std::max<uint64_t>(1, 2 * g.C));
+  DA(g.route_cnt, G);
+  DA(g.local_inbox_cnt, 1);
+  DA(g.score, g.Q);
+  DA(g.fills, g.ucap);
+  DA(g.cands, g.ucap);
+  DA(g.scr, 1);
+  DA(g.hist, (size_t)kHist * F_NFIELDS);
+  DA(g.cum, F_NFIELDS);
+#undef DA
+  if (static_scores) {  // this home's nodes v = rank + k*G, in k order
+    std::vector<uint8_t> mine(g.Q, 0);
+    for (uint64_t k = 0; k < g.Q; ++k) {
+      const uint64_t v = (uint64_t)g.rank + k * G;
+      if (v < g.N) mine[k] = static_scores[v];
+    }
+    CK(cudaMemcpy(g.score, mine.data(), g.Q, cudaMemcpyHostToDevice));
+  }
+  if (g.C) {
+    const size_t qb = (size_t)g.W * g.C * g.R;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&g.qrows_host), qb, cudaHostAllocMapped | cudaHostAllocPortable));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g.qrows_dev), g.qrows_host, 0));
+  }
+  {
+    void* hb = nullptr;
+    CK(cudaHostAlloc(&hb, 64, cudaHostAllocMapped));
+    std::memset(hb, 0, 64);
+    g.bad_host = reinterpret_cast<volatile uint32_t*>(hb);
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g.bad_dev), hb, 0));
+  }
+  CK(cudaStreamCreateWithFlags(&g.side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&g.ev_main, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&g.ev_pvp, cudaEventDisableTiming));
+  CK(cudaFuncSetAttribute(k_set, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(g.warp_bytes * g.set_warps)));
+  if (G > 1) {
+    cudaDriverEntryPointQueryResult q1, q2;
+    CK(cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void**>(&g.waitv), cudaEnableDefault, &q1));
+    CK(cudaGetDriverEntryPoint("cuStreamWriteValue32", reinterpret_cast<void**>(&g.writev), cudaEnableDefault, &q2));
+    if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !g.waitv || !g.writev)
+      return set_err(LSMGNN_ECOMM, "stream memory operations unavailable");
+  }
+  CK(cudaDeviceSynchronize());
+  g.inited = true;
+  g.connected = (G == 1);
+  g.t_next = 0;
+  g.feed_next = 1;
+  return 0;
+}
+
+int lsmgnn_attach_storage(const void* host_rows, const char* nvme_path) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "attach_storage before init");
+  if (nvme_path) return set_err(LSMGNN_EINVAL, "NVMe tier not implemented (DESIGN.md: out of scope this round)");
+  if (!host_rows) return set_err(LSMGNN_EINVAL, "null storage");
+  if (g.table_registered) {
+    cudaHostUnregister((void*)g.table_host);
+    g.table_registered = false;
+  }
+  const uint64_t rows = (g.N > (uint64_t)g.rank) ? (g.N - g.rank + g.world - 1) / g.world : 0;
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, host_rows);
+  if (e != cudaSuccess) cudaGetLastError();
+  if (e == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer) {
+    g.table_dev = reinterpret_cast<const uint8_t*>(at.devicePointer);
+  } else {
+    CK(cudaHostRegister(const_cast<void*>(host_rows), rows * g.R, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    g.table_registered = true;
+    void* dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, const_cast<void*>(host_rows), 0));
+    g.table_dev = reinterpret_cast<const uint8_t*>(dp);
+  }
+  g.table_host = reinterpret_cast<const uint8_t*>(host_rows);
+  return 0;
+}
+
+int lsmgnn_export_handle(void* buf, size_t cap) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "export before init");
+  if (!buf || cap < sizeof(Handle)) return set_err(LSMGNN_EINVAL, "buffer too small");
+  Handle h{};
+  CK(cudaIpcGetMemHandle(&h.ipc, g.arena));
+  h.arena_bytes = g.arena_bytes;
+  h.layout_sig = (g.off_pool * 1315423911ull) ^ (g.pool_rows << 17) ^ g.cap ^ ((uint64_t)g.R << 40);
+  h.rank = g.rank;
+  h.world = g.world;
+  std::memcpy(buf, &h, sizeof h);
+  return 0;
+}
+
+int lsmgnn_connect(const void* peer_handles, int32_t world) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "connect before init");
+  if (world != g.world) return set_err(LSMGNN_EINVAL, "world mismatch");
+  if (world == 1) {
+    g.connected = true;
+    return 0;
+  }
+  Handle mine{};
+  if (int rc = lsmgnn_export_handle(&mine, sizeof mine)) return rc;
+  const Handle* hs = reinterpret_cast<const Handle*>(peer_handles);
+  for (int r = 0; r < world; ++r) {
+    if (hs[r].rank != r || hs[r].world != world || hs[r].layout_sig != mine.layout_sig ||
+        hs[r].arena_bytes != mine.arena_bytes)
+      return set_err(LSMGNN_ECOMM, "peer %d handle does not match this rank's layout", r);
+    if (r == g.rank) continue;
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, hs[r].ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return set_err(LSMGNN_ECOMM, "cudaIpcOpenMemHandle(peer %d): %s", r, cudaGetErrorString(e));
+    g.peer_arena[r] = reinterpret_cast<char*>(p);
+  }
+  g.connected = true;
+  return 0;
+}
+
+int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
+  if (!g.inited || !g.connected) return set_err(LSMGNN_ESTATE, "gather before init/connect");
+  if (!g.table_dev) return set_err(LSMGNN_ESTATE, "no storage attached");
+  if (n < 0 || (uint64_t)n > g.cap) return set_err(LSMGNN_EINVAL, "n=%lld exceeds max_batch_ids", (long long)n);
+  if (n > 0 && (!node_ids || !out)) return set_err(LSMGNN_EINVAL, "null ids/out");
+  if (reinterpret_cast<uintptr_t>(out) % 16) return set_err(LSMGNN_EINVAL, "out must be 16-byte aligned");
+  if (int rc = check_sticky()) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g.world;
+  const int64_t t = g.t_next;
+  const uint32_t stamp = (uint32_t)(t + 1);
+  unsigned long long* rec = g.hist + (size_t)(t % kHist) * F_NFIELDS;
+
+  if (g.pvp_pending) {
+    CK(cudaStreamWaitEvent(st, g.ev_pvp, 0));
+    g.pvp_pending = false;
+  }
+  k_begin<<<1, 32, 0, st>>>(rec, g.scr, (uint64_t)t);
+  LAUNCHED();
+
+  // ---- S1/S2 route + exchange
+  const uint32_t* inbox;
+  const uint32_t* inbox_cnt;
+  if (G == 1) {
+    CK(cudaMemsetAsync(g.local_inbox_cnt, 0, sizeof(uint32_t), st));
+    if (n > 0) {
+      k_route_local<<<grid_for(n, 256), 256, 0, st>>>(node_ids, n, g.N, inbox_of(g.arena), g.local_inbox_cnt, g.scr);
+      LAUNCHED();
+    }
+    inbox = inbox_of(g.arena);
+    inbox_cnt = g.local_inbox_cnt;
+  } else {
+    if (int rc = exchange_ids(node_ids, n, false, stamp, st)) return rc;
+    inbox = inbox_of(g.arena);
+    inbox_cnt = icnt_of(g.arena);
+  }
+
+  // ---- S3 dedup + set grouping
+  const int64_t maxreq = (int64_t)g.cap * G;
+  k_dedup<<<grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n, 1) * G), 256, 4), 256, 0, st>>>(
+      inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, stamp, g.mark,
+      g.uniq, g.set_cnt, g.scr, rec);
+  LAUNCHED();
+  const uint32_t par = (uint32_t)(t & 1);
+  k_scan<<<1, 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes + par * g.C : nullptr,
+                             &g.scr->staged[par], g.mark, stamp, (uint32_t)G, rec);
+  LAUNCHED();
+  k_bucket<<<grid_for(std::max<int64_t>(n, 1) * G, 256, 4), 256, 0, st>>>(g.uniq, g.scr, (uint32_t)G, (uint32_t)g.S,
+                                                                           g.set_off, g.set_cnt, g.bucket);
+  LAUNCHED();
+
+  // ---- S4/S5 probe + replacement
+  SetParams sp{};
+  sp.set_off = g.set_off;
+  sp.bucket = g.bucket;
+  sp.tags = g.tags;
+  sp.last_use = g.last_use;
+  sp.rr = g.rr;
+  sp.score = g.score;
+  sp.mask = g.mask;
+  sp.node_loc = loc_of(g.arena);
+  sp.vst_stamp = g.vst_stamp;
+  sp.vst_idx = g.vst_idx;
+  sp.fills = g.fills;
+  sp.cands = g.cands;
+  sp.scr = g.scr;
+  sp.rec = rec;
+  sp.S = (uint32_t)g.S;
+  sp.A = g.A;
+  sp.G = (uint32_t)G;
+  sp.W = g.W;
+  sp.T = g.T;
+  sp.MW = g.MW;
+  sp.policy = (uint32_t)g.opt.policy;
+  sp.pvp = (uint32_t)g.opt.pvp;
+  sp.reinsert = (uint32_t)g.opt.reinsert_victims;
+  sp.t = (uint32_t)t;
+  sp.stamp = stamp;
+  sp.p0 = (uint32_t)((t + 1) % g.Wp1);
+  sp.P = g.P;
+  sp.warp_bytes = g.warp_bytes;
+  sp.stage_base = (uint32_t)(g.stage_base0 + par * g.C);
+  sp.bypass_base = (uint32_t)g.bypass_base;
+  {
+    const int64_t blocks = std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * 8);
+    k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);
+    LAUNCHED();
+  }
+  // ---- S5 victim admission (PVP)
+  if (g.C) {
+    const int qg = grid_for(g.ucap, 256, 2);
+    k_qhist<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qcnt);
+    LAUNCHED();
+    k_scan<<<1, 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, nullptr, nullptr, 0, 1, nullptr);
+    LAUNCHED();
+    k_qscatter<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
+    LAUNCHED();
+    k_admit<<<g.W, 256, 0, st>>>(g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint32_t)g.C, rec);
+    LAUNCHED();
+  }
+  // ---- S6 fill (victim D2H + storage/staging -> slot)
+  {
+    uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
+    const uint4* tab = reinterpret_cast<const uint4*>(g.table_dev);
+    uint4* hq = reinterpret_cast<uint4*>(g.qrows_dev);
+    const int blocks = g.sms * 4;
+    if (g.nvec >= 256)
+      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
+    else
+      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
+    LAUNCHED();
+  }
+  // ---- S7/S8 serve: homes signal, requesters pull
+  if (G > 1) {
+    for (int r = 0; r < G; ++r)
+      if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[G + g.rank], stamp)) return rc;
+    for (int h = 0; h < G; ++h)
+      if (int rc = flag_wait(st, &flags_of(g.arena)[G + h], stamp)) return rc;
+  }
+  if (n > 0) {
+    PullArgs pa{};
+    for (int h = 0; h < G; ++h) {
+      pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
+      pa.node_loc[h] = loc_of(g.peer_arena[h]);
+    }
+    pa.G = (uint32_t)G;
+    const int blocks = grid_for(n * 32, 256, 8);
+    if (g.nvec >= 256)
+      k_pull<8><<<blocks, 256, 0, st>>>(node_ids, n, g.N, pa, reinterpret_cast<uint4*>(out), g.nvec);
+    else
+      k_pull<2><<<blocks, 256, 0, st>>>(node_ids, n, g.N, pa, reinterpret_cast<uint4*>(out), g.nvec);
+    LAUNCHED();
+  }
+  k_end<<<1, 32, 0, st>>>(rec, g.cum, g.scr, (uint64_t)t, g.R);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(g.bad_dev, &g.scr->bad_ids, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  g.t_next = t + 1;
+  g.last_stream = st;
+  return 0;
+}
+
+int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batches, int64_t first_iter,
+                    void* stream) {
+  if (!g.inited || !g.connected) return set_err(LSMGNN_ESTATE, "prefetch before init/connect");
+  if (num_batches < 0 || (num_batches > 0 && !offsets)) return set_err(LSMGNN_EINVAL, "bad batches");
+  if (num_batches > 0 && first_iter != g.feed_next)
+    return set_err(LSMGNN_ESTATE, "window iteration %lld fed, %lld expected", (long long)first_iter,
+                   (long long)g.feed_next);
+  if (int rc = check_sticky()) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g.world;
+  for (int32_t b = 0; b < num_batches; ++b) {
+    const int64_t k = first_iter + b;
+    const int64_t n = offsets[b + 1] - offsets[b];
+    if (n < 0 || (uint64_t)n > g.cap) return set_err(LSMGNN_EINVAL, "window batch of %lld ids", (long long)n);
+    if (k > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
+    const uint32_t slot = (uint32_t)(k % g.Wp1);
+    uint32_t* ring_slot = g.ring + (size_t)slot * g.cap * G;
+    // drop the bits of the iteration that last used this slot (k - (W+1))
+    k_mask_clear<<<grid_for((int64_t)g.cap * G, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, (uint32_t)G,
+                                                                        g.MW, slot, g.mask);
+    LAUNCHED();
+    if (G == 1) {
+      CK(cudaMemsetAsync(g.ring_len + slot, 0, sizeof(uint32_t), st));
+      if (n > 0) {
+        k_route_local<<<grid_for(n, 256), 256, 0, st>>>(ids + offsets[b], n, g.N, ring_slot, g.ring_len + slot, g.scr);
+        LAUNCHED();
+      }
+    } else {
+      const uint32_t seq = ++g.win_seq;
+      if (int rc = exchange_ids(n > 0 ? ids + offsets[b] : nullptr, n, true, seq, st)) return rc;
+      k_win_gather<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(win_of(g.arena), wcnt_of(g.arena), (uint32_t)G,
+                                                                      (uint32_t)g.cap, ring_slot, g.ring_len + slot);
+      LAUNCHED();
+      for (int r = 0; r < G; ++r)  // window inbox consumed
+        if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[3 * G + g.rank], seq)) return rc;
+    }
+    k_mask_set<<<grid_for((int64_t)g.cap * G, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, (uint32_t)G, g.MW,
+                                                                      slot, g.mask);
+    LAUNCHED();
+    g.feed_next = k + 1;
+  }
+  // ---- S11 PVP copy for iteration t+1 on the side stream (after gather(t))
+  if (g.C && g.t_next > 0 && !g.pvp_pending) {
+    const int64_t t1 = g.t_next;  // = t + 1
+    const uint32_t par = (uint32_t)(t1 & 1);
+    CK(cudaEventRecord(g.ev_main, st));
+    CK(cudaStreamWaitEvent(g.side, g.ev_main, 0));
+    const uint32_t kq = (uint32_t)(t1 % g.W);
+    uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
+    const int blocks = g.sms * 2;
+    if (g.nvec >= 256)
+      k_pvp<8><<<blocks, 256, 0, g.side>>>(kq, (uint32_t)t1, (uint32_t)(t1 + 1), (uint32_t)g.C, (uint32_t)G, g.qlen,
+                                           g.qnode, g.qreuse, reinterpret_cast<const uint4*>(g.qrows_dev), pool,
+                                           (uint32_t)(g.stage_base0 + par * g.C), g.stg_nodes + par * g.C,
+                                           g.vst_stamp, g.vst_idx, g.scr, par, g.nvec);
+    else
+      k_pvp<2><<<blocks, 256, 0, g.side>>>(kq, (uint32_t)t1, (uint32_t)(t1 + 1), (uint32_t)g.C, (uint32_t)G, g.qlen,
+                                           g.qnode, g.qreuse, reinterpret_cast<const uint4*>(g.qrows_dev), pool,
+                                           (uint32_t)(g.stage_base0 + par * g.C), g.stg_nodes + par * g.C,
+                                           g.vst_stamp, g.vst_idx, g.scr, par, g.nvec);
+    LAUNCHED();
+    CK(cudaEventRecord(g.ev_pvp, g.side));
+    g.pvp_pending = true;
+  }
+  g.last_stream = st;
+  return 0;
+}
+
+int lsmgnn_gather_host(const int64_t* host_ids, int64_t n, void* host_out, void* stream) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
+  if (n < 0 || (uint64_t)n > g.cap) return set_err(LSMGNN_EINVAL, "bad n");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (!g.tmp_ids) {
+    CK(cudaMalloc(reinterpret_cast<void**>(&g.tmp_ids), g.cap * sizeof(int64_t)));
+    CK(cudaMalloc(&g.tmp_out, g.cap * (size_t)g.R));
+  }
+  if (n > 0) CK(cudaMemcpyAsync(g.tmp_ids, host_ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (int rc = lsmgnn_gather(g.tmp_ids, n, g.tmp_out, stream)) return rc;
+  if (n > 0) CK(cudaMemcpyAsync(host_out, g.tmp_out, n * (size_t)g.R, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return check_sticky();
+}
+
+int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
+  if (!out_host || (scope != 0 && scope != 1)) return set_err(LSMGNN_EINVAL, "bad args");
+  static_assert(sizeof(lsmgnn_stats_t) == F_NFIELDS * sizeof(uint64_t), "stats layout");
+  CK(cudaDeviceSynchronize());
+  if (scope == 1) {
+    CK(cudaMemcpy(out_host, g.cum, sizeof(lsmgnn_stats_t), cudaMemcpyDeviceToHost));
+  } else if (g.t_next == 0) {
+    std::memset(out_host, 0, sizeof *out_host);
+  } else {
+    CK(cudaMemcpy(out_host, g.hist + (size_t)((g.t_next - 1) % kHist) * F_NFIELDS, sizeof(lsmgnn_stats_t),
+                  cudaMemcpyDeviceToHost));
+  }
+  return check_sticky();
+}
+
+int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
+  if (count < 0 || first < 0 || first + count > g.t_next || (g.t_next - first) > kHist)
+    return set_err(LSMGNN_EINVAL, "history range [%lld,+%lld) unavailable", (long long)first, (long long)count);
+  CK(cudaDeviceSynchronize());
+  for (int64_t i = 0; i < count; ++i)
+    CK(cudaMemcpy(out_host + i, g.hist + (size_t)((first + i) % kHist) * F_NFIELDS, sizeof(lsmgnn_stats_t),
+                  cudaMemcpyDeviceToHost));
+  return check_sticky();
+}
+
+int lsmgnn_finalize(void) {
+  if (!g.inited) return 0;
+  free_all();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+"""Shared driver for parity tests and the bench: runs a trace through the CUDA path
+(via the C-ABI binding) and through the CPU oracle on identical seeded inputs.
+
+Both sides consume the same inputs from `synth` (graph, trace, scores, feature table);
+neither computes anything for the other.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import synth
+
+
+def table_for(N: int, D: int, seed_f: int = 5, pinned: bool = False, home: int = 0, G: int = 1):
+    """Host feature table rows of home `home` (node home + k*G at row k), uint8 [rows, 4D]."""
+    import torch
+    rows = (N - home + G - 1) // G
+    if pinned:
+        t = torch.empty((rows, 4 * D), dtype=torch.uint8, pin_memory=True)
+    else:
+        t = torch.empty((rows, 4 * D), dtype=torch.uint8)
+    if G == 1:
+        synth.fill_features(t.data_ptr(), 0, rows, D, seed_f)
+    else:
+        ids = np.arange(home, N, G, dtype=np.int64)
+        synth._lib().synth_fill_f32_ids(t.data_ptr(), ids.ctypes.data, ids.size, D, seed_f)
+    return t
+
+
+def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1, table=None,
+            check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False):
+    """Run trace[t][rank] through the library. Returns (history [K, 24] uint64, outs or None, bad_rows).
+
+    check_rows: "full" compares every row with the closed form F(v); "none" skips it."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    K = len(trace)
+    R = 4 * D
+    mine = [np.asarray(trace[t][rank], np.int64) for t in range(K)]
+    mb = max_batch_ids or max(1, max(x.size for x in mine))
+    c = LsmGnn(N, D, L, A, V, scores, policy=policy, pvp=pvp, window=W, threshold=T, reinsert=reinsert,
+               max_batch_ids=mb, rank=rank, world=world, group=group)
+    if table is None:
+        table = table_for(N, D, seed_f, pinned=True, home=rank, G=world)
+    c.attach_storage(table)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ids_d = [torch.from_numpy(x).to(dev) for x in mine]
+    empty = torch.zeros(0, dtype=torch.int64, device=dev)
+    c.prefetch([ids_d[k] if k < K else empty for k in range(1, W + 1)], first_iter=1)
+    outs = []
+    bad = 0
+    for t in range(K):
+        out = torch.empty((max(1, ids_d[t].numel()), R), dtype=torch.uint8, device=dev)
+        c.gather(ids_d[t], out)
+        k = t + 1 + W
+        c.prefetch([ids_d[k] if k < K else empty], first_iter=k)
+        if check_rows == "full" and ids_d[t].numel():
+            host = out[: ids_d[t].numel()].cpu().numpy()
+            nb, _ = synth.check_rows(host.view(np.uint32).reshape(-1, D), mine[t], D, seed_f)
+            bad += nb
+            if keep_outs:
+                outs.append(host)
+    torch.cuda.synchronize()
+    hist = c.history(0, K)
+    c.close()
+    return hist, (outs if keep_outs else None), bad
+
+
+def run_oracle(trace, *, G, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1):
+    from oracle import Oracle, run_trace
+    o = Oracle(G, N, 4 * D, L, A, scores, policy=policy, pvp=pvp, W=W, T=T, V=V, reinsert=reinsert)
+    return run_trace(o, trace)
+
+
+def small_workload(N=16384, m=8, G=1, batch=256, fanout=(10, 5), iters=20, dedup=True, seed_s=4):
+    g = synth.plcite(N, m)
+    tr = synth.make_trace(g, G, batch, fanout, iters, dedup=dedup, seed_s=seed_s)
+    return g, tr, synth.static_scores(g)

@@ -1,0 +1,141 @@
+"""GPU parity: CUDA path (through the C-ABI) vs the CPU oracle, bit-exact (-m gpu).
+
+Bytes: every gathered row equals the closed form F(v) (= the oracle's plain gather
+of the same synth table). Counts: every field of every per-iteration record equals
+the oracle's, integer for integer.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import COUNT_FIELDS
+
+from .harness import run_gpu, run_oracle, small_workload
+
+pytestmark = pytest.mark.gpu
+
+F = {n: i for i, n in enumerate(COUNT_FIELDS)}
+
+
+def compare(hg, ho, label=""):
+    assert hg.shape == ho.shape, (hg.shape, ho.shape)
+    if not np.array_equal(hg, ho):
+        bad = np.argwhere(hg != ho)
+        t, f = bad[0]
+        raise AssertionError(f"{label}: first mismatch iter {t} field {COUNT_FIELDS[f]}: gpu {hg[t, f]} oracle "
+                             f"{ho[t, f]} ({len(bad)} mismatching cells)\n gpu {hg[t]}\n orc {ho[t]}")
+
+
+@pytest.fixture(scope="module")
+def cfg1_g1():
+    # configs[0] shape (16,384 nodes / 131,072 edges, fanout (10,5), batch 256, 8-way, 512 victim
+    # lines, 20 batches) on ONE home: 1,024 lines
+    return small_workload(16384, 8, G=1, batch=256, fanout=(10, 5), iters=20)
+
+
+@pytest.mark.parametrize("policy", ["hybrid", "static", "lru", "rr", "dynamic"])
+@pytest.mark.parametrize("pvp", [0, 1])
+def test_cfg1_single_home(cfg1_g1, policy, pvp):
+    g, tr, sc = cfg1_g1
+    kw = dict(N=16384, D=128, L=1024, A=8, scores=sc, policy=policy, pvp=pvp, W=8, V=512)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"{policy}/pvp{pvp}")
+    assert ho[:, F["bypassed"]].sum() > 0  # the oversubscribed regime of config 1 is exercised
+    if pvp:
+        assert ho[:, F["victim_admitted"]].sum() > 0 and ho[:, F["victim_hits"]].sum() > 0
+
+
+def test_duplicates_and_ragged():
+    """Raw sampler lists with duplicates and ragged batch sizes."""
+    g, tr, sc = small_workload(4096, 6, G=1, batch=64, fanout=(6, 3), iters=15, dedup=False)
+    tr = [[x[: (7 * t) % len(x) + 1]] for t, (x,) in enumerate(tr)]
+    kw = dict(N=4096, D=32, L=256, A=4, scores=sc, policy="hybrid", pvp=1, W=5, V=40)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho)
+    assert ho[:, F["requests"]].sum() > ho[:, F["unique"]].sum()
+
+
+@pytest.mark.parametrize("case", ["empty", "one_way", "full_assoc", "w1", "reinsert0", "tiny_queue", "thresh",
+                                  "same_node", "no_window"])
+def test_edge_cases(case):
+    rng = np.random.default_rng(7)
+    N, D = 2000, 4
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    tr = [[rng.integers(0, N, int(rng.integers(0, 300)))] for _ in range(25)]
+    kw = dict(N=N, D=D, L=64, A=8, scores=sc, policy="hybrid", pvp=1, W=6, V=60)
+    if case == "empty":
+        tr = [[np.zeros(0, np.int64)] if t % 3 == 0 else x for t, x in enumerate(tr)]
+    elif case == "one_way":
+        kw.update(L=32, A=1)
+    elif case == "full_assoc":
+        kw.update(L=32, A=32)
+    elif case == "w1":
+        kw.update(W=1, V=4)
+    elif case == "reinsert0":
+        kw.update(reinsert=0)
+    elif case == "tiny_queue":
+        kw.update(V=6)  # C = 1: queue overflow -> admission by node order
+    elif case == "thresh":
+        kw.update(T=4)
+    elif case == "same_node":
+        tr = [[np.full(50, 17, np.int64)] for _ in range(10)]
+    elif case == "no_window":
+        kw.update(pvp=0, policy="dynamic", W=1)
+    hg, _, bad = run_gpu(tr, max_batch_ids=400, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, case)
+
+
+def test_bad_ids_sticky_erange():
+    import torch
+    from paper_2407_15264_b200 import LsmGnn, LsmGnnError
+    from .harness import table_for
+    N, D = 100, 4
+    c = LsmGnn(N, D, 16, 4, 0, np.zeros(N, np.uint8), window=2, max_batch_ids=16)
+    c.attach_storage(table_for(N, D, pinned=True))
+    ids = torch.tensor([1, 2, 150, 3], dtype=torch.int64, device="cuda")
+    out = torch.full((4, 16), 7, dtype=torch.uint8, device="cuda")
+    c.gather(ids, out)
+    torch.cuda.synchronize()
+    assert out[2].sum().item() == 0
+    good = out[[0, 1, 3]].cpu().numpy().view(np.uint32).reshape(3, D)
+    assert synth.check_rows(good, [1, 2, 3], D)[0] == 0
+    with pytest.raises(LsmGnnError):
+        c.stats()
+    with pytest.raises(LsmGnnError):
+        c.gather(ids, out)
+    c.close()
+
+
+def test_abi_errors():
+    from paper_2407_15264_b200 import LsmGnn, LsmGnnError
+    with pytest.raises(LsmGnnError):
+        LsmGnn(100, 3, 16, 4)  # R = 12 bytes: not a multiple of 16
+    with pytest.raises(LsmGnnError):
+        LsmGnn(100, 4, 18, 4)  # lines not a multiple of ways
+    c = LsmGnn(100, 4, 16, 4, max_batch_ids=8)
+    import torch
+    ids = torch.zeros(9, dtype=torch.int64, device="cuda")
+    out = torch.empty((9, 16), dtype=torch.uint8, device="cuda")
+    with pytest.raises(LsmGnnError):
+        c.gather(ids, out)  # no storage attached / n > max_batch_ids
+    c.close()
+
+
+@pytest.mark.parametrize("policy,pvp", [("hybrid", 0), ("hybrid", 1), ("static", 0), ("lru", 0)])
+def test_cfg2_shape_reduced(policy, pvp):
+    """configs[1] shape (IGB-small: 1M nodes, fanout (10,5,5), batch 1024, 10% cache, 32-way,
+    W=256) with 64-dim rows and 12 iterations; counts must match exactly."""
+    g = synth.plcite(1_000_000, 12)
+    tr = synth.make_trace(g, 1, 1024, (10, 5, 5), 12)
+    sc = synth.static_scores(g)
+    kw = dict(N=1_000_000, D=16, L=100_000, A=32, scores=sc, policy=policy, pvp=pvp, W=256, V=256 * 64)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"cfg2/{policy}/pvp{pvp}")
