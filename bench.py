@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py — effective feature-gather GB/s of the LSM-GNN hot path on B200.
+
+Contract (see DESIGN.md §"Measurement"):
+  python bench.py --gpus N --steps K --warmup W [--impl reference]
+A step is one pass of the whole hot path over one batch: gather(t) (route, dedup, probe,
+replacement, victim admission, fill, pull) + prefetch(t) (window feed, PVP copy). The
+workload at N=1 is BASELINE.json configs[1] (IGB-small-shaped: 1M nodes, 1024-dim fp32
+rows, fanout (10,5,5), batch 1024, cache = 10% of the features, 32-way, W = 256).
+Inputs are synthetic (synth/), generated before the timed region and resident in HBM.
+
+value = sum over timed steps and ranks of requested rows x R / max over ranks of the
+device time of the K steps (CUDA events on the launching stream).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "effective feature-gather GB/s (box, device-timed)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", default="lsmgnn", choices=["lsmgnn", "reference"])
+    p.add_argument("--config", default="cfg2")
+    p.add_argument("--policy", default="hybrid")
+    p.add_argument("--pvp", type=int, default=None)
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-profile", action="store_true")
+    p.add_argument("--lines", type=int, default=None, help="override lines per GPU")
+    return p.parse_args()
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/lsmgnn_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def build_inputs(wl, G, rank, iters, seed_offset=0):
+    import synth
+    t0 = time.time()
+    g = synth.plcite(wl.N, wl.m, seed_g=wl.seeds["g"], seed_pi=wl.seeds["pi"])
+    trace = synth.make_trace_parallel(g, G, wl.batch, wl.fanout, iters, seed_train=wl.seeds["train"],
+                                      seed_s=wl.seeds["s"])
+    scores = synth.static_scores(g)
+    log(f"[bench] inputs: graph N={wl.N} m={wl.m}, {iters} iterations x {G} ranks in {time.time() - t0:.1f}s")
+    return g, trace, scores
+
+
+def run_reference(args, wl, G, rank):
+    """--impl reference: the CPU oracle (as it stands) timed on the host cores, same metric."""
+    if rank != 0:
+        return
+    import oracle
+    from tests.harness import table_for
+    K, Wu = args.steps, args.warmup
+    pvp = wl.pvp if args.pvp is None else args.pvp
+    iters = Wu + K + wl.window + 1
+    _, trace, scores = build_inputs(wl, G, rank, iters)
+    table = table_for(wl.N, wl.D).numpy()
+    o = oracle.Oracle(G, wl.N, wl.R, args.lines or wl.lines_per_gpu, wl.ways, scores, policy=args.policy, pvp=pvp,
+                      W=wl.window, V=wl.victim_lines)
+    for k in range(1, wl.window + 1):
+        o.feed(k, trace[k])
+    byts, tsum = 0, 0.0
+    for t in range(Wu + K):
+        t0 = time.perf_counter()
+        o.gather(t, trace[t], table)
+        o.pvp_prefetch(t)
+        o.feed(t + 1 + wl.window, trace[t + 1 + wl.window] if t + 1 + wl.window < len(trace) else
+               [np.zeros(0, np.int64)] * G)
+        dt = time.perf_counter() - t0
+        if t >= Wu:
+            tsum += dt
+            byts += sum(len(x) for x in trace[t]) * wl.R
+    gbs = byts / tsum / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": G,
+            "steps": K, "warmup": Wu, "ms_per_step": round(tsum / K * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": wl.name + " (" + ("IGB-small-shaped" if wl.name == "cfg2" else wl.name) + ")",
+                       "N": wl.N, "row_bytes": wl.R, "batch_per_rank": wl.batch, "fanout": list(wl.fanout),
+                       "lines_per_gpu": args.lines or wl.lines_per_gpu, "ways": wl.ways, "window": wl.window,
+                       "policy": args.policy, "pvp": pvp},
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"full {wl.name} iterations {Wu}..{Wu + K - 1} after {Wu} untimed, rows "
+                                       f"materialised by memcpy from the host table, single thread"},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(wl, G, trace, scores, table_np, args, lines):
+    """The oracle as it stands, timed on this host: a bounded sample (about args.cpu_seconds)."""
+    import oracle
+    pvp = wl.pvp if args.pvp is None else args.pvp
+    o = oracle.Oracle(G, wl.N, wl.R, lines, wl.ways, scores, policy=args.policy, pvp=pvp, W=wl.window,
+                      V=wl.victim_lines)
+    for k in range(1, wl.window + 1):
+        o.feed(k, trace[k])
+    byts, tsum, t = 0, 0.0, 0
+    while tsum < args.cpu_seconds and t + 1 + wl.window < len(trace):
+        t0 = time.perf_counter()
+        o.gather(t, trace[t], table_np)
+        o.pvp_prefetch(t)
+        o.feed(t + 1 + wl.window, trace[t + 1 + wl.window])
+        tsum += time.perf_counter() - t0
+        byts += sum(len(x) for x in trace[t]) * wl.R
+        t += 1
+    return {"value": round(byts / tsum / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{wl.name} iterations 0..{t - 1} from a cold cache ({tsum:.1f}s), rows materialised by "
+                      f"memcpy from the host table, single thread (C oracle, gcc -O2)"}
+
+
+def main():
+    args = parse()
+    import synth
+    wl = synth.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    G = max(world, 1)
+    if args.gpus != G and world > 1:
+        log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}; using {G}")
+    if args.impl == "reference":
+        return run_reference(args, wl, G, rank)
+
+    import torch
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if G > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist.group.WORLD
+    from paper_2407_15264_b200 import LsmGnn
+    from tests.harness import table_for
+
+    K, Wu = args.steps, args.warmup
+    E = 0 if args.no_e2e else args.e2e_steps
+    W = wl.window
+    pvp = wl.pvp if args.pvp is None else args.pvp
+    lines = args.lines or wl.lines_per_gpu
+    iters = Wu + K + E + W + 1
+    g_, trace, scores = build_inputs(wl, G, rank, iters)
+    mine = [np.asarray(trace[t][rank], np.int64) for t in range(iters)]
+    max_ids = max(x.size for row in trace for x in row)
+    t0 = time.time()
+    table = table_for(wl.N, wl.D, wl.seeds["f"], pinned=True, home=rank, G=G)
+    log(f"[bench] host table {table.numel() / 2**30:.2f} GiB pinned in {time.time() - t0:.1f}s")
+
+    c = LsmGnn(wl.N, wl.D, lines, wl.ways, wl.victim_lines, scores, policy=args.policy, pvp=pvp, window=W,
+               max_batch_ids=max_ids, rank=rank, world=G, device=local, group=pg)
+    c.attach_storage(table)
+    ids_d = [torch.from_numpy(x).to(dev) for x in mine]
+    maxn = max(x.numel() for x in ids_d)
+    out = torch.empty((maxn, wl.R), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+    c.prefetch(ids_d[1:W + 1], first_iter=1)
+
+    def step(t):
+        c.gather(ids_d[t], out)
+        k = t + 1 + W
+        c.prefetch([ids_d[k]], first_iter=k)
+
+    for t in range(Wu):
+        step(t)
+    torch.cuda.synchronize()
+    if G > 1:
+        torch.distributed.barrier()
+    s0 = c.stats(1)
+    l0 = c.kernel_launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    if not args.no_profile:
+        c.profile(True)
+        c.profile_read()  # reset
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if G > 1:
+        torch.distributed.barrier()
+    e_start.record(st)
+    for i in range(K):
+        t = Wu + i
+        ev[i][0].record(st)
+        step(t)
+        ev[i][1].record(st)
+    e_end.record(st)
+    torch.cuda.synchronize()
+    if G > 1:
+        torch.distributed.barrier()
+    launches = c.kernel_launches() - l0
+    prof = c.profile_read() if not args.no_profile else {}
+    c.profile(False)
+    clk = clocks.stop()
+    s1 = c.stats(1)
+    T = e_start.elapsed_time(e_end) / 1e3
+    per_step = [a.elapsed_time(b) for a, b in ev]
+    my_bytes = sum(mine[Wu + i].size for i in range(K)) * wl.R
+    if G > 1:
+        x = torch.tensor([T, float(my_bytes)], dtype=torch.float64, device=dev)
+        tmax = x[:1].clone()
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+        tot = x[1:].clone()
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
+        T, all_bytes = float(tmax.item()), float(tot.item())
+    else:
+        all_bytes = float(my_bytes)
+    value = all_bytes / T / 1e9
+    d = {k: s1[k] - s0[k] for k in s1 if k != "iter"}
+
+    # ---- end to end through the public API with HOST buffers (copies inside the timed region)
+    e2e = None
+    if E:
+        hids = [torch.from_numpy(mine[Wu + K + i]).pin_memory() for i in range(E)]
+        hout = torch.empty((maxn, wl.R), dtype=torch.uint8, pin_memory=True)
+        torch.cuda.synchronize()
+        if G > 1:
+            torch.distributed.barrier()
+        tsum, eb, h2d, d2h = 0.0, 0, 0, 0
+        for i in range(E):
+            t = Wu + K + i
+            t0 = time.perf_counter()
+            c.gather_host(hids[i], hout)
+            k = t + 1 + W
+            c.prefetch([ids_d[k]], first_iter=k)
+            torch.cuda.synchronize()
+            tsum += time.perf_counter() - t0
+            eb += hids[i].numel() * wl.R
+            h2d += hids[i].numel() * 8
+            d2h += hids[i].numel() * wl.R
+        if G > 1:
+            x = torch.tensor([tsum], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+            tsum = float(x.item())
+            y = torch.tensor([float(eb)], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(y, op=torch.distributed.ReduceOp.SUM)
+            eb = float(y.item())
+        e2e = {"value": round(eb / tsum / 1e9, 4), "unit": "GB/s", "h2d_bytes_per_step": int(h2d / E),
+               "d2h_bytes_per_step": int(d2h / E), "steps": E,
+               "what": "lsmgnn_gather_host: pinned host IDs -> device, gather, rows -> pinned host, synchronous"}
+
+    # ---- roofline of the dominant phase, per-tier fractions
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    pcie_peak = measure_h2d(dev)
+    R = wl.R
+    phases = {}
+    for name, (ms, n) in prof.items():
+        phases[name] = {"ms": round(ms, 3), "launch_spans": n, "share_of_step": round(ms / (T * 1e3), 4)}
+    # algorithmic bytes: fill moves storage rows H2D + victim rows D2H, and
+    # writes every installed/bypassed row into HBM; pull reads + writes R per request.
+    fill_pcie = (d["storage_reads"] + 0) * R
+    fill_ms = prof.get("fill", (0.0, 0))[0]
+    pull_bytes = 2 * d["requests"] * R
+    pull_ms = prof.get("pull", (0.0, 0))[0]
+    roof = None
+    if fill_ms > 0:
+        ach = fill_pcie / (fill_ms / 1e3) / 1e9
+        roof = {"bound": "pcie", "kernel": "k_fill", "achieved": round(ach, 2), "peak": round(pcie_peak, 2),
+                "unit": "GB/s", "frac": round(ach / pcie_peak, 4), "traffic": None,
+                "peak_source": "cudaMemcpy pinned H2D 1 GiB best-of-5 measured in this run (the PCIe Gen5 x16 "
+                               "link is the bound of the storage tier)",
+                "per_launch": {"algorithmic_bytes": int(fill_pcie / K), "units": "storage rows x R (H2D)",
+                               "avg_ms": round(fill_ms / K, 4)}}
+        phases["fill"]["pcie_h2d_GBps"] = round(ach, 2)
+        phases["fill"]["frac_pcie"] = round(ach / pcie_peak, 4)
+    if pull_ms > 0:
+        ach = pull_bytes / (pull_ms / 1e3) / 1e9
+        phases["pull"]["hbm_GBps"] = round(ach, 1)
+        phases["pull"]["frac_hbm"] = round(ach / hbm_peak, 4)
+        phases["pull"]["hbm_peak_source"] = hbm_src
+    uniq = max(d["unique"], 1)
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": G, "steps": K, "warmup": Wu,
+        "ms_per_step": round(T / K * 1e3, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"{wl.name} (BASELINE.json configs[1], IGB-small-shaped)" if wl.name == "cfg2"
+                   else wl.name, "N": wl.N, "row_bytes": R, "payload": "fp32 rows (1024-dim), copied bytewise",
+                   "batch_per_rank": wl.batch, "fanout": list(wl.fanout), "lines_per_gpu": lines, "ways": wl.ways,
+                   "window": W, "threshold": max(1, W // 8), "policy": args.policy, "pvp": pvp,
+                   "victim_lines": wl.victim_lines if pvp else 0, "parallelism": f"shared cache over {G} GPU",
+                   "l2": "inputs larger than L2: cache 400 MB, out ~550 MB/step, host table 4 GB",
+                   "seeds": wl.seeds},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "roofline": roof,
+        "cpu_baseline": None,
+        "e2e": e2e,
+        "per_step_ms": {"median": round(statistics.median(per_step), 4), "min": round(min(per_step), 4),
+                        "max": round(max(per_step), 4)},
+        "tiers": {"hit_ratio": round(d["hits"] / uniq, 4), "victim_hit_ratio": round(d["victim_hits"] / uniq, 4),
+                  "storage_ratio": round(d["storage_reads"] / uniq, 4),
+                  "requests_per_step": d["requests"] / K, "unique_per_step": d["unique"] / K,
+                  "storage_GB_per_step": d["bytes_h2d_storage"] / K / 1e9,
+                  "pcie_h2d_GBps_over_step": round(d["bytes_h2d_storage"] / T / 1e9, 2),
+                  "victim_d2h_GBps_over_step": round(d["bytes_d2h_victim"] / T / 1e9, 2),
+                  "pvp_h2d_GBps_over_step": round(d["bytes_h2d_pvp"] / T / 1e9, 2),
+                  "bypassed_per_step": d["bypassed"] / K, "evictions_per_step": d["evictions"] / K},
+        "phases": phases,
+    }
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, G, trace, scores, table.numpy(), args, lines)
+    c.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if G > 1:
+        torch.distributed.destroy_process_group()
+
+
+def measure_h2d(dev) -> float:
+    import torch
+    nb = 1 << 30
+    h = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nb, dtype=torch.uint8, device=dev)
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        d.copy_(h, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, nb / (a.elapsed_time(b) / 1e3) / 1e9)
+    del h, d
+    return best
+
+
+if __name__ == "__main__":
+    main()

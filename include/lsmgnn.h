@@ -172,6 +172,16 @@ int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count)
 /* Number of kernels the library has launched since init (launch accounting). */
 int64_t lsmgnn_kernel_launches(void);
 
+/* Phase timing with CUDA events recorded on the stream each phase runs on (the user
+ * stream, or the PVP side stream). Phases (LSMGNN_PHASE_*): 0 route+exchange, 1 dedup
+ * (dedup, scan, bucket), 2 probe+replace (k_set), 3 victim admission, 4 fill, 5 serve+pull,
+ * 6 window feed (prefetch mask update), 7 PVP copy (side stream). enable=1 starts
+ * recording; lsmgnn_profile_read synchronises, writes the summed milliseconds per phase
+ * and the number of timed launches per phase (either pointer may be NULL) and resets. */
+#define LSMGNN_NPHASES 8
+int lsmgnn_profile(int32_t enable);
+int lsmgnn_profile_read(double* ms_per_phase, int64_t* count_per_phase);
+
 int lsmgnn_finalize(void);
 const char* lsmgnn_last_error(void);
 

@@ -23,7 +23,8 @@ STATS_FIELDS = ["iter", "requests", "peer_requests", "unique", "hits", "victim_h
 EXPORTS = ["lsmgnn_bind", "lsmgnn_set_options", "lsmgnn_init", "lsmgnn_attach_storage", "lsmgnn_handle_bytes",
            "lsmgnn_export_handle", "lsmgnn_connect", "lsmgnn_gather", "lsmgnn_gather_host", "lsmgnn_prefetch",
            "lsmgnn_stats", "lsmgnn_stats_history", "lsmgnn_kernel_launches", "lsmgnn_finalize",
-           "lsmgnn_last_error"]
+           "lsmgnn_last_error", "lsmgnn_profile", "lsmgnn_profile_read"]
+PHASES = ["route", "dedup", "probe_replace", "admit", "fill", "pull", "window", "pvp"]
 
 
 class Options(ctypes.Structure):
@@ -71,6 +72,8 @@ def load_library(path: str = SO_PATH) -> ctypes.CDLL:
         "lsmgnn_kernel_launches": ([], i64),
         "lsmgnn_finalize": ([], i32),
         "lsmgnn_last_error": ([], ctypes.c_char_p),
+        "lsmgnn_profile": ([i32], i32),
+        "lsmgnn_profile_read": ([vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -197,6 +200,17 @@ class LsmGnn:
         arr = (Stats * max(count, 1))()
         _check(_LIB.lsmgnn_stats_history(arr, first, count))
         return np.stack([arr[i].as_array() for i in range(count)]) if count else np.zeros((0, 24), np.uint64)
+
+    @staticmethod
+    def profile(enable: bool) -> None:
+        _check(load_library().lsmgnn_profile(1 if enable else 0))
+
+    @staticmethod
+    def profile_read() -> dict:
+        ms = np.zeros(len(PHASES), np.float64)
+        cnt = np.zeros(len(PHASES), np.int64)
+        _check(load_library().lsmgnn_profile_read(ms.ctypes.data, cnt.ctypes.data))
+        return {p: (float(ms[i]), int(cnt[i])) for i, p in enumerate(PHASES)}
 
     @staticmethod
     def kernel_launches() -> int:

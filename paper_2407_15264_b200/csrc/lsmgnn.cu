@@ -92,6 +92,13 @@ struct Ctx {
   uint32_t win_seq = 0;    // window batches exchanged (G > 1)
   int64_t launches = 0;
 
+  // phase profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  struct Span { int phase; cudaEvent_t a, b; };
+  std::vector<Span> spans;
+  cudaEvent_t open_ev[LSMGNN_NPHASES] = {};
+
   // driver entry points (stream memory operations)
   PFN_cuStreamWaitValue32_v2 waitv = nullptr;
   PFN_cuStreamWriteValue32_v2 writev = nullptr;
@@ -207,6 +214,30 @@ int exchange_ids(const int64_t* ids, int64_t n, bool win, uint32_t seq, cudaStre
   return 0;
 }
 
+cudaEvent_t take_event() {
+  if (g.ev_pool.empty()) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = g.ev_pool.back();
+  g.ev_pool.pop_back();
+  return e;
+}
+// Phase span on stream st: prof_begin records the start event, prof_end the end event.
+void prof_begin(int ph, cudaStream_t st) {
+  if (!g.prof) return;
+  g.open_ev[ph] = take_event();
+  cudaEventRecord(g.open_ev[ph], st);
+}
+void prof_end(int ph, cudaStream_t st) {
+  if (!g.prof || !g.open_ev[ph]) return;
+  cudaEvent_t b = take_event();
+  cudaEventRecord(b, st);
+  g.spans.push_back({ph, g.open_ev[ph], b});
+  g.open_ev[ph] = nullptr;
+}
+
 int free_all() {
   cudaDeviceSynchronize();
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off,
@@ -223,6 +254,11 @@ int free_all() {
   if (g.side) cudaStreamDestroy(g.side);
   if (g.ev_main) cudaEventDestroy(g.ev_main);
   if (g.ev_pvp) cudaEventDestroy(g.ev_pvp);
+  for (auto& sp : g.spans) {
+    cudaEventDestroy(sp.a);
+    cudaEventDestroy(sp.b);
+  }
+  for (auto e : g.ev_pool) cudaEventDestroy(e);
   const int rank = g.rank, world = g.world, dev = g.device;
   const lsmgnn_options opt = g.opt;
   const bool opt_set = g.opt_set;
@@ -498,6 +534,7 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   LAUNCHED();
 
   // ---- S1/S2 route + exchange
+  prof_begin(0, st);
   const uint32_t* inbox;
   const uint32_t* inbox_cnt;
   if (G == 1) {
@@ -514,7 +551,9 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     inbox_cnt = icnt_of(g.arena);
   }
 
+  prof_end(0, st);
   // ---- S3 dedup + set grouping
+  prof_begin(1, st);
   const int64_t maxreq = (int64_t)g.cap * G;
   k_dedup<<<grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n, 1) * G), 256, 4), 256, 0, st>>>(
       inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, stamp, g.mark,
@@ -528,7 +567,9 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
                                                                            g.set_off, g.set_cnt, g.bucket);
   LAUNCHED();
 
+  prof_end(1, st);
   // ---- S4/S5 probe + replacement
+  prof_begin(2, st);
   SetParams sp{};
   sp.set_off = g.set_off;
   sp.bucket = g.bucket;
@@ -565,8 +606,10 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);
     LAUNCHED();
   }
+  prof_end(2, st);
   // ---- S5 victim admission (PVP)
   if (g.C) {
+    prof_begin(3, st);
     const int qg = grid_for(g.ucap, 256, 2);
     k_qhist<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qcnt);
     LAUNCHED();
@@ -576,8 +619,10 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     LAUNCHED();
     k_admit<<<g.W, 256, 0, st>>>(g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint32_t)g.C, rec);
     LAUNCHED();
+    prof_end(3, st);
   }
   // ---- S6 fill (victim D2H + storage/staging -> slot)
+  prof_begin(4, st);
   {
     uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
     const uint4* tab = reinterpret_cast<const uint4*>(g.table_dev);
@@ -589,7 +634,9 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
       k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
     LAUNCHED();
   }
+  prof_end(4, st);
   // ---- S7/S8 serve: homes signal, requesters pull
+  prof_begin(5, st);
   if (G > 1) {
     for (int r = 0; r < G; ++r)
       if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[G + g.rank], stamp)) return rc;
@@ -610,6 +657,7 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
       k_pull<2><<<blocks, 256, 0, st>>>(node_ids, n, g.N, pa, reinterpret_cast<uint4*>(out), g.nvec);
     LAUNCHED();
   }
+  prof_end(5, st);
   k_end<<<1, 32, 0, st>>>(rec, g.cum, g.scr, (uint64_t)t, g.R);
   LAUNCHED();
   CK(cudaMemcpyAsync(g.bad_dev, &g.scr->bad_ids, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
@@ -628,6 +676,7 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
   if (int rc = check_sticky()) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int G = g.world;
+  if (num_batches > 0) prof_begin(6, st);
   for (int32_t b = 0; b < num_batches; ++b) {
     const int64_t k = first_iter + b;
     const int64_t n = offsets[b + 1] - offsets[b];
@@ -659,6 +708,7 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
     LAUNCHED();
     g.feed_next = k + 1;
   }
+  if (num_batches > 0) prof_end(6, st);
   // ---- S11 PVP copy for iteration t+1 on the side stream (after gather(t))
   if (g.C && g.t_next > 0 && !g.pvp_pending) {
     const int64_t t1 = g.t_next;  // = t + 1
@@ -668,6 +718,7 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
     const uint32_t kq = (uint32_t)(t1 % g.W);
     uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
     const int blocks = g.sms * 2;
+    prof_begin(7, g.side);
     if (g.nvec >= 256)
       k_pvp<8><<<blocks, 256, 0, g.side>>>(kq, (uint32_t)t1, (uint32_t)(t1 + 1), (uint32_t)g.C, (uint32_t)G, g.qlen,
                                            g.qnode, g.qreuse, reinterpret_cast<const uint4*>(g.qrows_dev), pool,
@@ -679,6 +730,7 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
                                            (uint32_t)(g.stage_base0 + par * g.C), g.stg_nodes + par * g.C,
                                            g.vst_stamp, g.vst_idx, g.scr, par, g.nvec);
     LAUNCHED();
+    prof_end(7, g.side);
     CK(cudaEventRecord(g.ev_pvp, g.side));
     g.pvp_pending = true;
   }
@@ -726,6 +778,29 @@ int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count)
     CK(cudaMemcpy(out_host + i, g.hist + (size_t)((first + i) % kHist) * F_NFIELDS, sizeof(lsmgnn_stats_t),
                   cudaMemcpyDeviceToHost));
   return check_sticky();
+}
+
+int lsmgnn_profile(int32_t enable) {
+  g.prof = enable != 0;
+  return 0;
+}
+
+int lsmgnn_profile_read(double* ms, int64_t* cnt) {
+  CK(cudaDeviceSynchronize());
+  if (ms)
+    for (int i = 0; i < LSMGNN_NPHASES; ++i) ms[i] = 0;
+  if (cnt)
+    for (int i = 0; i < LSMGNN_NPHASES; ++i) cnt[i] = 0;
+  for (auto& sp : g.spans) {
+    float x = 0;
+    CK(cudaEventElapsedTime(&x, sp.a, sp.b));
+    if (ms) ms[sp.phase] += x;
+    if (cnt) cnt[sp.phase] += 1;
+    g.ev_pool.push_back(sp.a);
+    g.ev_pool.push_back(sp.b);
+  }
+  g.spans.clear();
+  return 0;
 }
 
 int lsmgnn_finalize(void) {

@@ -234,6 +234,31 @@ def make_trace(g: Graph, G: int, batch: int, fanout, iters: int, seed_train: int
     return trace
 
 
+_PAR_GRAPH = None
+
+
+def _trace_chunk(args):
+    G, batch, fanout, t0, n, seed_train, seed_s, dedup = args
+    return make_trace(_PAR_GRAPH, G, batch, fanout, n, seed_train, seed_s, dedup, t0)
+
+
+def make_trace_parallel(g: Graph, G: int, batch: int, fanout, iters: int, seed_train: int = 3, seed_s: int = 4,
+                        dedup: bool = True, procs: int | None = None):
+    """make_trace split over worker processes (fork); identical output."""
+    import multiprocessing as mp
+    global _PAR_GRAPH
+    procs = procs or min(16, os.cpu_count() or 1)
+    if procs <= 1 or iters < 8:
+        return make_trace(g, G, batch, fanout, iters, seed_train, seed_s, dedup)
+    _PAR_GRAPH = g
+    step = -(-iters // procs)
+    jobs = [(G, batch, fanout, t0, min(step, iters - t0), seed_train, seed_s, dedup) for t0 in range(0, iters, step)]
+    with mp.get_context("fork").Pool(len(jobs)) as pool:
+        parts = pool.map(_trace_chunk, jobs)
+    _PAR_GRAPH = None
+    return [row for part in parts for row in part]
+
+
 def window_union(batch_lists) -> np.ndarray:
     """B_k as a plain set union (sorted) of the ranks' lists — test helper."""
     if not batch_lists:
