@@ -1,0 +1,63 @@
+"""Worker for multi-process tests: one rank of a G-rank run of the CUDA path.
+
+Launched by tests/test_gpu_multiproc.py (GPU) and tests/test_mp_cpu.py (CPU, gloo) with
+torch.distributed.run --nproc-per-node G --master-addr 127.0.0.1. Every rank may share one
+physical GPU (CUDA IPC within a device stands in for NVLink P2P on a 1-GPU pool).
+
+usage: python -m torch.distributed.run ... tests/mp_worker.py MODE OUTDIR [policy pvp]
+  MODE = gather  : run a config-1-shaped trace, save this home's per-iteration counters and
+                   the number of rows that differ from F(v)
+  MODE = cpu     : CPU-only host logic (handle exchange through gloo, layout checks)
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+    mode, outdir = sys.argv[1], sys.argv[2]
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dist.init_process_group("gloo")
+    if mode == "cpu":
+        # host-side bootstrap logic: every rank contributes a blob, all see all in rank order
+        blob = bytes([rank]) * 8
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob)
+        assert blobs == [bytes([r]) * 8 for r in range(world)]
+        import synth
+        g = synth.plcite(4096, 4)
+        tr = synth.make_trace(g, world, 32, (4, 2), 3)
+        mine = [tr[t][rank] for t in range(3)]
+        homes = [np.unique(x % world) for x in mine]
+        json.dump({"rank": rank, "homes": [h.tolist() for h in homes]}, open(os.path.join(outdir, f"r{rank}.json"), "w"))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
+    policy = sys.argv[3] if len(sys.argv) > 3 else "hybrid"
+    pvp = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(rank % ndev)
+    import synth
+    from tests.harness import run_gpu
+    N, D = 16384, 128
+    g = synth.plcite(N, 8)
+    tr = synth.make_trace(g, world, 256, (10, 5), 20)
+    sc = synth.static_scores(g)
+    hist, _, bad = run_gpu(tr, N=N, D=D, L=1024, A=8, scores=sc, policy=policy, pvp=pvp, W=8, V=512,
+                           rank=rank, world=world, group=dist.group.WORLD,
+                           max_batch_ids=max(len(x) for row in tr for x in row))
+    np.save(os.path.join(outdir, f"hist{rank}.npy"), hist)
+    json.dump({"rank": rank, "bad": int(bad)}, open(os.path.join(outdir, f"r{rank}.json"), "w"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,54 @@
+"""G > 1 parity (-m gpu): G processes, one home each, exchanging node IDs, flags and rows
+through CUDA IPC mappings and stream memory operations — the communication layer of
+P:294-313. On a 1-GPU pool all ranks share cuda:0. Every home's per-iteration counters
+must equal the oracle's G-home simulation, and every row must equal F(v)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+
+from .harness import run_oracle
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch(G, tmp, *args, timeout=600):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(ROOT, "tests", "mp_worker.py"), *args]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
+
+
+@pytest.mark.parametrize("G,policy,pvp", [(2, "hybrid", 1), (2, "lru", 0), (3, "hybrid", 0), (4, "static", 1)])
+def test_multiprocess_parity(tmp_path, G, policy, pvp):
+    launch(G, tmp_path, "gather", str(tmp_path), policy, str(pvp))
+    N, D = 16384, 128
+    g = synth.plcite(N, 8)
+    tr = synth.make_trace(g, G, 256, (10, 5), 20)
+    sc = synth.static_scores(g)
+    ho = run_oracle(tr, G=G, N=N, D=D, L=1024, A=8, scores=sc, policy=policy, pvp=pvp, W=8, V=512)
+    for r in range(G):
+        meta = json.load(open(tmp_path / f"r{r}.json"))
+        assert meta["bad"] == 0
+        hg = np.load(tmp_path / f"hist{r}.npy")
+        if not np.array_equal(hg, ho[:, r, :]):
+            bad = np.argwhere(hg != ho[:, r, :])
+            raise AssertionError(f"home {r}: {len(bad)} mismatches, first {bad[0]}: gpu {hg[bad[0][0]]} "
+                                 f"oracle {ho[bad[0][0], r]}")
+    assert ho[:, :, 2].sum() > 0  # peer requests crossed homes
