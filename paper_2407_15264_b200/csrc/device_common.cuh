@@ -27,8 +27,9 @@ struct FillEnt {
   uint32_t src;     // kHostBit|q: backing-table row q; else a pool row (PVP staging)
   uint32_t dst;     // pool row (cache slot or bypass staging)
   uint32_t victim;  // host victim-queue row the OLD content of dst goes to first, or kInvalid
-  uint32_t pad;
+  uint32_t node;    // node v whose row this is (fused delivery walks its request list)
 };
+constexpr uint32_t kDelivered = 0x80000000u;  // node_loc bit: row delivered to `out` by the fill
 // One victim-buffer candidate.
 struct Cand {
   uint32_t x;      // evicted node

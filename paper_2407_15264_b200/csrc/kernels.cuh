@@ -56,7 +56,7 @@ __global__ void k_end(unsigned long long* rec, unsigned long long* cum, Scratch*
 // Validate the caller's int64 IDs and write them (u32) into this home's inbox.
 __global__ void k_route_local(const int64_t* __restrict__ ids, int64_t n, uint64_t N,
                               uint32_t* __restrict__ inbox, uint32_t* __restrict__ inbox_cnt,
-                              Scratch* scr) {
+                              Scratch* scr, uint32_t* __restrict__ inbox_i) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -69,7 +69,10 @@ __global__ void k_route_local(const int64_t* __restrict__ ids, int64_t n, uint64
       if (!ok) atomicAdd(&scr->bad_ids, 1u);
     }
     const uint32_t pos = warp_reserve(inbox_cnt, ok ? 1u : 0u);
-    if (ok) inbox[pos] = v;
+    if (ok) {
+      inbox[pos] = v;
+      if (inbox_i) inbox_i[pos] = (uint32_t)i;
+    }
   }
 }
 
@@ -124,10 +127,13 @@ __global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
 // Home: one representative per distinct node (stamp table indexed by q = v / G),
 // appended to uniq[]; per-set counts for the bucket pass. Requests and peer requests
 // are counted here (every count but `requests` is over unique nodes, R11).
+// With `head` != null (G = 1, fused delivery) it also threads every request position onto
+// its node's list: head[q] = stamp<<32 | last position, nxt[pos] = previous (kInvalid = end).
 __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
                         uint32_t nsrc, uint32_t cap, uint32_t me, uint32_t G, uint32_t S,
                         uint32_t stamp, uint32_t* __restrict__ mark, uint32_t* __restrict__ uniq,
-                        uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* rec) {
+                        uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* rec,
+                        unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt) {
   uint32_t nreq = 0, npeer = 0;
   for (uint32_t r = 0; r < nsrc; ++r) {
     const uint32_t n = inbox_cnt[r];
@@ -142,6 +148,10 @@ __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __re
         const uint32_t q = v / G;
         first = atomicExch(&mark[q], stamp) != stamp;
         if (first) atomicAdd(&set_cnt[q % S], 1u);
+        if (head) {
+          const unsigned long long old = atomicExch(&head[q], ((unsigned long long)stamp << 32) | i);
+          nxt[i] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
+        }
         ++nreq;
         if (r != me) ++npeer;
       }
@@ -240,6 +250,7 @@ struct SetParams {
   uint32_t warp_bytes;   // per-warp shared memory
   uint32_t stage_base;   // pool row of this iteration's PVP staging buffer
   uint32_t bypass_base;  // pool row of the bypass staging area
+  uint32_t deliver;      // kDelivered when k_serve delivers filled rows (G = 1), else 0
 };
 
 enum { C_HIT, C_VHIT, C_STOR, C_INS, C_BYP, C_EVICT, C_EV0, C_EV1, C_EV2, C_EV3, C_ENR, C_N };
@@ -475,9 +486,9 @@ __global__ void k_set(SetParams p) {
         f.src = kind == kVHit ? p.stage_base + p.vst_idx[q] : (kHostBit | q);
         f.dst = slot;
         f.victim = kInvalid;
-        f.pad = 0;
+        f.node = v;
         p.fills[fidx] = f;
-        p.node_loc[q] = slot;
+        p.node_loc[q] = slot | p.deliver;
         p.tags[slot] = v;
         p.last_use[slot] = p.t;
         ++ctr[C_INS];
@@ -513,9 +524,9 @@ __global__ void k_set(SetParams p) {
         f.src = kHostBit | (v / G);
         f.dst = p.bypass_base + b;
         f.victim = kInvalid;
-        f.pad = 0;
+        f.node = v;
         p.fills[fidx] = f;
-        p.node_loc[v / G] = p.bypass_base + b;
+        p.node_loc[v / G] = (p.bypass_base + b) | p.deliver;
       }
     }
     __syncwarp();
@@ -646,7 +657,7 @@ struct PullArgs {
   const uint32_t* node_loc[8];
   uint32_t G;
 };
-template <int UNROLL>
+template <int UNROLL, int OUT>
 __global__ void k_pull(const int64_t* __restrict__ ids, int64_t n, uint64_t N, PullArgs a,
                        uint4* __restrict__ out, uint32_t nvec) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -655,12 +666,76 @@ __global__ void k_pull(const int64_t* __restrict__ ids, int64_t n, uint64_t N, P
     const int64_t x = ids[i];
     uint4* dst = out + (size_t)i * nvec;
     if (x < 0 || (uint64_t)x >= N) {  // ERANGE: zero-filled row
-      for (uint32_t k = lane_id(); k < nvec; k += 32) dst[k] = make_uint4(0, 0, 0, 0);
+      for (uint32_t k = lane_id(); k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
       continue;
     }
     const uint32_t v = (uint32_t)x, g = v % a.G, q = v / a.G;
     const uint32_t loc = a.node_loc[g][q];
-    warp_copy_row<UNROLL, kDev, kDev>(dst, a.pool[g] + (size_t)loc * nvec, nvec);
+    warp_copy_row<UNROLL, kDev, OUT>(dst, a.pool[g] + (size_t)(loc & ~kDelivered) * nvec, nvec);
+  }
+}
+
+// ------------------------------------------------------------------------------ S6+S8 fused (G = 1)
+// One launch serves the whole batch. Fill warps stream each missing row from the backing
+// table (PCIe) or PVP staging into registers once and store it to its cache slot / bypass
+// row AND to every requester position of that node (the request list built by k_dedup) —
+// the storage read and the delivery overlap, and the row is never re-read from HBM. The
+// remaining warps (1 in 8) copy rows not delivered by a fill (hits, staged rows served in
+// place) from HBM into `out`, concurrently with the PCIe-bound fills.
+template <int UNROLL, int OUT>
+__global__ void k_serve(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
+                        const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
+                        const unsigned long long* __restrict__ head, const uint32_t* __restrict__ nxt,
+                        const uint32_t* __restrict__ inbox_i, uint32_t stamp, const int64_t* __restrict__ ids,
+                        int64_t n, uint64_t N, const uint32_t* __restrict__ node_loc, uint4* __restrict__ out) {
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t npull = nw >= 8 ? nw / 8 : 1;
+  const int lane = (int)lane_id();
+  if (gw < npull) {  // ---- pull warps: rows not delivered by a fill
+    for (int64_t i = gw; i < n; i += npull) {
+      const int64_t x = ids[i];
+      uint4* dst = out + (size_t)i * nvec;
+      if (x < 0 || (uint64_t)x >= N) {
+        for (uint32_t k = lane; k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
+        continue;
+      }
+      const uint32_t loc = node_loc[(uint32_t)x];
+      if (loc & kDelivered) continue;
+      warp_copy_row<UNROLL, kDev, OUT>(dst, pool + (size_t)loc * nvec, nvec);
+    }
+    return;
+  }
+  const uint32_t nf = scr->nfill;
+  for (uint32_t e = gw - npull; e < nf; e += nw - npull) {
+    const FillEnt f = fills[e];
+    uint4* slot = pool + (size_t)f.dst * nvec;
+    if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, slot, nvec);
+    const bool from_host = (f.src & kHostBit) != 0;
+    const uint4* src = from_host ? table + (size_t)(f.src & ~kHostBit) * nvec : pool + (size_t)f.src * nvec;
+    const unsigned long long h = head[f.node];
+    const uint32_t first = (uint32_t)(h >> 32) == stamp ? (uint32_t)h : kInvalid;
+    for (uint32_t base = 0; base < nvec; base += 32 * UNROLL) {
+      uint4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint32_t k = base + lane + 32 * u;
+        if (k < nvec) v[u] = from_host ? ld16<kHost>(src + k) : ld16<kDev>(src + k);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint32_t k = base + lane + 32 * u;
+        if (k < nvec) st16<kDev>(slot + k, v[u]);
+      }
+      for (uint32_t pos = first; pos != kInvalid; pos = nxt[pos]) {
+        uint4* dst = out + (size_t)inbox_i[pos] * nvec;
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const uint32_t k = base + lane + 32 * u;
+          if (k < nvec) st16<OUT>(dst + k, v[u]);
+        }
+      }
+    }
   }
 }
 

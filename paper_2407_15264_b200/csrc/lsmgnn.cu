@@ -63,6 +63,8 @@ struct Ctx {
   uint32_t *bucket = nullptr, *uniq = nullptr, *ring = nullptr, *ring_len = nullptr;
   uint32_t *qcnt = nullptr, *qoff = nullptr, *qb = nullptr, *qlen = nullptr, *qnode = nullptr;
   uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr, *local_inbox_cnt = nullptr;
+  unsigned long long* head = nullptr;            // G = 1 fused delivery: per-node request list heads
+  uint32_t *nxt = nullptr, *inbox_i = nullptr;   // next position / original request index
   uint8_t* score = nullptr;
   FillEnt* fills = nullptr;
   Cand* cands = nullptr;
@@ -242,7 +244,8 @@ int free_all() {
   cudaDeviceSynchronize();
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off,
                   g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
-                  g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.score, g.fills, g.cands, g.scr, g.hist,
+                  g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.head, g.nxt, g.inbox_i, g.score, g.fills, g.cands,
+                  g.scr, g.hist,
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -405,6 +408,11 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.stg_nodes, std::max<uint64_t>(1, 2 * g.C));
   DA(g.route_cnt, G);
   DA(g.local_inbox_cnt, 1);
+  if (G == 1) {
+    DA(g.head, g.Q);
+    DA(g.nxt, g.cap);
+    DA(g.inbox_i, g.cap);
+  }
   DA(g.score, g.Q);
   DA(g.fills, g.ucap);
   DA(g.cands, g.ucap);
@@ -520,6 +528,19 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   if (n > 0 && (!node_ids || !out)) return set_err(LSMGNN_EINVAL, "null ids/out");
   if (reinterpret_cast<uintptr_t>(out) % 16) return set_err(LSMGNN_EINVAL, "out must be 16-byte aligned");
   if (int rc = check_sticky()) return rc;
+  // `out` may be device memory or pinned (mapped) host memory: rows are then stored over PCIe
+  bool out_host = false;
+  if (n > 0) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, out) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
+      cudaGetLastError();
+      return set_err(LSMGNN_EINVAL, "out must be device memory or pinned host memory");
+    }
+    if (at.type == cudaMemoryTypeHost) {
+      out_host = true;
+      out = at.devicePointer;
+    }
+  }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int G = g.world;
   const int64_t t = g.t_next;
@@ -540,7 +561,8 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   if (G == 1) {
     CK(cudaMemsetAsync(g.local_inbox_cnt, 0, sizeof(uint32_t), st));
     if (n > 0) {
-      k_route_local<<<grid_for(n, 256), 256, 0, st>>>(node_ids, n, g.N, inbox_of(g.arena), g.local_inbox_cnt, g.scr);
+      k_route_local<<<grid_for(n, 256), 256, 0, st>>>(node_ids, n, g.N, inbox_of(g.arena), g.local_inbox_cnt, g.scr,
+                                                      g.inbox_i);
       LAUNCHED();
     }
     inbox = inbox_of(g.arena);
@@ -557,7 +579,7 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   const int64_t maxreq = (int64_t)g.cap * G;
   k_dedup<<<grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n, 1) * G), 256, 4), 256, 0, st>>>(
       inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, stamp, g.mark,
-      g.uniq, g.set_cnt, g.scr, rec);
+      g.uniq, g.set_cnt, g.scr, rec, G == 1 ? g.head : nullptr, g.nxt);
   LAUNCHED();
   const uint32_t par = (uint32_t)(t & 1);
   k_scan<<<1, 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes + par * g.C : nullptr,
@@ -601,6 +623,7 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   sp.warp_bytes = g.warp_bytes;
   sp.stage_base = (uint32_t)(g.stage_base0 + par * g.C);
   sp.bypass_base = (uint32_t)g.bypass_base;
+  sp.deliver = G == 1 ? kDelivered : 0u;
   {
     const int64_t blocks = std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * 8);
     k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);
@@ -621,41 +644,56 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     LAUNCHED();
     prof_end(3, st);
   }
-  // ---- S6 fill (victim D2H + storage/staging -> slot)
-  prof_begin(4, st);
-  {
-    uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
-    const uint4* tab = reinterpret_cast<const uint4*>(g.table_dev);
-    uint4* hq = reinterpret_cast<uint4*>(g.qrows_dev);
+  // ---- S6 fill (victim D2H + storage/staging -> slot) and S7/S8 serve
+  uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
+  const uint4* tab = reinterpret_cast<const uint4*>(g.table_dev);
+  uint4* hq = reinterpret_cast<uint4*>(g.qrows_dev);
+  uint4* o4 = reinterpret_cast<uint4*>(out);
+  const bool wide = g.nvec >= 256;
+  if (G == 1) {
+    // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits
+    prof_begin(4, st);
     const int blocks = g.sms * 4;
-    if (g.nvec >= 256)
+#define SERVE(U, O)                                                                                              \
+  k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.inbox_i, stamp, \
+                                        node_ids, n, g.N, loc_of(g.arena), o4)
+    if (wide && !out_host) SERVE(8, kDev);
+    else if (wide) SERVE(8, kHost);
+    else if (!out_host) SERVE(2, kDev);
+    else SERVE(2, kHost);
+#undef SERVE
+    LAUNCHED();
+    prof_end(4, st);
+    prof_begin(5, st);
+  } else {
+    prof_begin(4, st);
+    const int blocks = g.sms * 4;
+    if (wide)
       k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
     else
       k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
     LAUNCHED();
-  }
-  prof_end(4, st);
-  // ---- S7/S8 serve: homes signal, requesters pull
-  prof_begin(5, st);
-  if (G > 1) {
+    prof_end(4, st);
+    // homes signal "served", requesters wait for every home, then pull
+    prof_begin(5, st);
     for (int r = 0; r < G; ++r)
       if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[G + g.rank], stamp)) return rc;
     for (int h = 0; h < G; ++h)
       if (int rc = flag_wait(st, &flags_of(g.arena)[G + h], stamp)) return rc;
-  }
-  if (n > 0) {
-    PullArgs pa{};
-    for (int h = 0; h < G; ++h) {
-      pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
-      pa.node_loc[h] = loc_of(g.peer_arena[h]);
+    if (n > 0) {
+      PullArgs pa{};
+      for (int h = 0; h < G; ++h) {
+        pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
+        pa.node_loc[h] = loc_of(g.peer_arena[h]);
+      }
+      pa.G = (uint32_t)G;
+      const int pblocks = grid_for(n * 32, 256, 8);
+      if (wide && !out_host) k_pull<8, kDev><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
+      else if (wide) k_pull<8, kHost><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
+      else if (!out_host) k_pull<2, kDev><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
+      else k_pull<2, kHost><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
+      LAUNCHED();
     }
-    pa.G = (uint32_t)G;
-    const int blocks = grid_for(n * 32, 256, 8);
-    if (g.nvec >= 256)
-      k_pull<8><<<blocks, 256, 0, st>>>(node_ids, n, g.N, pa, reinterpret_cast<uint4*>(out), g.nvec);
-    else
-      k_pull<2><<<blocks, 256, 0, st>>>(node_ids, n, g.N, pa, reinterpret_cast<uint4*>(out), g.nvec);
-    LAUNCHED();
   }
   prof_end(5, st);
   k_end<<<1, 32, 0, st>>>(rec, g.cum, g.scr, (uint64_t)t, g.R);
@@ -691,7 +729,8 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
     if (G == 1) {
       CK(cudaMemsetAsync(g.ring_len + slot, 0, sizeof(uint32_t), st));
       if (n > 0) {
-        k_route_local<<<grid_for(n, 256), 256, 0, st>>>(ids + offsets[b], n, g.N, ring_slot, g.ring_len + slot, g.scr);
+        k_route_local<<<grid_for(n, 256), 256, 0, st>>>(ids + offsets[b], n, g.N, ring_slot, g.ring_len + slot, g.scr,
+                                                        nullptr);
         LAUNCHED();
       }
     } else {
@@ -742,13 +781,20 @@ int lsmgnn_gather_host(const int64_t* host_ids, int64_t n, void* host_out, void*
   if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
   if (n < 0 || (uint64_t)n > g.cap) return set_err(LSMGNN_EINVAL, "bad n");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (!g.tmp_ids) {
-    CK(cudaMalloc(reinterpret_cast<void**>(&g.tmp_ids), g.cap * sizeof(int64_t)));
-    CK(cudaMalloc(&g.tmp_out, g.cap * (size_t)g.R));
-  }
+  if (!g.tmp_ids) CK(cudaMalloc(reinterpret_cast<void**>(&g.tmp_ids), g.cap * sizeof(int64_t)));
   if (n > 0) CK(cudaMemcpyAsync(g.tmp_ids, host_ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  if (int rc = lsmgnn_gather(g.tmp_ids, n, g.tmp_out, stream)) return rc;
-  if (n > 0) CK(cudaMemcpyAsync(host_out, g.tmp_out, n * (size_t)g.R, cudaMemcpyDeviceToHost, st));
+  // pinned host `out`: the serve kernels store the rows straight over PCIe (D2H overlaps the
+  // storage H2D of the same launch); pageable `out`: device staging + cudaMemcpy
+  cudaPointerAttributes at{};
+  const bool pinned = n > 0 && cudaPointerGetAttributes(&at, host_out) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (pinned || n == 0) {
+    if (int rc = lsmgnn_gather(g.tmp_ids, n, host_out, stream)) return rc;
+  } else {
+    if (!g.tmp_out) CK(cudaMalloc(&g.tmp_out, g.cap * (size_t)g.R));
+    if (int rc = lsmgnn_gather(g.tmp_ids, n, g.tmp_out, stream)) return rc;
+    CK(cudaMemcpyAsync(host_out, g.tmp_out, n * (size_t)g.R, cudaMemcpyDeviceToHost, st));
+  }
   CK(cudaStreamSynchronize(st));
   return check_sticky();
 }
