@@ -186,12 +186,19 @@ def main():
 
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    local = local % ndev  # ranks may share a device on a 1-GPU pool (CUDA IPC within one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
+    cdev = dev  # device of the control-collective tensors
     if G > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if ndev >= G:
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # NCCL refuses two ranks on one GPU; the data path never uses NCCL anyway
+            dist.init_process_group("gloo")
+            cdev = torch.device("cpu")
         pg = dist.group.WORLD
     from paper_2407_15264_b200 import LsmGnn
     from tests.harness import table_for
@@ -259,7 +266,7 @@ def main():
     per_step = [a.elapsed_time(b) for a, b in ev]
     my_bytes = sum(mine[Wu + i].size for i in range(K)) * wl.R
     if G > 1:
-        x = torch.tensor([T, float(my_bytes)], dtype=torch.float64, device=dev)
+        x = torch.tensor([T, float(my_bytes)], dtype=torch.float64, device=cdev)
         tmax = x[:1].clone()
         torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
         tot = x[1:].clone()
@@ -291,10 +298,10 @@ def main():
             h2d += hids[i].numel() * 8
             d2h += hids[i].numel() * wl.R
         if G > 1:
-            x = torch.tensor([tsum], dtype=torch.float64, device=dev)
+            x = torch.tensor([tsum], dtype=torch.float64, device=cdev)
             torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
             tsum = float(x.item())
-            y = torch.tensor([float(eb)], dtype=torch.float64, device=dev)
+            y = torch.tensor([float(eb)], dtype=torch.float64, device=cdev)
             torch.distributed.all_reduce(y, op=torch.distributed.ReduceOp.SUM)
             eb = float(y.item())
         e2e = {"value": round(eb / tsum / 1e9, 4), "unit": "GB/s", "h2d_bytes_per_step": int(h2d / E),

@@ -13,7 +13,7 @@
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
 
-template <int U>
+template <int U, int MODE>
 __global__ void k_ldg(const uint4* __restrict__ host, const uint32_t* __restrict__ rows, uint32_t n,
                       uint4* __restrict__ dst, int nvec) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -21,10 +21,15 @@ __global__ void k_ldg(const uint4* __restrict__ host, const uint32_t* __restrict
   for (uint32_t e = warp; e < n; e += nw) {
     const uint4* s = host + (size_t)rows[e] * nvec;
     uint4* d = dst + (size_t)e * nvec;
+    if (MODE == 3 && lane == 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s), "r"(nvec * 16) : "memory");
     for (int i = lane; i < nvec; i += 32 * U) {
       uint4 v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) if (i + 32 * u < nvec) asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(s + i + 32 * u));
+      for (int u = 0; u < U; ++u) if (i + 32 * u < nvec) {
+        if (MODE == 0) asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(s + i + 32 * u));
+        else if (MODE == 1) asm volatile("ld.global.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(s + i + 32 * u));
+        else asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(s + i + 32 * u));
+      }
 #pragma unroll
       for (int u = 0; u < U; ++u) if (i + 32 * u < nvec) d[i + 32 * u] = v[u];
     }
@@ -135,13 +140,17 @@ int main(int argc, char** argv) {
   for (int blocks : {sms, 2 * sms, 4 * sms}) {
     char nm[64];
     snprintf(nm, 64, "ldg U=8 grid=%d x256", blocks);
-    timeit(nm, [&] { k_ldg<8><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
-    snprintf(nm, 64, "ldg U=4 grid=%d x256", blocks);
-    timeit(nm, [&] { k_ldg<4><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
+    timeit(nm, [&] { k_ldg<8, 0><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
+    snprintf(nm, 64, "ldg L2::256B U=8 grid=%d", blocks);
+    timeit(nm, [&] { k_ldg<8, 1><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
+    snprintf(nm, 64, "ldg.nc L2::256B U=8 grid=%d", blocks);
+    timeit(nm, [&] { k_ldg<8, 2><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
+    snprintf(nm, 64, "bulk.prefetch.L2 + ldg U=8 grid=%d", blocks);
+    timeit(nm, [&] { k_ldg<8, 3><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
   }
-  for (int stages : {2, 4}) {
-    for (int warps : {4, 8}) {
-      for (uint32_t chunk : {4096u, 1024u, 512u}) {
+  for (int stages : {4}) {
+    for (int warps : {8}) {
+      for (uint32_t chunk : {4096u}) {
         size_t smem = (size_t)warps * stages * R;
         char nm[96];
         snprintf(nm, 96, "tma st=%d warps=%d chunk=%u grid=%d", stages, warps, chunk, sms);
