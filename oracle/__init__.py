@@ -34,7 +34,8 @@ COUNT_FIELDS = ["iter", "requests", "peer_requests", "unique", "hits", "victim_h
 class _Config(ctypes.Structure):
     _fields_ = [("G", ctypes.c_int32), ("N", ctypes.c_int64), ("R", ctypes.c_int32), ("L", ctypes.c_int64),
                 ("A", ctypes.c_int32), ("policy", ctypes.c_int32), ("pvp", ctypes.c_int32), ("W", ctypes.c_int32),
-                ("T", ctypes.c_int32), ("reinsert", ctypes.c_int32), ("V", ctypes.c_int64)]
+                ("T", ctypes.c_int32), ("reinsert", ctypes.c_int32), ("V", ctypes.c_int64),
+                ("P", ctypes.c_int32)]
 
 
 _LIB = None
@@ -87,10 +88,10 @@ def _concat(lists):
 class Oracle:
     """One simulated box of G homes. ``gather(t, lists)`` returns (counts[G, 24], out)."""
 
-    def __init__(self, G, N, R, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, reinsert=1, V=0):
+    def __init__(self, G, N, R, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, reinsert=1, V=0, P=1):
         self.G, self.N, self.R, self.L, self.A, self.W = G, N, R, L, A, W
         self.policy = POLICIES[policy] if isinstance(policy, str) else policy
-        cfg = _Config(G, N, R, L, A, self.policy, pvp, W, T, reinsert, V)
+        cfg = _Config(G, N, R, L, A, self.policy, pvp, W, T, reinsert, V, P)
         self._scores = np.ascontiguousarray(scores, dtype=np.uint8)
         assert self._scores.size == N
         self._o = _lib().orc_create(ctypes.byref(cfg), self._scores.ctypes.data)

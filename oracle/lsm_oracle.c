@@ -47,6 +47,9 @@ typedef struct { int64_t x, reuse; } qent;
 typedef struct {
     int64_t* tag;       /* [S*A], NONE = invalid */
     int64_t* last_use;  /* [S*A] */
+    int64_t* info;      /* [S*A] dynamic information of the line: next reuse iteration recorded
+                           by the last window scan, NONE (no reuse found) or FRESH (inserted
+                           after the scan) — the three states of draft P:333 */
     int32_t* rr;        /* [S] round-robin cursor */
     qent**   q;         /* [W] victim queues */
     int64_t* qlen;      /* [W] */
@@ -124,12 +127,27 @@ static int64_t next_use(orc_t* o, int64_t v, int64_t t) {
     return NONE;
 }
 
-/* Class of a resident line holding x at gather(t) (R4:
- * Near <=> d <= T, Far <=> d > T; Fresh needs an update period P > 1, not modelled). */
-static int cls_of(orc_t* o, int64_t x, int64_t t) {
-    int64_t k = next_use(o, x, t);
-    if (k == NONE) return ORC_NOREUSE;
-    return (k - t) <= o->c.T ? ORC_NEAR : ORC_FAR;
+#define FRESH (-2)
+
+/* Is gather(t) a dynamic-information update iteration? The window scan runs every P
+ * iterations ("updates the dynamic information for a configurable number of
+ * iterations"; R6); P <= 1 scans before every gather. */
+static int is_update(const orc_t* o, int64_t t) { return o->c.P <= 1 || t % o->c.P == 0; }
+
+/* Class from a line's dynamic information at gather(t) (R4, R7):
+ * FRESH (inserted after the last scan, draft P:333 "recently inserted") or a recorded
+ * reuse that has already passed (stale) -> Fresh; NONE -> NoReuse; else d = info - t:
+ * Near if d <= T, Far otherwise. */
+static int cls_from_info(const orc_t* o, int64_t info, int64_t t) {
+    if (info == NONE) return ORC_NOREUSE;
+    if (info == FRESH || info <= t) return ORC_FRESH;
+    return (info - t) <= o->c.T ? ORC_NEAR : ORC_FAR;
+}
+
+/* Information an incoming miss has when the batch is decided: exact at an update
+ * iteration (the scan precedes aggregation), none yet otherwise (Fresh). */
+static int64_t incoming_info(orc_t* o, int64_t v, int64_t t) {
+    return is_update(o, t) ? next_use(o, v, t) : FRESH;
 }
 
 /* Priority level (rank) of a class: lowest evicted first.
@@ -144,24 +162,25 @@ static int64_t rank_of(const orc_t* o, int cls) {
     }
 }
 
-/* Eviction key of a line holding x with last use lu at gather(t); smallest goes first.
+/* Eviction key of a line holding x (last use lu, dynamic info `info`) at gather(t);
+ * smallest goes first.
  *   HYBRID  (rank(class), score, x)      P:361 "lowest static priority value"; tie by node (R8)
  *   STATIC  (0, score, x)                P:645 static-only
  *   LRU     (0, last_use, x)             north-star baseline (R20)
  *   DYNAMIC NoReuse (0,0,x), Fresh (1,0,x), reuse d (2, W-d, x)   P:645 dynamic-only (R19)
  *   RR      (0, 0, x) — only used to order bypassed misses (R20) */
-static key3 key_of(orc_t* o, int64_t x, int64_t lu, int64_t t) {
+static key3 key_of(orc_t* o, int64_t x, int64_t lu, int64_t info, int64_t t) {
     key3 k = {0, 0, x};
+    const int cls = cls_from_info(o, info, t);
     switch (o->c.policy) {
-        case ORC_HYBRID: k.k0 = rank_of(o, cls_of(o, x, t)); k.k1 = o->score[x]; break;
+        case ORC_HYBRID: k.k0 = rank_of(o, cls); k.k1 = o->score[x]; break;
         case ORC_STATIC: k.k1 = o->score[x]; break;
         case ORC_LRU:    k.k1 = lu; break;
-        case ORC_DYNAMIC: {
-            int64_t n = next_use(o, x, t);
-            if (n == NONE) { k.k0 = 0; k.k1 = 0; }
-            else { k.k0 = 2; k.k1 = o->c.W - (n - t); }
+        case ORC_DYNAMIC:
+            if (cls == ORC_NOREUSE) { k.k0 = 0; k.k1 = 0; }
+            else if (cls == ORC_FRESH) { k.k0 = 1; k.k1 = 0; }
+            else { k.k0 = 2; k.k1 = o->c.W - (info - t); }
             break;
-        }
         default: break;
     }
     return k;
@@ -186,6 +205,8 @@ orc_t* orc_create(const orc_config* cfg, const uint8_t* scores) {
         home_t* h = &o->home[g];
         h->tag = malloc((size_t)cfg->L * sizeof(int64_t));
         h->last_use = calloc((size_t)cfg->L, sizeof(int64_t));
+        h->info = malloc((size_t)cfg->L * sizeof(int64_t));
+        for (int64_t i = 0; i < cfg->L; ++i) h->info[i] = NONE;
         for (int64_t i = 0; i < cfg->L; ++i) h->tag[i] = NONE;
         h->rr = calloc((size_t)o->S, sizeof(int32_t));
         h->q = calloc((size_t)cfg->W, sizeof(qent*));
@@ -207,7 +228,7 @@ void orc_destroy(orc_t* o) {
     if (!o) return;
     if (o->home) for (int g = 0; g < o->c.G; ++g) {
         home_t* h = &o->home[g];
-        free(h->tag); free(h->last_use); free(h->rr);
+        free(h->tag); free(h->last_use); free(h->info); free(h->rr);
         for (int k = 0; k < o->c.W; ++k) free(h->q[k]);
         free(h->q); free(h->qlen); free(h->staging);
     }
@@ -291,6 +312,13 @@ static void gather_home(orc_t* o, int g, int64_t t, const int64_t* ids, const in
     memset(cnt, 0, sizeof *cnt);
     cnt->iter = (uint64_t)t;
 
+    /* window scan ("scans the sampled nodes in the window buffer to determine the
+     * next reuse iteration for the cache-lines that currently reside in the cache before
+     * the feature aggregation stage"), every P iterations */
+    if (is_update(o, t))
+        for (int64_t i = 0; i < o->c.L; ++i)
+            h->info[i] = h->tag[i] == NONE ? NONE : next_use(o, h->tag[i], t);
+
     /* Req = [(r,i,v) : v = batch_r(t)[i], home(v) = g]  (P:296 split by hash) */
     int64_t total = offs[o->c.G] - offs[0];
     int64_t* U = malloc((size_t)(total > 0 ? total : 1) * sizeof(int64_t));
@@ -348,6 +376,7 @@ static void gather_home(orc_t* o, int g, int64_t t, const int64_t* ids, const in
         while (q < no && set_of(o, U[order[q]]) == s) ++q;
         int64_t* tag = h->tag + s * A;
         int64_t* lu = h->last_use + s * A;
+        int64_t* info = h->info + s * A;
         /* H = ways whose tag is requested: protected for the whole batch (R10) */
         for (int w = 0; w < A; ++w) { prot[w] = 0; filled[w] = 0; }
         int64_t nH = 0, nM = 0;
@@ -360,7 +389,7 @@ static void gather_home(orc_t* o, int g, int64_t t, const int64_t* ids, const in
                 /* M = misses to insert (R15: victim-buffer hits re-inserted unless reinsert=0) */
                 M[nM].v = v;
                 /* incoming key = key as if resident with last_use = t (R10) */
-                M[nM].k = key_of(o, v, t, t);
+                M[nM].k = key_of(o, v, t, incoming_info(o, v, t), t);
                 nM++;
             }
         }
@@ -393,7 +422,7 @@ static void gather_home(orc_t* o, int g, int64_t t, const int64_t* ids, const in
                 key3 best = {0, 0, 0};
                 for (int ww = 0; ww < A; ++ww) {
                     if (prot[ww] || filled[ww]) continue;
-                    key3 k = key_of(o, tag[ww], lu[ww], t);
+                    key3 k = key_of(o, tag[ww], lu[ww], info[ww], t);
                     if (w < 0 || key_less(k, best)) { w = ww; best = k; }
                 }
             }
@@ -401,22 +430,25 @@ static void gather_home(orc_t* o, int g, int64_t t, const int64_t* ids, const in
                 /* evict x: count by class; with PVP a line that has a next
                  * reuse iteration becomes a victim-buffer candidate, else it is discarded */
                 int64_t x = tag[w];
-                key3 kx = key_of(o, x, lu[w], t);
+                key3 kx = key_of(o, x, lu[w], info[w], t);
                 log_event(o, g, s, 0, x, kx);
                 cnt->evictions++;
-                cnt->evict_by_class[cls_of(o, x, t)]++;
-                int64_t nx = next_use(o, x, t);
-                if (o->c.pvp && nx != NONE) { cand[ncand].x = x; cand[ncand].reuse = nx; ncand++; }
-                else cnt->evicted_no_reuse++;
+                const int cx = cls_from_info(o, info[w], t);
+                cnt->evict_by_class[cx]++;
+                if (o->c.pvp && (cx == ORC_NEAR || cx == ORC_FAR)) {
+                    cand[ncand].x = x; cand[ncand].reuse = info[w]; ncand++;
+                } else {
+                    cnt->evicted_no_reuse++;
+                }
             }
-            tag[w] = v; lu[w] = t; filled[w] = 1;
+            tag[w] = v; lu[w] = t; info[w] = FRESH; filled[w] = 1;
             cnt->inserted++;
-            log_event(o, g, s, 3, v, key_of(o, v, t, t));
+            log_event(o, g, s, 3, v, key_of(o, v, t, incoming_info(o, v, t), t));
         }
         /* survivors for the class-minimality invariant (I6) */
         for (int w = 0; w < A; ++w)
             if (tag[w] != NONE && !prot[w] && !filled[w])
-                log_event(o, g, s, 1, tag[w], key_of(o, tag[w], lu[w], t));
+                log_event(o, g, s, 1, tag[w], key_of(o, tag[w], lu[w], info[w], t));
         free(ins);
         p = q;
     }

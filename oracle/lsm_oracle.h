@@ -33,6 +33,7 @@ typedef struct {
     int32_t T;            /* threshold; 0 => max(1, W/8) */
     int32_t reinsert;     /* 1: victim-buffer hits are re-inserted (R15) */
     int64_t V;            /* victim lines per home; C = V / W lines per queue */
+    int32_t P;            /* dynamic-information update period; 0 or 1 = every iteration */
 } orc_config;
 
 /* Per (iteration, home) counters, field order identical to lsmgnn_stats_t in

@@ -107,7 +107,7 @@ class LsmGnn:
     """
 
     def __init__(self, num_nodes, feat_dim, lines_per_gpu, ways, victim_lines=0, scores=None, *, dtype=F32,
-                 policy="hybrid", pvp=0, window=256, threshold=0, reinsert=1, max_batch_ids=1 << 20,
+                 policy="hybrid", pvp=0, window=256, threshold=0, reinsert=1, max_batch_ids=1 << 20, period=1,
                  rank=0, world=1, device=None, group=None):
         import torch
         if not torch.cuda.is_available():
@@ -124,7 +124,7 @@ class LsmGnn:
         self._keep = []
         _check(L.lsmgnn_bind(rank, world, device))
         opt = Options(1, POLICY[policy] if isinstance(policy, str) else int(policy), int(pvp), int(window),
-                      int(threshold), 1, int(reinsert), int(max_batch_ids))
+                      int(threshold), int(period), int(reinsert), int(max_batch_ids))
         _check(L.lsmgnn_set_options(ctypes.byref(opt)))
         sp = None
         if scores is not None:

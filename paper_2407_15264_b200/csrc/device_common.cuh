@@ -9,6 +9,8 @@ namespace lsm {
 
 constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // empty cache way / "no victim slot"
 constexpr uint32_t kHostBit = 0x80000000u;  // FillEnt::src: bit 31 set => backing-table row q
+constexpr uint32_t kInfoNone = 0xFFFFFFFFu;  // line snapshot: no reuse found in the window
+constexpr uint32_t kInfoFresh = 0xFFFFFFFEu; // line snapshot: inserted after the last scan
 
 // Dynamic-information classes; index of evict_by_class[].
 enum Cls : int { kNoReuse = 0, kFar = 1, kFresh = 2, kNear = 3 };

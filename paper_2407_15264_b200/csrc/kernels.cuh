@@ -227,6 +227,23 @@ __global__ void k_bucket(const uint32_t* __restrict__ uniq, const Scratch* scr, 
   }
 }
 
+// ------------------------------------------------------------------------------ S4 (period > 1)
+// Window scan of every resident line ("scans the sampled nodes in the window buffer to
+// determine the next reuse iteration for the cache-lines that currently reside in the cache
+// before the feature aggregation stage"), run every P-th iteration.
+__global__ void k_snapshot(const uint32_t* __restrict__ tags, uint32_t L, uint32_t G, const uint32_t* __restrict__ mask,
+                           uint32_t MW, uint32_t p0, uint32_t W, uint32_t t, uint32_t* __restrict__ line_info) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    const uint32_t x = tags[i];
+    uint32_t info = kInfoNone;
+    if (x != kInvalid) {
+      const int d = next_reuse_d(mask + (size_t)(x / G) * MW, (int)p0, (int)W);
+      if (d) info = t + (uint32_t)d;
+    }
+    line_info[i] = info;
+  }
+}
+
 // ------------------------------------------------------------------------------ S4 + S5
 struct SetParams {
   const uint32_t* set_off;
@@ -247,6 +264,8 @@ struct SetParams {
   uint32_t policy, pvp, reinsert;
   uint32_t t, stamp, p0;
   uint32_t P;            // per-warp capacity (power of two >= max bucket)
+  uint32_t period;       // dynamic-information update period; 1 = exact every batch
+  uint32_t* line_info;   // period > 1: per-line snapshot (reuse iteration / kInfoNone / kInfoFresh)
   uint32_t warp_bytes;   // per-warp shared memory
   uint32_t stage_base;   // pool row of this iteration's PVP staging buffer
   uint32_t bypass_base;  // pool row of the bypass staging area
@@ -267,18 +286,29 @@ __device__ __forceinline__ uint64_t level_of(int cls, uint32_t pvp) {
 __device__ __forceinline__ int class_of(int d, uint32_t T) {
   return d == 0 ? kNoReuse : ((uint32_t)d <= T ? kNear : kFar);
 }
+// Class and reuse distance of a line from its snapshot (period > 1): none -> NoReuse;
+// inserted after the scan, or a recorded reuse already passed -> Fresh (R7).
+__device__ __forceinline__ int class_of_info(uint32_t info, uint32_t t, uint32_t T, int* d) {
+  *d = 0;
+  if (info == kInfoNone) return kNoReuse;
+  if (info == kInfoFresh || info <= t) return kFresh;
+  *d = (int)(info - t);
+  return (uint32_t)*d <= T ? kNear : kFar;
+}
 // 64-bit eviction key, smallest evicted first; the node ID in the low 32 bits makes
 // every key unique (tie-break by node, R8).
-__device__ __forceinline__ uint64_t policy_key(const SetParams& p, uint32_t v, uint32_t lu, int d) {
+__device__ __forceinline__ uint64_t policy_key(const SetParams& p, uint32_t v, uint32_t lu, int cls, int d) {
   switch (p.policy) {
     case 0:  // HYBRID: (level, static score, node)
-      return (level_of(class_of(d, p.T), p.pvp) << 40) | ((uint64_t)p.score[v / p.G] << 32) | v;
+      return (level_of(cls, p.pvp) << 40) | ((uint64_t)p.score[v / p.G] << 32) | v;
     case 1:  // STATIC: (score, node)
       return ((uint64_t)p.score[v / p.G] << 32) | v;
     case 2:  // LRU: (last use, node)
       return ((uint64_t)lu << 32) | v;
-    case 4:  // DYNAMIC: no reuse first, then farthest reuse
-      return d == 0 ? (uint64_t)v : ((2ull << 48) | ((uint64_t)(p.W - d) << 32) | v);
+    case 4:  // DYNAMIC: no reuse first, then recently inserted, then farthest reuse
+      return cls == kNoReuse ? (uint64_t)v
+             : cls == kFresh ? ((1ull << 48) | v)
+                             : ((2ull << 48) | ((uint64_t)(p.W - d) << 32) | v);
     default:  // RR: bypass order only
       return v;
   }
@@ -300,6 +330,8 @@ __global__ void k_set(SetParams p) {
   uint32_t* stag = reinterpret_cast<uint32_t*>(skey + p.P);
   uint32_t* svict = stag + 32;
   int* sd = reinterpret_cast<int*>(svict + 32);
+  int* scls = sd + 32;
+  const bool upd = p.period <= 1 || p.t % p.period == 0;  // exact information for incoming misses
 
   uint32_t ctr[C_N];
 #pragma unroll
@@ -320,9 +352,17 @@ __global__ void k_set(SetParams p) {
       lu = p.last_use[s * A + lane];
     }
     stag[lane] = tg;
-    int d = 0;  // next reuse distance of the resident node (0 = none in the window)
-    if (tg != kInvalid) d = next_reuse_d(p.mask + (size_t)(tg / G) * p.MW, p.p0, p.W);
+    int d = 0, cls = kNoReuse;  // next reuse distance (0 = none) and class of the resident line
+    if (tg != kInvalid) {
+      if (p.period <= 1) {  // exact, from the window bitmask (P = 1)
+        d = next_reuse_d(p.mask + (size_t)(tg / G) * p.MW, p.p0, p.W);
+        cls = class_of(d, p.T);
+      } else {              // the last window scan's snapshot
+        cls = class_of_info(p.line_info[s * A + lane], p.t, p.T, &d);
+      }
+    }
     sd[lane] = d;
+    scls[lane] = cls;
     __syncwarp();
     warp_bitonic_sort(sv, (int)Pm);  // nodes ascending (R10: misses installed in node order)
 
@@ -377,9 +417,12 @@ __global__ void k_set(SetParams p) {
         unsigned long long key = ~0ull;
         if (k < nM) {
           const uint32_t v = sv[sidx[k]];
-          const int dv = (p.policy == 0 || p.policy == 4)
-                             ? next_reuse_d(p.mask + (size_t)(v / G) * p.MW, p.p0, p.W) : 0;
-          key = policy_key(p, v, p.t, dv);
+          int dv = 0, cv = kFresh;  // a miss has no information until the next scan ...
+          if (upd && (p.policy == 0 || p.policy == 4)) {  // ... except at a scan iteration
+            dv = next_reuse_d(p.mask + (size_t)(v / G) * p.MW, p.p0, p.W);
+            cv = class_of(dv, p.T);
+          }
+          key = policy_key(p, v, p.t, cv, dv);
         }
         skey[k] = key;
       }
@@ -432,7 +475,7 @@ __global__ void k_set(SetParams p) {
           if (((candm >> w) & 1u) && ((w + A - c0) % A) < pos) ++before;
         rank = before;
       } else {
-        const unsigned long long key = cand ? policy_key(p, tg, lu, d) : ~0ull;
+        const unsigned long long key = cand ? policy_key(p, tg, lu, cls, d) : ~0ull;
         rank = 0;
         for (int w = 0; w < 32; ++w) {
           const unsigned long long kw = __shfl_sync(0xffffffffu, key, w);
@@ -468,10 +511,10 @@ __global__ void k_set(SetParams p) {
       bool is_cand = false;
       uint32_t reuse = 0;
       if (act && x != kInvalid) {
-        const int dx = sd[way];
+        const int dx = sd[way], cx = scls[way];
         ++ctr[C_EVICT];
-        ++ctr[C_EV0 + class_of(dx, p.T)];
-        if (p.pvp && dx) {
+        ++ctr[C_EV0 + cx];
+        if (p.pvp && (cx == kNear || cx == kFar)) {
           is_cand = true;
           reuse = p.t + (uint32_t)dx;
         } else {
@@ -491,6 +534,7 @@ __global__ void k_set(SetParams p) {
         p.node_loc[q] = slot | p.deliver;
         p.tags[slot] = v;
         p.last_use[slot] = p.t;
+        if (p.period > 1) p.line_info[slot] = kInfoFresh;
         ++ctr[C_INS];
         if (is_cand) {
           Cand c;

@@ -64,6 +64,7 @@ struct Ctx {
   uint32_t *qcnt = nullptr, *qoff = nullptr, *qb = nullptr, *qlen = nullptr, *qnode = nullptr;
   uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr, *local_inbox_cnt = nullptr;
   unsigned long long* head = nullptr;            // G = 1 fused delivery: per-node request list heads
+  uint32_t* line_info = nullptr;                 // update period > 1: per-line dynamic information
   uint32_t *nxt = nullptr, *inbox_i = nullptr;   // next position / original request index
   uint8_t* score = nullptr;
   FillEnt* fills = nullptr;
@@ -244,7 +245,7 @@ int free_all() {
   cudaDeviceSynchronize();
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off,
                   g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
-                  g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.head, g.nxt, g.inbox_i, g.score, g.fills, g.cands,
+                  g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.head, g.nxt, g.inbox_i, g.line_info, g.score, g.fills, g.cands,
                   g.scr, g.hist,
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
@@ -312,8 +313,7 @@ int lsmgnn_set_options(const lsmgnn_options* opt) {
   if (opt->policy < 0 || opt->policy > 4) return set_err(LSMGNN_EINVAL, "bad policy");
   if (opt->window < 1 || opt->window > 65534) return set_err(LSMGNN_EINVAL, "window must be 1..65534");
   if (opt->threshold < 0 || opt->threshold > opt->window) return set_err(LSMGNN_EINVAL, "bad threshold");
-  if (opt->update_period != 1 && opt->update_period != 0)
-    return set_err(LSMGNN_EINVAL, "only update_period = 1 is implemented (DESIGN.md R6)");
+  if (opt->update_period < 0 || opt->update_period > 65536) return set_err(LSMGNN_EINVAL, "bad update_period");
   if (opt->max_batch_ids < 1 || opt->max_batch_ids > (1ll << 30)) return set_err(LSMGNN_EINVAL, "bad max_batch_ids");
   g.opt = *opt;
   g.opt_set = true;
@@ -362,7 +362,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   const uint64_t maxm = std::min<uint64_t>((g.Q + g.S - 1) / g.S, g.ucap);
   g.P = 32;
   while (g.P < maxm) g.P <<= 1;
-  g.warp_bytes = (uint32_t)align_up(20ull * g.P + 3 * 32 * 4, 16);
+  g.warp_bytes = (uint32_t)align_up(20ull * g.P + 4 * 32 * 4, 16);
   g.set_warps = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(8, (160 * 1024) / g.warp_bytes));
   if ((uint64_t)g.warp_bytes * g.set_warps > 200 * 1024)
     return set_err(LSMGNN_EINVAL, "a cache set can receive %llu distinct nodes per batch; use more sets",
@@ -408,6 +408,10 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.stg_nodes, std::max<uint64_t>(1, 2 * g.C));
   DA(g.route_cnt, G);
   DA(g.local_inbox_cnt, 1);
+  if (g.opt.update_period > 1) {
+    DA(g.line_info, g.L);
+    CK(cudaMemset(g.line_info, 0xFF, g.L * sizeof(uint32_t)));
+  }
   if (G == 1) {
     DA(g.head, g.Q);
     DA(g.nxt, g.cap);
@@ -624,6 +628,13 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   sp.stage_base = (uint32_t)(g.stage_base0 + par * g.C);
   sp.bypass_base = (uint32_t)g.bypass_base;
   sp.deliver = G == 1 ? kDelivered : 0u;
+  sp.period = (uint32_t)std::max(1, g.opt.update_period);
+  sp.line_info = g.line_info;
+  if (sp.period > 1 && t % sp.period == 0) {  // the periodic window scan
+    k_snapshot<<<grid_for((int64_t)g.L, 256, 4), 256, 0, st>>>(g.tags, (uint32_t)g.L, (uint32_t)G, g.mask, g.MW,
+                                                                sp.p0, g.W, (uint32_t)t, g.line_info);
+    LAUNCHED();
+  }
   {
     const int64_t blocks = std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * 8);
     k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);

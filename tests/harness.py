@@ -28,7 +28,7 @@ def table_for(N: int, D: int, seed_f: int = 5, pinned: bool = False, home: int =
 
 
 def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1, table=None,
-            check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False):
+            check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False, P=1):
     """Run trace[t][rank] through the library. Returns (history [K, 24] uint64, outs or None, bad_rows).
 
     check_rows: "full" compares every row with the closed form F(v); "none" skips it."""
@@ -39,7 +39,7 @@ def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0,
     mine = [np.asarray(trace[t][rank], np.int64) for t in range(K)]
     mb = max_batch_ids or max(1, max(x.size for x in mine))
     c = LsmGnn(N, D, L, A, V, scores, policy=policy, pvp=pvp, window=W, threshold=T, reinsert=reinsert,
-               max_batch_ids=mb, rank=rank, world=world, group=group)
+               max_batch_ids=mb, rank=rank, world=world, group=group, period=P)
     if table is None:
         table = table_for(N, D, seed_f, pinned=True, home=rank, G=world)
     c.attach_storage(table)
@@ -66,9 +66,9 @@ def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0,
     return hist, (outs if keep_outs else None), bad
 
 
-def run_oracle(trace, *, G, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1):
+def run_oracle(trace, *, G, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1, P=1):
     from oracle import Oracle, run_trace
-    o = Oracle(G, N, 4 * D, L, A, scores, policy=policy, pvp=pvp, W=W, T=T, V=V, reinsert=reinsert)
+    o = Oracle(G, N, 4 * D, L, A, scores, policy=policy, pvp=pvp, W=W, T=T, V=V, reinsert=reinsert, P=P)
     return run_trace(o, trace)
 
 

@@ -139,3 +139,18 @@ def test_cfg2_shape_reduced(policy, pvp):
     ho = run_oracle(tr, G=1, **kw)[:, 0, :]
     assert bad == 0
     compare(hg, ho, f"cfg2/{policy}/pvp{pvp}")
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("policy,pvp", [("hybrid", 0), ("hybrid", 1), ("dynamic", 0)])
+def test_update_period(cfg1_g1, P, policy, pvp):
+    """NEXT N1: the paper's periodic dynamic-information update (P = 4 in P:607)
+    with the Fresh class: the GPU's every-P-th window scan (k_snapshot) matches the
+    oracle bit-exactly."""
+    g, tr, sc = cfg1_g1
+    kw = dict(N=16384, D=128, L=1024, A=8, scores=sc, policy=policy, pvp=pvp, W=8, V=512, P=P)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"P={P}/{policy}/pvp{pvp}")
+    assert ho[:, F["evict_fresh"]].sum() > 0

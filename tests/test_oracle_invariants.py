@@ -168,3 +168,17 @@ def test_bad_ids_rejected():
         o.gather(0, [np.array([3, 10])])
     with pytest.raises(RuntimeError):
         o.feed(1, [np.array([-1])])
+
+
+@pytest.mark.parametrize("P", [2, 3, 5])
+@pytest.mark.parametrize("policy", ["hybrid", "dynamic"])
+@pytest.mark.parametrize("pvp", [0, 1])
+def test_invariants_update_period(P, policy, pvp):
+    """I2-I6 hold with the periodic update (N1)."""
+    rng = np.random.default_rng(P * 10 + pvp)
+    G, A, S, W, C = 2, 4, 4, 6, 3
+    N = 80
+    o = Oracle(G, N, 16, S * A, A, rng.integers(0, 256, N).astype(np.uint8), policy=policy, pvp=pvp, W=W,
+               V=C * W, P=P)
+    c = run_checked(o, rand_trace(rng, G, N, 30, 25), C)
+    assert c[..., F["evict_fresh"]].sum() > 0

@@ -310,3 +310,38 @@ def test_spec_split_example():
 def test_quantize_example():
     gold = json.load(open(os.path.join(GOLD, "spec_examples.json")))["quantize"]
     assert synth.quantize_scores(np.array(gold["raw"])).tolist() == gold["scores"]
+
+
+# ----------------------------------------------------------------------------- N1: update period P > 1
+def test_update_period_hand_derived():
+    """P:357-358 periodic update, P = 2, on the Appendix-A trace (hybrid, pvp = 0). Hand
+    derivation: t0 (scan) 1,2 miss -> Fresh; t1 (no scan) 3 misses, both lines Fresh,
+    lowest node 1 evicted; t2 (scan: 2 -> reuse 3 Near, 3 -> reuse 4 Far) 1 misses, 3
+    evicted; t3 2 hits; t4 (scan: 1, 2 no reuse) 3 misses, 1 evicted. Totals: hits 1,
+    storage 5, evictions 3 = Fresh 1 + Far 1 + NoReuse 1 (vs hits 2 / storage 4 at P = 1)."""
+    o = Oracle(1, 4, 16, 2, 2, np.zeros(4, np.uint8), policy="hybrid", pvp=0, W=4, P=2)
+    c = run_trace(o, [[np.array(b)] for b in [[1, 2], [3], [1], [2], [3]]])
+    assert (tot(c, "hits"), tot(c, "storage_reads"), tot(c, "evictions")) == (1, 5, 3)
+    assert (tot(c, "evict_noreuse"), tot(c, "evict_far"), tot(c, "evict_fresh"), tot(c, "evict_near")) == (1, 1, 1, 0)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_update_period_never_reduces_to_static(seed):
+    """With P longer than the trace, only the t = 0 scan happens (on an empty cache): every
+    resident line is 'recently inserted' (Fresh) for the whole run, so HYBRID orders
+    victims by (score, node) = STATIC, and DYNAMIC by node = STATIC with all-zero scores
+    (no bypass at t = 0, where incoming misses still carry exact information)."""
+    rng = np.random.default_rng(seed)
+    N, S, A = 30, 2, 3
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    trace = [[np.array([int(rng.integers(0, N))])] for _ in range(40)]
+    want = run_trace(Oracle(1, N, 16, S * A, A, sc, policy="static", W=6), trace)
+    got = run_trace(Oracle(1, N, 16, S * A, A, sc, policy="hybrid", W=6, P=1000), trace)
+    assert np.array_equal(want[..., 1:10], got[..., 1:10])
+    z = np.zeros(N, np.uint8)
+    want = run_trace(Oracle(1, N, 16, S * A, A, z, policy="static", W=6), trace)
+    got = run_trace(Oracle(1, N, 16, S * A, A, sc, policy="dynamic", W=6, P=1000), trace)
+    assert np.array_equal(want[..., 1:10], got[..., 1:10])
+    # all lines Fresh: nothing carries reuse information, so PVP admits nothing
+    c = run_trace(Oracle(1, N, 16, S * A, A, sc, policy="hybrid", pvp=1, W=6, V=60, P=1000), trace)
+    assert tot(c, "victim_admitted") == 0 and tot(c, "evict_fresh") == tot(c, "evictions")
