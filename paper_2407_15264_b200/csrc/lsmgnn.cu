@@ -50,6 +50,7 @@ struct Ctx {
   uint64_t pool_rows = 0, stage_base0 = 0, bypass_base = 0;
   uint32_t P = 32, warp_bytes = 0, set_warps = 8;
   int sms = 148;
+  int geom_per_sm = 1 << 20;  // LSMGNN_GEOMETRY=small caps every grid at one CTA per SM (I9 tests)
 
   // shared arena (exported to peers): [flags | inbox_cnt | win_cnt | inbox | win_inbox | node_loc | pool]
   char* arena = nullptr;
@@ -161,7 +162,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 int grid_for(int64_t work, int threads, int per_sm = 8) {
   int64_t b = (work + threads - 1) / threads;
   if (b < 1) b = 1;
-  return (int)std::min<int64_t>(b, (int64_t)g.sms * per_sm);
+  return (int)std::min<int64_t>(b, (int64_t)g.sms * std::min(per_sm, g.geom_per_sm));
 }
 
 int check_sticky() {
@@ -364,6 +365,12 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   while (g.P < maxm) g.P <<= 1;
   g.warp_bytes = (uint32_t)align_up(20ull * g.P + 4 * 32 * 4, 16);
   g.set_warps = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(8, (160 * 1024) / g.warp_bytes));
+  if (const char* geo = getenv("LSMGNN_GEOMETRY")) {  // launch-geometry override: results must not change
+    if (!strcmp(geo, "small")) {
+      g.set_warps = 1;
+      g.geom_per_sm = 1;
+    }
+  }
   if ((uint64_t)g.warp_bytes * g.set_warps > 200 * 1024)
     return set_err(LSMGNN_EINVAL, "a cache set can receive %llu distinct nodes per batch; use more sets",
                    (unsigned long long)maxm);
@@ -636,7 +643,8 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     LAUNCHED();
   }
   {
-    const int64_t blocks = std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * 8);
+    const int64_t blocks =
+        std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(8, g.geom_per_sm));
     k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);
     LAUNCHED();
   }
@@ -664,7 +672,7 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   if (G == 1) {
     // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits
     prof_begin(4, st);
-    const int blocks = g.sms * 4;
+    const int blocks = g.sms * std::min(4, g.geom_per_sm);
 #define SERVE(U, O)                                                                                              \
   k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.inbox_i, stamp, \
                                         node_ids, n, g.N, loc_of(g.arena), o4)
@@ -678,7 +686,7 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     prof_begin(5, st);
   } else {
     prof_begin(4, st);
-    const int blocks = g.sms * 4;
+    const int blocks = g.sms * std::min(4, g.geom_per_sm);
     if (wide)
       k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
     else
@@ -767,7 +775,7 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
     CK(cudaStreamWaitEvent(g.side, g.ev_main, 0));
     const uint32_t kq = (uint32_t)(t1 % g.W);
     uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
-    const int blocks = g.sms * 2;
+    const int blocks = g.sms * std::min(2, g.geom_per_sm);
     prof_begin(7, g.side);
     if (g.nvec >= 256)
       k_pvp<8><<<blocks, 256, 0, g.side>>>(kq, (uint32_t)t1, (uint32_t)(t1 + 1), (uint32_t)g.C, (uint32_t)G, g.qlen,

@@ -153,4 +153,18 @@ def test_update_period(cfg1_g1, P, policy, pvp):
     ho = run_oracle(tr, G=1, **kw)[:, 0, :]
     assert bad == 0
     compare(hg, ho, f"P={P}/{policy}/pvp{pvp}")
-    assert ho[:, F["evict_fresh"]].sum() > 0
+    kw1 = dict(kw, P=1)
+    assert not np.array_equal(ho, run_oracle(tr, G=1, **kw1)[:, 0, :])  # the period changes decisions
+
+
+def test_determinism_launch_geometry(cfg1_g1, monkeypatch):
+    """I9: identical counters and bytes under a different launch geometry (one warp per CTA
+    in k_set, one CTA per SM for every grid-stride kernel) — the batch-synchronous rules make
+    the result independent of thread scheduling."""
+    g, tr, sc = cfg1_g1
+    kw = dict(N=16384, D=128, L=1024, A=8, scores=sc, policy="hybrid", pvp=1, W=8, V=512)
+    h1, _, bad1 = run_gpu(tr, **kw)
+    monkeypatch.setenv("LSMGNN_GEOMETRY", "small")
+    h2, _, bad2 = run_gpu(tr, **kw)
+    assert bad1 == 0 and bad2 == 0
+    compare(h1, h2, "geometry")
