@@ -40,6 +40,22 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         return
+    if mode == "cfg3":  # full-size configs[2]: trace from the driver's npz
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+        import synth
+        from tests.harness import run_gpu
+        wl = synth.CONFIGS["cfg3"]
+        z = np.load(os.path.join(outdir, "trace.npz"))
+        K = len([k for k in z.files if k.endswith("_r0")])
+        tr = [[z[f"t{t}_r{r}"] for r in range(world)] for t in range(K)]
+        hist, _, bad = run_gpu(tr, N=wl.N, D=wl.D, L=wl.lines_per_gpu, A=wl.ways, scores=z["scores"],
+                               policy="hybrid", pvp=1, W=wl.window, V=wl.victim_lines, rank=rank, world=world,
+                               group=dist.group.WORLD, max_batch_ids=max(len(x) for row in tr for x in row))
+        np.save(os.path.join(outdir, f"hist{rank}.npy"), hist)
+        json.dump({"rank": rank, "bad": int(bad)}, open(os.path.join(outdir, f"r{rank}.json"), "w"))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     policy = sys.argv[3] if len(sys.argv) > 3 else "hybrid"
     pvp = int(sys.argv[4]) if len(sys.argv) > 4 else 1
     ndev = torch.cuda.device_count()
