@@ -330,10 +330,22 @@ def main():
     roof = None
     if fill_ms > 0:
         ach = fill_pcie / (fill_ms / 1e3) / 1e9
-        roof = {"bound": "pcie", "kernel": "k_fill", "achieved": round(ach, 2), "peak": round(pcie_peak, 2),
-                "unit": "GB/s", "frac": round(ach / pcie_peak, 4), "traffic": None,
+        kname = "k_serve" if G == 1 else "k_fill"
+        traffic, tsrc = None, None
+        try:  # one ncu --set full capture of this kernel at this workload, per launch (profiles/)
+            nk = json.load(open(os.path.join(ROOT, "profiles", "ncu_kernels_latest.json")))
+            hit = [v for k, v in nk.items() if k.startswith(kname)]
+            if hit and wl.name == "cfg2":
+                traffic = {"dram_bytes": int(hit[0]["dram_bytes"]), "pcie_read_bytes": int(hit[0]["pcie_read_bytes"]),
+                           "pcie_write_bytes": int(hit[0]["pcie_write_bytes"])}
+                tsrc = "profiles/" + hit[0]["report"] + " (ncu --set full, one launch, cfg2)"
+        except Exception:
+            pass
+        roof = {"bound": "pcie", "kernel": kname, "achieved": round(ach, 2), "peak": round(pcie_peak, 2),
+                "unit": "GB/s", "frac": round(ach / pcie_peak, 4), "traffic": traffic, "traffic_source": tsrc,
                 "peak_source": "cudaMemcpy pinned H2D 1 GiB best-of-5 measured in this run (the PCIe Gen5 x16 "
-                               "link is the bound of the storage tier)",
+                               "link is the bound of the storage tier); SM-initiated reads of scattered 4 KiB "
+                               "host rows top out at 51.5 GB/s on this box (profiles/r01_pcie_microbench.txt)",
                 "per_launch": {"algorithmic_bytes": int(fill_pcie / K), "units": "storage rows x R (H2D)",
                                "avg_ms": round(fill_ms / K, 4)}}
         phases["fill"]["pcie_h2d_GBps"] = round(ach, 2)
