@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true")
+    p.add_argument("--no-ablation", action="store_true", help="skip the PVP on/off ablation")
     p.add_argument("--lines", type=int, default=None, help="override lines per GPU")
     return p.parse_args()
 
@@ -387,10 +388,69 @@ def main():
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, G, trace, scores, table.numpy(), args, lines)
     c.close()
+    if not args.no_ablation and G == 1:
+        line["pvp_ablation"] = pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if G > 1:
         torch.distributed.destroy_process_group()
+
+
+def pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev, train_ms=10.0, warm=10, steps=20):
+    """S11 measured: hybrid with the PVP off vs on, with a fixed GPU "training" stand-in of
+    train_ms between batches (SURVEY.md §8(d) primary variant). The PVP's side-stream copy of
+    victim queue t+1 overlaps the stand-in ("the CPU to GPU transfer is done at the
+    training stage"); the gather side is timed with CUDA events around gather + prefetch only."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    W = wl.window
+    st = torch.cuda.current_stream()
+    cycles = int(train_ms * 1e-3 * 1.9e9)
+    out = torch.empty((max(x.numel() for x in ids_d), wl.R), dtype=torch.uint8, device=dev)
+    res = {"train_stand_in_ms": train_ms, "steps": steps, "warmup": warm,
+           "what": "torch.cuda._sleep on the user stream after each prefetch; value = requested bytes / "
+                   "device time of gather+prefetch (training excluded)"}
+    for pvp in (0, 1):
+        c = LsmGnn(wl.N, wl.D, lines, wl.ways, wl.victim_lines if pvp else 0, scores, policy=args.policy, pvp=pvp,
+                   window=W, max_batch_ids=max_ids, device=dev.index)
+        c.attach_storage(table)
+        c.prefetch(ids_d[1:W + 1], first_iter=1)
+        ev = []
+        s0 = None
+        for t in range(warm + steps):
+            if t == warm:
+                torch.cuda.synchronize()
+                s0 = c.stats(1)
+                c.profile(True)
+                c.profile_read()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            c.gather(ids_d[t], out)
+            c.prefetch([ids_d[t + 1 + W]], first_iter=t + 1 + W)
+            b.record(st)
+            torch.cuda._sleep(cycles)
+            if t >= warm:
+                ev.append((a, b))
+        torch.cuda.synchronize()
+        prof = c.profile_read()
+        c.profile(False)
+        s1 = c.stats(1)
+        c.close()
+        d = {k: s1[k] - s0[k] for k in s1 if k != "iter"}
+        tg = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+        u = max(d["unique"], 1)
+        res[f"pvp{pvp}"] = {"gather_GBps": round(d["requests"] * wl.R / tg / 1e9, 3),
+                            "gather_ms_per_step": round(tg / steps * 1e3, 3),
+                            "hit_ratio": round(d["hits"] / u, 4), "victim_hit_ratio": round(d["victim_hits"] / u, 4),
+                            "storage_ratio": round(d["storage_reads"] / u, 4),
+                            "storage_GB_per_step": round(d["bytes_h2d_storage"] / steps / 1e9, 4),
+                            "pvp_h2d_GB_per_step": round(d["bytes_h2d_pvp"] / steps / 1e9, 4),
+                            "victim_d2h_GB_per_step": round(d["bytes_d2h_victim"] / steps / 1e9, 4),
+                            "pvp_side_stream_ms_per_step": round(prof.get("pvp", (0.0, 0))[0] / steps, 3),
+                            "victim_dropped_per_step": d["victim_dropped"] / steps,
+                            "victim_lines": wl.victim_lines if pvp else 0}
+    res["gather_speedup_pvp"] = round(res["pvp1"]["gather_GBps"] / res["pvp0"]["gather_GBps"], 4)
+    return res
 
 
 def measure_h2d(dev) -> float:
