@@ -36,6 +36,34 @@ __global__ void k_ldg(const uint4* __restrict__ host, const uint32_t* __restrict
   }
 }
 
+// device rows -> pinned host rows (the e2e out path), 8 x 16 B per lane in flight
+__global__ void k_d2h(const uint4* __restrict__ src, uint32_t n, uint4* __restrict__ hout, int nvec) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t e = warp; e < n; e += nw)
+    for (int i = lane; i < nvec; i += 256) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = src[(size_t)e * nvec + i + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) hout[(size_t)e * nvec + i + 32 * u] = v[u];
+    }
+}
+// host row -> host out row (read over PCIe then write back over PCIe): the e2e miss path
+__global__ void k_relay(const uint4* __restrict__ host, const uint32_t* __restrict__ rows, uint32_t n,
+                        uint4* __restrict__ hout, int nvec) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t e = warp; e < n; e += nw)
+    for (int i = lane; i < nvec; i += 256) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = host[(size_t)rows[e] * nvec + i + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) hout[(size_t)e * nvec + i + 32 * u] = v[u];
+    }
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)), "r"(cnt));
 }
@@ -163,6 +191,19 @@ int main(int argc, char** argv) {
         }
       }
     }
+  }
+  // D2H: device rows -> pinned host (SM stores over PCIe), and both directions at once
+  uint8_t* hout;
+  CK(cudaHostAlloc(&hout, (size_t)n * R, cudaHostAllocMapped));
+  uint8_t* houtd;
+  CK(cudaHostGetDevicePointer((void**)&houtd, hout, 0));
+  timeit("copy engine D2H (contiguous n*R)", [&] { cudaMemcpyAsync(hout, dst, (size_t)n * R, cudaMemcpyDeviceToHost); });
+  for (int blocks : {sms, 4 * sms}) {
+    char nm[96];
+    snprintf(nm, 96, "SM D2H stores grid=%d", blocks);
+    timeit(nm, [&] { k_d2h<<<blocks, 256>>>((const uint4*)dst, n, (uint4*)houtd, R / 16); });
+    snprintf(nm, 96, "SM host->host relay (read+write) grid=%d", blocks);
+    timeit(nm, [&] { k_relay<<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)houtd, R / 16); });
   }
   CK(cudaGetLastError());
   // correctness of one row
