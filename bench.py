@@ -104,7 +104,7 @@ def build_inputs(wl, G, rank, iters, seed_offset=0):
     t0 = time.time()
     g = synth.plcite(wl.N, wl.m, seed_g=wl.seeds["g"], seed_pi=wl.seeds["pi"])
     trace = synth.make_trace_parallel(g, G, wl.batch, wl.fanout, iters, seed_train=wl.seeds["train"],
-                                      seed_s=wl.seeds["s"])
+                                      seed_s=wl.seeds["s"], procs=max(1, (os.cpu_count() or 1) // max(G, 1)))
     scores = synth.static_scores(g)
     log(f"[bench] inputs: graph N={wl.N} m={wl.m}, {iters} iterations x {G} ranks in {time.time() - t0:.1f}s")
     return g, trace, scores

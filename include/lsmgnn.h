@@ -161,6 +161,27 @@ int lsmgnn_gather_host(const int64_t* host_ids, int64_t n, void* host_out, void*
 int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batches,
                     int64_t first_iter, void* stream);
 
+/* ---- NEXT N3: the window producer on the GPU (the step before the path).
+ * GraphSAGE multi-hop neighbour sampling (§2.1; fanout P:603) over a CSR
+ * pinned in host memory and read by GPU threads with zero-copy UVA loads. The list
+ * produced is exactly DESIGN.md §3's definition (oracle/lsm_sampler.c): per frontier position
+ * p, layer l, draw j: all neighbours if deg <= f, else f draws at CSR offset
+ * floor(U01(h(seed, t, r, l, p, j)) * deg); the next frontier is the first-occurrence unique of
+ * the layer's draws; the result is the first-occurrence unique of seeds ++ all draws.
+ *
+ * lsmgnn_sampler_attach: indptr host int64[num_nodes+1], indices host int32[nnz] (CSR, page-
+ *   locked here unless already pinned; referenced, not owned). Independent of lsmgnn_init.
+ * lsmgnn_sample: seeds device int64[nseeds]; fanout host int32[nlayers]; out device
+ *   int64[cap] with cap >= nseeds * (1 + f0 + f0 f1 + ...) (the bound); the list length is
+ *   written to count_dev (device int64) — nothing synchronises. Stream-ordered on `stream`.
+ * lsmgnn_prefetch_dev: window feed of ONE batch (device int64 ids, device int64 count) for
+ *   iteration first_iter — lsmgnn_prefetch semantics for G = 1 without reading the count on
+ *   the host; issue the PVP copy with lsmgnn_prefetch(NULL, NULL, 0, 0, stream). */
+int lsmgnn_sampler_attach(const int64_t* indptr, const int32_t* indices, int64_t num_nodes, int64_t nnz);
+int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, int32_t nlayers, uint64_t seed,
+                  int64_t t, int32_t r, int64_t* out, int64_t cap, int64_t* count_dev, void* stream);
+int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t first_iter, void* stream);
+
 /* Counters of this home: scope 0 = the last completed gather, 1 = cumulative.
  * Synchronises with the last stream used. */
 int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope);

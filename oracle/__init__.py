@@ -20,6 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "lsm_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "lsm_sampler.c")]
 
 HYBRID, STATIC, LRU, RR, DYNAMIC = range(5)
 POLICIES = {"hybrid": HYBRID, "static": STATIC, "lru": LRU, "rr": RR, "dynamic": DYNAMIC}
@@ -43,9 +44,9 @@ _LIB = None
 
 def build() -> str:
     """Compile liboracle.so (gcc -O2, single-threaded)."""
-    if not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(_SRC),
-                                                              os.path.getmtime(os.path.join(_HERE, "lsm_oracle.h"))):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-o", _SO, _SRC])
+    deps = _SRCS + [os.path.join(_HERE, "lsm_oracle.h")]
+    if not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(p) for p in deps):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-o", _SO, *_SRCS])
     return _SO
 
 
@@ -73,6 +74,8 @@ def _lib():
         L.orc_next_use.restype = i64
         L.orc_dump_events.argtypes = [vp, vp, i64]
         L.orc_dump_events.restype = i64
+        L.orc_sample.argtypes = [vp, vp, i64, vp, i64, vp, i32, ctypes.c_uint64, i64, i32, vp, i64]
+        L.orc_sample.restype = i64
         _LIB = L
     return _LIB
 
@@ -157,6 +160,21 @@ class Oracle:
         buf = np.empty((max(n, 1), 7), np.int64)
         _lib().orc_dump_events(self._o, buf.ctypes.data, n)
         return buf[:n]
+
+
+def sample_batch(indptr, indices, seeds, fanout, seed_s: int, t: int, r: int) -> np.ndarray:
+    """NEXT N3 oracle: GraphSAGE sampling of one rank's batch (lsm_sampler.c)."""
+    indptr = np.ascontiguousarray(indptr, np.int64)
+    indices = np.ascontiguousarray(indices, np.int32)
+    seeds = np.ascontiguousarray(seeds, np.int64)
+    fan = np.ascontiguousarray(fanout, np.int32)
+    cap = int(seeds.size * (1 + np.cumprod(fan.astype(np.int64)).sum())) + 1
+    out = np.empty(cap, np.int64)
+    n = _lib().orc_sample(indptr.ctypes.data, indices.ctypes.data, indptr.size - 1, seeds.ctypes.data, seeds.size,
+                          fan.ctypes.data, fan.size, seed_s, t, r, out.ctypes.data, cap)
+    if n < 0:
+        raise RuntimeError("sample overflow")
+    return out[:n].copy()
 
 
 def run_trace(orc: Oracle, trace, table=None, pvp=None, feed=True):

@@ -23,7 +23,8 @@ STATS_FIELDS = ["iter", "requests", "peer_requests", "unique", "hits", "victim_h
 EXPORTS = ["lsmgnn_bind", "lsmgnn_set_options", "lsmgnn_init", "lsmgnn_attach_storage", "lsmgnn_handle_bytes",
            "lsmgnn_export_handle", "lsmgnn_connect", "lsmgnn_gather", "lsmgnn_gather_host", "lsmgnn_prefetch",
            "lsmgnn_stats", "lsmgnn_stats_history", "lsmgnn_kernel_launches", "lsmgnn_finalize",
-           "lsmgnn_last_error", "lsmgnn_profile", "lsmgnn_profile_read"]
+           "lsmgnn_last_error", "lsmgnn_profile", "lsmgnn_profile_read", "lsmgnn_sampler_attach", "lsmgnn_sample",
+           "lsmgnn_prefetch_dev"]
 PHASES = ["route", "dedup", "probe_replace", "admit", "fill", "pull", "window", "pvp"]
 
 
@@ -74,6 +75,9 @@ def load_library(path: str = SO_PATH) -> ctypes.CDLL:
         "lsmgnn_last_error": ([], ctypes.c_char_p),
         "lsmgnn_profile": ([i32], i32),
         "lsmgnn_profile_read": ([vp, vp], i32),
+        "lsmgnn_sampler_attach": ([vp, vp, i64, i64], i32),
+        "lsmgnn_sample": ([vp, i64, vp, i32, ctypes.c_uint64, i64, i32, vp, i64, vp, vp], i32),
+        "lsmgnn_prefetch_dev": ([vp, vp, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -219,3 +223,45 @@ class LsmGnn:
     def close(self) -> None:
         if _LIB is not None:
             _LIB.lsmgnn_finalize()
+
+
+class Sampler:
+    """NEXT N3: GPU GraphSAGE sampler over a host-pinned CSR (lsmgnn_sampler_attach/_sample)."""
+
+    def __init__(self, indptr: np.ndarray, indices: np.ndarray):
+        import torch
+        if not torch.cuda.is_available():
+            raise LsmGnnError("CUDA device required")
+        L = load_library()
+        self.indptr = torch.from_numpy(np.ascontiguousarray(indptr, np.int64)).pin_memory()
+        self.indices = torch.from_numpy(np.ascontiguousarray(indices, np.int32)).pin_memory()
+        _check(L.lsmgnn_sampler_attach(ctypes.c_void_p(self.indptr.data_ptr()), ctypes.c_void_p(self.indices.data_ptr()),
+                                       self.indptr.numel() - 1, self.indices.numel()))
+
+    @staticmethod
+    def bound(nseeds: int, fanout) -> int:
+        b, p = nseeds, nseeds
+        for f in fanout:
+            p *= f
+            b += p
+        return b
+
+    def sample(self, seeds, fanout, seed: int, t: int, r: int, out=None, count=None, stream=None):
+        """Returns (out int64 CUDA tensor of capacity bound, count int64 CUDA tensor [1])."""
+        import torch
+        dev = seeds.device
+        if out is None:
+            out = torch.empty(max(1, self.bound(seeds.numel(), fanout)), dtype=torch.int64, device=dev)
+        if count is None:
+            count = torch.zeros(1, dtype=torch.int64, device=dev)
+        fan = np.ascontiguousarray(fanout, np.int32)
+        _check(_LIB.lsmgnn_sample(ctypes.c_void_p(seeds.data_ptr()), seeds.numel(), fan.ctypes.data_as(ctypes.c_void_p),
+                                  fan.size, seed, t, r, ctypes.c_void_p(out.data_ptr()), out.numel(),
+                                  ctypes.c_void_p(count.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))))
+        return out, count
+
+
+def prefetch_dev(ids, count, first_iter: int, stream=None) -> None:
+    """Window feed of one device-resident batch (G = 1)."""
+    _check(_LIB.lsmgnn_prefetch_dev(ctypes.c_void_p(ids.data_ptr()), ctypes.c_void_p(count.data_ptr()), int(first_iter),
+                                    ctypes.c_void_p(_stream_ptr(stream))))

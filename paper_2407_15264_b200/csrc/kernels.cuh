@@ -76,6 +76,26 @@ __global__ void k_route_local(const int64_t* __restrict__ ids, int64_t n, uint64
   }
 }
 
+// Same, with the length read on the device (*n_dev), grid sized by the host's bound.
+__global__ void k_route_local_dev(const int64_t* __restrict__ ids, const int64_t* n_dev, int64_t bound, uint64_t N,
+                                  uint32_t* __restrict__ inbox, uint32_t* __restrict__ inbox_cnt, Scratch* scr) {
+  const int64_t n = min(*n_dev, bound);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool ok = false;
+    uint32_t v = 0;
+    if (i < n) {
+      const int64_t x = ids[i];
+      ok = x >= 0 && (uint64_t)x < N;
+      v = (uint32_t)x;
+      if (!ok) atomicAdd(&scr->bad_ids, 1u);
+    }
+    const uint32_t pos = warp_reserve(inbox_cnt, ok ? 1u : 0u);
+    if (ok) inbox[pos] = v;
+  }
+}
+
 // ------------------------------------------------------------------------------ S1 (G > 1)
 // Requester side of the communication layer: bucket each valid ID by its
 // home g = v mod G and store it straight into home g's inbox slot [me] through the

@@ -19,6 +19,7 @@
 
 #include "../../include/lsmgnn.h"
 #include "kernels.cuh"
+#include "sampler.cuh"
 
 using namespace lsm;
 
@@ -95,6 +96,19 @@ struct Ctx {
   int64_t feed_next = 1;   // next window iteration to feed
   uint32_t win_seq = 0;    // window batches exchanged (G > 1)
   int64_t launches = 0;
+
+  // GPU sampler (NEXT N3): CSR in pinned host memory + scratch
+  const int64_t* s_indptr = nullptr;   // device mapping of the host CSR
+  const int32_t* s_indices = nullptr;
+  const void* s_host_indptr = nullptr;
+  const void* s_host_indices = nullptr;
+  bool s_reg_indptr = false, s_reg_indices = false;
+  uint64_t s_N = 0, s_cap = 0;
+  unsigned long long* s_tab = nullptr;  // first-occurrence table, u64 per node
+  uint32_t *s_raw = nullptr, *s_layer = nullptr, *s_front = nullptr, *s_cnt = nullptr, *s_off = nullptr;
+  uint32_t *s_keep = nullptr, *s_pos = nullptr, *s_bsum = nullptr;
+  SampCounts* s_counts = nullptr;
+  uint32_t s_hi = 0xFFFFFFFFu;
 
   // phase profiling
   bool prof = false;
@@ -251,6 +265,11 @@ int free_all() {
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  void* sp[] = {g.s_tab, g.s_raw, g.s_layer, g.s_front, g.s_cnt, g.s_off, g.s_keep, g.s_pos, g.s_bsum, g.s_counts};
+  for (void* p : sp)
+    if (p) cudaFree(p);
+  if (g.s_reg_indptr) cudaHostUnregister(const_cast<void*>(g.s_host_indptr));
+  if (g.s_reg_indices) cudaHostUnregister(const_cast<void*>(g.s_host_indices));
   for (int h = 0; h < kMaxG; ++h)
     if (g.peer_arena[h] && g.peer_arena[h] != g.arena) cudaIpcCloseMemHandle(g.peer_arena[h]);
   if (g.qrows_host) cudaFreeHost(g.qrows_host);
@@ -843,6 +862,154 @@ int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count)
     CK(cudaMemcpy(out_host + i, g.hist + (size_t)((first + i) % kHist) * F_NFIELDS, sizeof(lsmgnn_stats_t),
                   cudaMemcpyDeviceToHost));
   return check_sticky();
+}
+
+// ------------------------------------------------------------------ NEXT N3: GPU sampler
+int lsmgnn_sampler_attach(const int64_t* indptr, const int32_t* indices, int64_t num_nodes, int64_t nnz) {
+  if (!indptr || !indices || num_nodes < 1 || num_nodes > 0xFFFFFFF0ll || nnz < 0)
+    return set_err(LSMGNN_EINVAL, "bad CSR");
+  if (g.device < 0) CK(cudaGetDevice(&g.device));
+  CK(cudaSetDevice(g.device));
+  CK(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, g.device));
+  auto map = [](const void* p, size_t bytes, bool* registered, const void** dev) -> int {
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) cudaGetLastError();
+    if (e == cudaSuccess && at.type == cudaMemoryTypeHost && at.devicePointer) {
+      *dev = at.devicePointer;
+      *registered = false;
+      return 0;
+    }
+    CK(cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterMapped | cudaHostRegisterPortable | cudaHostRegisterReadOnly));
+    void* d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, const_cast<void*>(p), 0));
+    *dev = d;
+    *registered = true;
+    return 0;
+  };
+  if (int rc = map(indptr, (num_nodes + 1) * sizeof(int64_t), &g.s_reg_indptr, (const void**)&g.s_indptr)) return rc;
+  if (int rc = map(indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t), &g.s_reg_indices, (const void**)&g.s_indices))
+    return rc;
+  g.s_host_indptr = indptr;
+  g.s_host_indices = indices;
+  g.s_N = (uint64_t)num_nodes;
+  if (g.s_tab) cudaFree(g.s_tab);
+  CK(cudaMalloc(&g.s_tab, g.s_N * sizeof(unsigned long long)));
+  CK(cudaMemset(g.s_tab, 0xFF, g.s_N * sizeof(unsigned long long)));
+  if (!g.s_counts) CK(cudaMalloc(&g.s_counts, sizeof(SampCounts)));
+  g.s_hi = 0xFFFFFFFFu;
+  return 0;
+}
+
+int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, int32_t nlayers, uint64_t seed,
+                  int64_t t, int32_t r, int64_t* out, int64_t cap, int64_t* count_dev, void* stream) {
+  if (!g.s_tab) return set_err(LSMGNN_ESTATE, "sampler_attach first");
+  if (nseeds < 0 || nlayers < 0 || nlayers > 16 || (nseeds > 0 && (!seeds || !out)) || !count_dev || (nlayers && !fanout))
+    return set_err(LSMGNN_EINVAL, "bad sample arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // host-side upper bounds (the real sizes stay on the device)
+  uint64_t prod = (uint64_t)nseeds, bound = (uint64_t)nseeds, maxlayer = 0;
+  for (int l = 0; l < nlayers; ++l) {
+    if (fanout[l] < 0) return set_err(LSMGNN_EINVAL, "negative fanout");
+    prod *= (uint64_t)fanout[l];
+    bound += prod;
+    maxlayer = std::max(maxlayer, prod);
+  }
+  if (bound > (4ull << 20)) return set_err(LSMGNN_EINVAL, "sample bound %llu > 4M ids", (unsigned long long)bound);
+  if ((uint64_t)cap < bound) return set_err(LSMGNN_EINVAL, "out capacity %lld < bound %llu", (long long)cap,
+                                            (unsigned long long)bound);
+  if (bound > g.s_cap) {  // grow scratch (first use / larger fanout)
+    for (uint32_t* p : {g.s_raw, g.s_layer, g.s_front, g.s_cnt, g.s_off, g.s_keep, g.s_pos, g.s_bsum})
+      if (p) cudaFree(p);
+    const size_t b = bound + 1;
+    CK(cudaMalloc(&g.s_raw, b * 4));
+    CK(cudaMalloc(&g.s_layer, b * 4));
+    CK(cudaMalloc(&g.s_front, b * 4));
+    CK(cudaMalloc(&g.s_cnt, b * 4));
+    CK(cudaMalloc(&g.s_off, b * 4));
+    CK(cudaMalloc(&g.s_keep, b * 4));
+    CK(cudaMalloc(&g.s_pos, b * 4));
+    CK(cudaMalloc(&g.s_bsum, 1024 * 4));
+    g.s_cap = bound;
+  }
+  SampCounts* c = g.s_counts;
+  auto xscan = [&](const uint32_t* x, const uint32_t* n_ptr, uint32_t* y, uint64_t nmax) -> int {
+    const int nb = (int)std::max<uint64_t>(1, (nmax + 4095) / 4096);
+    k_xscan_blocks<<<nb, 1024, 0, st>>>(x, n_ptr, 0, y, g.s_bsum);
+    LAUNCHED();
+    k_xscan_sums<<<1, 1024, 0, st>>>(g.s_bsum, (uint32_t)nb);
+    LAUNCHED();
+    k_xscan_add<<<grid_for((int64_t)nmax, 256, 4), 256, 0, st>>>(y, n_ptr, 0, g.s_bsum);
+    LAUNCHED();
+    return 0;
+  };
+  // first-occurrence unique of a[0..*n_ptr) -> out (OutT), count -> *n_out
+  auto unique_first = [&](const uint32_t* a, const uint32_t* n_ptr, uint64_t nmax, auto* outp, uint32_t* n_out) -> int {
+    const uint32_t hi = g.s_hi--;
+    const int gr = grid_for((int64_t)std::max<uint64_t>(nmax, 1), 256, 4);
+    k_fo_mark<<<gr, 256, 0, st>>>(a, n_ptr, 0, g.s_tab, hi);
+    LAUNCHED();
+    k_fo_flag<<<gr, 256, 0, st>>>(a, n_ptr, 0, g.s_tab, hi, g.s_keep);
+    LAUNCHED();
+    if (int rc = xscan(g.s_keep, n_ptr, g.s_pos, nmax)) return rc;
+    k_fo_compact<<<gr, 256, 0, st>>>(a, n_ptr, 0, g.s_keep, g.s_pos, outp, n_out);
+    LAUNCHED();
+    return 0;
+  };
+  k_samp_init<<<grid_for(std::max<int64_t>(nseeds, 1), 256, 4), 256, 0, st>>>(seeds, (uint32_t)nseeds, g.s_raw,
+                                                                              g.s_front, c);
+  LAUNCHED();
+  uint64_t fmax = (uint64_t)nseeds;
+  for (int l = 0; l < nlayers; ++l) {
+    const uint32_t f = (uint32_t)fanout[l];
+    const uint64_t lmax = fmax * f;
+    const int gr = grid_for((int64_t)std::max<uint64_t>(fmax, 1), 256, 4);
+    k_samp_count<<<gr, 256, 0, st>>>(g.s_front, c, g.s_indptr, f, g.s_cnt);
+    LAUNCHED();
+    if (int rc = xscan(g.s_cnt, &c->nf, g.s_off, fmax)) return rc;
+    k_xscan_total<<<1, 1, 0, st>>>(g.s_off, g.s_cnt, &c->nf, 0, &c->layer_n);
+    LAUNCHED();
+    k_samp_draw<<<gr, 256, 0, st>>>(g.s_front, c, g.s_indptr, g.s_indices, f, g.s_off, g.s_layer, seed, (uint64_t)t,
+                                    (uint64_t)r, (uint64_t)l);
+    LAUNCHED();
+    k_samp_append<<<grid_for((int64_t)std::max<uint64_t>(lmax, 1), 256, 4), 256, 0, st>>>(g.s_layer, c, g.s_raw);
+    LAUNCHED();
+    // next frontier = first-occurrence unique of this layer's draws
+    if (int rc = unique_first(g.s_layer, &c->layer_n, lmax, g.s_front, &c->nf)) return rc;
+    k_samp_advance<<<1, 1, 0, st>>>(c);
+    LAUNCHED();
+    fmax = lmax;
+  }
+  if (int rc = unique_first(g.s_raw, &c->nraw, bound, out, &c->nout)) return rc;
+  k_samp_out_count<<<1, 1, 0, st>>>(c, count_dev);
+  LAUNCHED();
+  return 0;
+}
+
+// Window feed of one batch whose length lives on the device (e.g. straight from
+// lsmgnn_sample): same semantics as lsmgnn_prefetch with num_batches = 1 (G = 1).
+int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t first_iter, void* stream) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
+  if (g.world != 1) return set_err(LSMGNN_EINVAL, "prefetch_dev is single-home only");
+  if (first_iter != g.feed_next) return set_err(LSMGNN_ESTATE, "window iteration out of order");
+  if (first_iter > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint32_t slot = (uint32_t)(first_iter % g.Wp1);
+  uint32_t* ring_slot = g.ring + (size_t)slot * g.cap;
+  prof_begin(6, st);
+  k_mask_clear<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, 1, g.MW, slot, g.mask);
+  LAUNCHED();
+  CK(cudaMemsetAsync(g.ring_len + slot, 0, sizeof(uint32_t), st));
+  k_route_local_dev<<<grid_for((int64_t)g.cap, 256), 256, 0, st>>>(ids, count_dev, (int64_t)g.cap, g.N, ring_slot,
+                                                                   g.ring_len + slot, g.scr);
+  LAUNCHED();
+  k_mask_set<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, 1, g.MW, slot, g.mask);
+  LAUNCHED();
+  prof_end(6, st);
+  g.feed_next = first_iter + 1;
+  // the PVP copy for t+1 is issued by lsmgnn_prefetch; call it with num_batches = 0 when needed
+  g.last_stream = st;
+  return 0;
 }
 
 int lsmgnn_profile(int32_t enable) {
