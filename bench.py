@@ -390,6 +390,7 @@ def main():
     c.close()
     if not args.no_ablation and G == 1:
         line["pvp_ablation"] = pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev)
+        line["gpu_sampler_pipeline"] = gpu_sampler_pipeline(wl, g_, scores, table, lines, args, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if G > 1:
@@ -451,6 +452,61 @@ def pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev, train_ms=1
                             "victim_lines": wl.victim_lines if pvp else 0}
     res["gather_speedup_pvp"] = round(res["pvp1"]["gather_GBps"] / res["pvp0"]["gather_GBps"], 4)
     return res
+
+
+def gpu_sampler_pipeline(wl, g, scores, table, lines, args, dev, warm=5, steps=20):
+    """N3 measured: the window producer on the GPU inside the step. Each step samples batch
+    t+1+W with the UVA sampler (lsmgnn_sample), feeds it (lsmgnn_prefetch_dev) and gathers
+    batch t (sampled W steps earlier). Reports the sampler's own time and the whole step."""
+    import torch
+    import synth
+    from paper_2407_15264_b200 import LsmGnn, Sampler, prefetch_dev
+    W = wl.window
+    st = torch.cuda.current_stream()
+    bound = Sampler.bound(wl.batch, wl.fanout)
+    c = LsmGnn(wl.N, wl.D, lines, wl.ways, 0, scores, policy=args.policy, pvp=0, window=W, max_batch_ids=bound,
+               device=dev.index)
+    c.attach_storage(table)
+    s = Sampler(g.indptr, g.indices)
+    perm = torch.from_numpy(synth.epoch_seeds(wl.N, 0)).to(dev)
+    total = warm + steps + W + 1
+    bufs = [(torch.empty(bound, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev))
+            for _ in range(W + 2)]
+    counts_host = {}
+
+    def sample(k):
+        o, cn = bufs[k % (W + 2)]
+        s.sample(perm[k * wl.batch:(k + 1) * wl.batch], wl.fanout, wl.seeds["s"], k, 0, out=o, count=cn)
+        return o, cn
+
+    for k in range(1, W + 1):
+        prefetch_dev(*sample(k), first_iter=k)
+    o0, c0 = sample(0)
+    out = torch.empty((bound, wl.R), dtype=torch.uint8, device=dev)
+    samp_ms, step_ms, nbytes, nids = 0.0, 0.0, 0, 0
+    for t in range(warm + steps):
+        o, cn = bufs[t % (W + 2)] if t else (o0, c0)
+        n = int(cn.item())  # sampled W steps ago: long complete
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(st)
+        ok, ck = sample(t + 1 + W)
+        e1.record(st)
+        c.gather(o[:n], out)
+        prefetch_dev(ok, ck, first_iter=t + 1 + W)
+        e2.record(st)
+        if t >= warm:
+            e2.synchronize()
+            samp_ms += e0.elapsed_time(e1)
+            step_ms += e0.elapsed_time(e2)
+            nbytes += n * wl.R
+            nids += int(ck.item())
+    c.close()
+    return {"steps": steps, "sampler_ms_per_batch": round(samp_ms / steps, 4),
+            "sampled_ids_per_s": round(nids / (samp_ms / 1e3), 1),
+            "step_ms_with_sampler": round(step_ms / steps, 4),
+            "gather_GBps_incl_sampler": round(nbytes / (step_ms / 1e3) / 1e9, 3),
+            "what": "GPU UVA GraphSAGE sampler (CSR pinned in host memory) feeding the window inside the step; "
+                    "hybrid, pvp 0, same workload"}
 
 
 def measure_h2d(dev) -> float:
