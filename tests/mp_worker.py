@@ -40,6 +40,20 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         return
+    if mode == "edge":  # ragged / empty / duplicate-heavy batches across ranks, tiny victim queues
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+        from tests.harness import run_gpu
+        z = np.load(os.path.join(outdir, "trace.npz"))
+        K = len([k for k in z.files if k.endswith("_r0")])
+        tr = [[z[f"t{t}_r{r}"] for r in range(world)] for t in range(K)]
+        cfg = json.load(open(os.path.join(outdir, "cfg.json")))
+        hist, _, bad = run_gpu(tr, scores=z["scores"], rank=rank, world=world, group=dist.group.WORLD,
+                               max_batch_ids=max(1, max(len(x) for row in tr for x in row)), **cfg)
+        np.save(os.path.join(outdir, f"hist{rank}.npy"), hist)
+        json.dump({"rank": rank, "bad": int(bad)}, open(os.path.join(outdir, f"r{rank}.json"), "w"))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if mode == "cfg3":  # full-size configs[2]: trace from the driver's npz
         torch.cuda.set_device(rank % torch.cuda.device_count())
         import synth

@@ -35,6 +35,36 @@ def launch(G, tmp, *args, timeout=600):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
 
 
+@pytest.mark.parametrize("G,case", [(2, "ragged"), (3, "dups"), (2, "period"), (4, "rr")])
+def test_multiprocess_edge_cases(tmp_path, G, case):
+    """Ranks with empty batches, cross-rank duplicates, raw lists, victim-queue overflow,
+    reinsert = 0, the periodic update and RR — per-home counters equal the oracle's."""
+    rng = np.random.default_rng(G * 7 + len(case))
+    N, D, K = 3000, 4, 18
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    tr = []
+    for t in range(K):
+        row = []
+        for r in range(G):
+            n = 0 if (case == "ragged" and (t + r) % 3 == 0) else int(rng.integers(1, 400))
+            x = rng.zipf(1.2, n) % N if case == "dups" else rng.integers(0, N, n)
+            row.append(np.asarray(x, np.int64))
+        tr.append(row)
+    cfg = dict(N=N, D=D, L=64 * 8, A=8, policy="hybrid", pvp=1, W=5, V=5 * 2, reinsert=1, P=1)
+    if case == "period":
+        cfg.update(P=3, reinsert=0)
+    if case == "rr":
+        cfg.update(policy="rr", pvp=0)
+    np.savez(tmp_path / "trace.npz", scores=sc, **{f"t{t}_r{r}": tr[t][r] for t in range(K) for r in range(G)})
+    json.dump(cfg, open(tmp_path / "cfg.json", "w"))
+    launch(G, tmp_path, "edge", str(tmp_path))
+    ho = run_oracle(tr, G=G, scores=sc, **cfg)
+    for r in range(G):
+        assert json.load(open(tmp_path / f"r{r}.json"))["bad"] == 0
+        hg = np.load(tmp_path / f"hist{r}.npy")
+        assert np.array_equal(hg, ho[:, r, :]), (case, r, np.argwhere(hg != ho[:, r, :])[:3])
+
+
 @pytest.mark.parametrize("G,policy,pvp", [(2, "hybrid", 1), (2, "lru", 0), (3, "hybrid", 0), (4, "static", 1)])
 def test_multiprocess_parity(tmp_path, G, policy, pvp):
     launch(G, tmp_path, "gather", str(tmp_path), policy, str(pvp))
