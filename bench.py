@@ -384,6 +384,8 @@ def main():
                   "pvp_h2d_GBps_over_step": round(d["bytes_h2d_pvp"] / T / 1e9, 2),
                   "bypassed_per_step": d["bypassed"] / K, "evictions_per_step": d["evictions"] / K},
         "phases": phases,
+        # T_roof = max over tiers of bytes / peak, per step; reported as T_roof / T_meas
+        "step_roofline": step_roofline(d, K, T, R, pcie_peak, hbm_peak),
     }
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, G, trace, scores, table.numpy(), args, lines)
@@ -391,6 +393,7 @@ def main():
     if not args.no_ablation and G == 1:
         line["pvp_ablation"] = pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev)
         line["gpu_sampler_pipeline"] = gpu_sampler_pipeline(wl, g_, scores, table, lines, args, dev)
+        line["storage_per_epoch"] = epoch_storage(wl, g_, scores, lines, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if G > 1:
@@ -451,6 +454,69 @@ def pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev, train_ms=1
                             "victim_dropped_per_step": d["victim_dropped"] / steps,
                             "victim_lines": wl.victim_lines if pvp else 0}
     res["gather_speedup_pvp"] = round(res["pvp1"]["gather_GBps"] / res["pvp0"]["gather_GBps"], 4)
+    return res
+
+
+def step_roofline(d, K, T, R, pcie_peak, hbm_peak):
+    """Per-tier lower bound on the step time: H2D = storage + PVP rows,
+    D2H = admitted victims, HBM = every request's row written to out and read at its source,
+    plus every filled row written to its slot. T_roof = the slowest tier; frac = T_roof / T."""
+    h2d = (d["bytes_h2d_storage"] + d["bytes_h2d_pvp"]) / K
+    d2h = d["bytes_d2h_victim"] / K
+    hbm = (2 * d["requests"] + d["inserted"] + d["bypassed"]) * R / K
+    tiers = {"pcie_h2d": h2d / (pcie_peak * 1e9), "pcie_d2h": d2h / (pcie_peak * 1e9), "hbm": hbm / (hbm_peak * 1e9)}
+    bound = max(tiers, key=tiers.get)
+    t_roof = tiers[bound]
+    return {"bound_tier": bound, "t_roof_ms": round(t_roof * 1e3, 4), "t_meas_ms": round(T / K * 1e3, 4),
+            "frac": round(t_roof / (T / K), 4), "tier_ms": {k: round(v * 1e3, 4) for k, v in tiers.items()},
+            "peaks_GBps": {"pcie": round(pcie_peak, 2), "hbm": hbm_peak}}
+
+
+def epoch_storage(wl, g, scores, lines, dev, policies=("hybrid", "static", "lru"), pvp_row=True):
+    """The metric's second half: storage-tier bytes per epoch for the
+    bench workload — epoch 0 warms the cache, epoch 1 is measured; hybrid vs static-only vs
+    LRU at equal lines (+ hybrid with PVP). Counts-only runs of the CUDA path with 16-B rows
+    (counters do not depend on the payload); bytes reported for the workload's rows."""
+    import torch
+    import synth
+    from paper_2407_15264_b200 import LsmGnn, STATS_FIELDS
+    W = wl.window
+    ipe = -(-wl.N // wl.batch)  # iterations per epoch at G = 1
+    t0 = time.time()
+    trace = synth.make_trace_parallel(g, 1, wl.batch, wl.fanout, 2 * ipe, seed_train=wl.seeds["train"],
+                                      seed_s=wl.seeds["s"])
+    gen_s = time.time() - t0
+    ids = [torch.from_numpy(np.asarray(row[0], np.int64)).to(dev) for row in trace]
+    K = len(ids)
+    empty = torch.zeros(0, dtype=torch.int64, device=dev)
+    mb = max(x.numel() for x in ids)
+    out = torch.empty((mb, 16), dtype=torch.uint8, device=dev)
+    table = torch.zeros((wl.N, 16), dtype=torch.uint8, pin_memory=True)
+    F = {n: i for i, n in enumerate(STATS_FIELDS)}
+    res = {"iterations_per_epoch": ipe, "epochs": "0 warm-up, 1 measured", "lines": lines,
+           "row_bytes_reported": wl.R, "trace_gen_s": round(gen_s, 1)}
+    runs = [(p, 0) for p in policies] + ([("hybrid", 1)] if pvp_row else [])
+    for pol, pvp in runs:
+        c = LsmGnn(wl.N, 4, lines, wl.ways, wl.victim_lines if pvp else 0, scores, policy=pol, pvp=pvp, window=W,
+                   max_batch_ids=mb, device=dev.index)
+        c.attach_storage(table)
+        c.prefetch([ids[k] if k < K else empty for k in range(1, W + 1)], first_iter=1)
+        t1 = time.time()
+        for t in range(K):
+            c.gather(ids[t], out)
+            k = t + 1 + W
+            c.prefetch([ids[k] if k < K else empty], first_iter=k)
+        h = c.history(ipe, K - ipe) if K - ipe <= 4096 else None
+        c.close()
+        e1 = h.sum(axis=0)
+        u = max(int(e1[F["unique"]]), 1)
+        key = pol + ("+pvp" if pvp else "")
+        res[key] = {"storage_GB_per_epoch": round(int(e1[F["storage_reads"]]) * wl.R / 1e9, 3),
+                    "hit_ratio": round(int(e1[F["hits"]] + e1[F["victim_hits"]]) / u, 4),
+                    "run_s": round(time.time() - t1, 2)}
+    h = res["hybrid"]["storage_GB_per_epoch"]
+    res["hybrid_vs_static"] = round(h / res["static"]["storage_GB_per_epoch"], 4)
+    res["hybrid_vs_lru"] = round(h / res["lru"]["storage_GB_per_epoch"], 4)
     return res
 
 
