@@ -69,7 +69,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -99,12 +99,13 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def build_inputs(wl, G, rank, iters, seed_offset=0):
+def build_inputs(wl, G, rank, iters, only_mine=False):
     import synth
     t0 = time.time()
     g = synth.plcite(wl.N, wl.m, seed_g=wl.seeds["g"], seed_pi=wl.seeds["pi"])
     trace = synth.make_trace_parallel(g, G, wl.batch, wl.fanout, iters, seed_train=wl.seeds["train"],
-                                      seed_s=wl.seeds["s"], procs=max(1, (os.cpu_count() or 1) // max(G, 1)))
+                                      seed_s=wl.seeds["s"], procs=max(1, (os.cpu_count() or 1) // max(G, 1)),
+                                      ranks=[rank] if only_mine else None)
     scores = synth.static_scores(g)
     log(f"[bench] inputs: graph N={wl.N} m={wl.m}, {iters} iterations x {G} ranks in {time.time() - t0:.1f}s")
     return g, trace, scores
@@ -210,9 +211,13 @@ def main():
     pvp = wl.pvp if args.pvp is None else args.pvp
     lines = args.lines or wl.lines_per_gpu
     iters = Wu + K + E + W + 1
-    g_, trace, scores = build_inputs(wl, G, rank, iters)
+    g_, trace, scores = build_inputs(wl, G, rank, iters, only_mine=G > 1)
     mine = [np.asarray(trace[t][rank], np.int64) for t in range(iters)]
     max_ids = max(x.size for row in trace for x in row)
+    if G > 1:  # every rank must size its inboxes identically (the layout is checked at connect)
+        mx = torch.tensor([float(max_ids)], dtype=torch.float64, device=cdev)
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        max_ids = int(mx.item())
     t0 = time.time()
     table = table_for(wl.N, wl.D, wl.seeds["f"], pinned=True, home=rank, G=G)
     log(f"[bench] host table {table.numel() / 2**30:.2f} GiB pinned in {time.time() - t0:.1f}s")

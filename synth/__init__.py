@@ -211,10 +211,12 @@ def epoch_seeds(num_nodes: int, epoch: int, seed_train: int = 3) -> np.ndarray:
 
 
 def make_trace(g: Graph, G: int, batch: int, fanout, iters: int, seed_train: int = 3,
-               seed_s: int = 4, dedup: bool = True, t0: int = 0):
+               seed_s: int = 4, dedup: bool = True, t0: int = 0, ranks=None):
     """trace[t][r] = node IDs rank r gathers at iteration t (int64). Rank r at
     iteration t takes seeds perm[(t*G + r)*B : +B] of the epoch permutation
-    (SPEC.md S:145); an epoch is ceil(N/(B*G)) iterations."""
+    (SPEC.md S:145); an epoch is ceil(N/(B*G)) iterations. `ranks` limits which ranks'
+    lists are generated (the others are left empty) — a rank of a multi-process run only
+    needs its own."""
     N = g.num_nodes
     per_epoch = -(-N // (batch * G))
     trace = []
@@ -227,6 +229,9 @@ def make_trace(g: Graph, G: int, batch: int, fanout, iters: int, seed_train: int
         perm = cache[ep]
         row = []
         for r in range(G):
+            if ranks is not None and r not in ranks:
+                row.append(np.zeros(0, np.int64))
+                continue
             lo = (te * G + r) * batch
             s = perm[lo:lo + batch]
             row.append(sample_batch(g, s, fanout, seed_s, t, r, dedup=dedup))
@@ -238,21 +243,22 @@ _PAR_GRAPH = None
 
 
 def _trace_chunk(args):
-    G, batch, fanout, t0, n, seed_train, seed_s, dedup = args
-    return make_trace(_PAR_GRAPH, G, batch, fanout, n, seed_train, seed_s, dedup, t0)
+    G, batch, fanout, t0, n, seed_train, seed_s, dedup, ranks = args
+    return make_trace(_PAR_GRAPH, G, batch, fanout, n, seed_train, seed_s, dedup, t0, ranks)
 
 
 def make_trace_parallel(g: Graph, G: int, batch: int, fanout, iters: int, seed_train: int = 3, seed_s: int = 4,
-                        dedup: bool = True, procs: int | None = None):
+                        dedup: bool = True, procs: int | None = None, ranks=None):
     """make_trace split over worker processes (fork); identical output."""
     import multiprocessing as mp
     global _PAR_GRAPH
     procs = procs or min(16, os.cpu_count() or 1)
     if procs <= 1 or iters < 8:
-        return make_trace(g, G, batch, fanout, iters, seed_train, seed_s, dedup)
+        return make_trace(g, G, batch, fanout, iters, seed_train, seed_s, dedup, 0, ranks)
     _PAR_GRAPH = g
     step = -(-iters // procs)
-    jobs = [(G, batch, fanout, t0, min(step, iters - t0), seed_train, seed_s, dedup) for t0 in range(0, iters, step)]
+    jobs = [(G, batch, fanout, t0, min(step, iters - t0), seed_train, seed_s, dedup, ranks)
+            for t0 in range(0, iters, step)]
     with mp.get_context("fork").Pool(len(jobs)) as pool:
         parts = pool.map(_trace_chunk, jobs)
     _PAR_GRAPH = None
