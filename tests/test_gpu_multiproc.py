@@ -82,3 +82,15 @@ def test_multiprocess_parity(tmp_path, G, policy, pvp):
             raise AssertionError(f"home {r}: {len(bad)} mismatches, first {bad[0]}: gpu {hg[bad[0][0]]} "
                                  f"oracle {ho[bad[0][0], r]}")
     assert ho[:, :, 2].sum() > 0  # peer requests crossed homes
+    if pvp == 0:
+        # SURVEY.md §4 "Equivalence" on the GPU: G homes x L lines == 1 home x G*L lines on the
+        # merged batches (I8) — pins the directory and the exchange GPU against GPU
+        from .harness import run_gpu
+        merged = [[np.concatenate(row)] for row in tr]
+        h1, _, bad = run_gpu(merged, N=N, D=D, L=G * 1024, A=8, scores=sc, policy=policy, pvp=0, W=8)
+        assert bad == 0
+        hg = sum(np.load(tmp_path / f"hist{r}.npy").astype(np.int64) for r in range(G))
+        skip = {0, 2, 20}  # iter, peer_requests, bytes_nvlink
+        for f in range(hg.shape[1]):
+            if f not in skip:
+                assert np.array_equal(hg[:, f], h1[:, f].astype(np.int64)), f
