@@ -84,6 +84,8 @@ def main():
     ap.add_argument("--gpus", default="2,4,8")
     ap.add_argument("--sizes", default="1,2,5,10,20")
     ap.add_argument("--policies", default="hybrid,static,lru,rr,dynamic")
+    ap.add_argument("--scores", default="degree", choices=["degree", "rpr"],
+                    help="static information: degree, or reverse PageRank (the paper's choice, P:645)")
     args = ap.parse_args()
     import synth
     N = args.nodes
@@ -92,12 +94,18 @@ def main():
     train = np.arange(0, n_paper, 10, dtype=np.int64)  # 10% of the paper range (a typed ID range)
     t0 = time.time()
     g = synth.plcite(N, 12)
-    scores = synth.static_scores(g)
+    if args.scores == "rpr":
+        t1 = time.time()
+        scores = synth.quantize_scores(synth.reverse_pagerank(g))
+        print(f"reverse PageRank in {time.time() - t1:.0f}s", flush=True)
+    else:
+        scores = synth.static_scores(g)
     print(f"graph {N} nodes in {time.time() - t0:.0f}s", flush=True)
     results = {"workload": {"N": N, "typed_ranges": {"paper": [0, n_paper], "author": [n_paper, int(0.997 * N)],
                                                      "fos+institute": [int(0.997 * N), N]},
                             "train": int(train.size), "fanout": list(fanout), "batch_per_gpu": batch, "W": W,
-                            "T": W // 8, "ways": ways, "scores": "u8 rank-quantised degree", "row_bytes_run": 16,
+                            "T": W // 8, "ways": ways, "scores": "u8 rank-quantised " + ("reverse PageRank (d=0.85, tol 1e-6, <=100 it)"
+                                                                           if args.scores == "rpr" else "degree"), "row_bytes_run": 16,
                             "bytes_reported_for_row": 4096,
                             "note": "G-GPU runs executed as 1 home x G*L lines on merged batches (I8, exact "
                                     "for pvp=0); hybrid+pvp uses G*V victim lines"},
