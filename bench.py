@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--no-ablation", action="store_true", help="skip the PVP on/off ablation")
     p.add_argument("--lines", type=int, default=None, help="override lines per GPU")
+    p.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph (G = 1)")
     return p.parse_args()
 
 
@@ -232,9 +233,14 @@ def main():
     c.prefetch(ids_d[1:W + 1], first_iter=1)
 
     def step(t):
+        if args.graph and t >= 1:  # one CUDA-graph launch per step (captured after step 0)
+            c.graph_replay()
+            return
         c.gather(ids_d[t], out)
         k = t + 1 + W
         c.prefetch([ids_d[k]], first_iter=k)
+        if args.graph and t == 0:
+            c.graph_capture(ids_d, out)
 
     for t in range(Wu):
         step(t)

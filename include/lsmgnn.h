@@ -65,7 +65,9 @@ typedef enum {
  *   pvp             1 = victim buffer + PVP on; default 0
  *   window          W, iterations of look-ahead (W = 256 in P:607); default 256
  *   threshold       T; 0 => max(1, W/8) ("by default ... 1/8 of the window")
- *   update_period   P; only 1 (exact dynamic information) is implemented (R6)
+ *   update_period   P (the paper uses 4); 0 or 1 = exact information every
+ *                   iteration; P > 1 = a window scan of every resident line every P-th
+ *                   iteration, lines inserted since (or stale) are Fresh (R6, R7); default 1
  *   reinsert_victims 1 = a victim-buffer hit is re-inserted into the cache (R15); default 1
  *   max_batch_ids   capacity: the largest n any rank passes to gather/prefetch; default 1<<20 */
 typedef struct {
@@ -181,6 +183,21 @@ int lsmgnn_sampler_attach(const int64_t* indptr, const int32_t* indices, int64_t
 int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, int32_t nlayers, uint64_t seed,
                   int64_t t, int32_t r, int64_t* out, int64_t cap, int64_t* count_dev, void* stream);
 int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t first_iter, void* stream);
+
+/* ---- CUDA-graph step (G = 1): one captured launch per iteration.
+ * lsmgnn_graph_capture records ONE step — gather(t) of batch ids_ring[t mod ring_len]
+ * (length n_ring[t mod ring_len]) into `out`, then the window feed of batch t+1+W from the
+ * same ring — as a CUDA graph whose kernels take every per-iteration value from the device
+ * (no host parameter changes between replays). lsmgnn_graph_replay(stream) launches it for
+ * the next iteration, plus the PVP side-stream copy when pvp = 1.
+ *   ids_ring: device array of ring_len device pointers (int64 IDs); n_ring: device
+ *   int64[ring_len]; ring_len >= W + 2; out: device or pinned host, >= max_batch_ids * R
+ *   bytes. Capture requires the window fed through t+W (the state after any gather/prefetch
+ *   pair). Replays advance the same counters as lsmgnn_gather + lsmgnn_prefetch, so the two
+ *   styles may be mixed. Returns EINVAL for G > 1. */
+int lsmgnn_graph_capture(const int64_t* const* ids_ring, const int64_t* n_ring, int32_t ring_len, void* out,
+                         void* stream);
+int lsmgnn_graph_replay(void* stream);
 
 /* Counters of this home: scope 0 = the last completed gather, 1 = cumulative.
  * Synchronises with the last stream used. */

@@ -24,7 +24,7 @@ EXPORTS = ["lsmgnn_bind", "lsmgnn_set_options", "lsmgnn_init", "lsmgnn_attach_st
            "lsmgnn_export_handle", "lsmgnn_connect", "lsmgnn_gather", "lsmgnn_gather_host", "lsmgnn_prefetch",
            "lsmgnn_stats", "lsmgnn_stats_history", "lsmgnn_kernel_launches", "lsmgnn_finalize",
            "lsmgnn_last_error", "lsmgnn_profile", "lsmgnn_profile_read", "lsmgnn_sampler_attach", "lsmgnn_sample",
-           "lsmgnn_prefetch_dev"]
+           "lsmgnn_prefetch_dev", "lsmgnn_graph_capture", "lsmgnn_graph_replay"]
 PHASES = ["route", "dedup", "probe_replace", "admit", "fill", "pull", "window", "pvp"]
 
 
@@ -78,6 +78,8 @@ def load_library(path: str = SO_PATH) -> ctypes.CDLL:
         "lsmgnn_sampler_attach": ([vp, vp, i64, i64], i32),
         "lsmgnn_sample": ([vp, i64, vp, i32, ctypes.c_uint64, i64, i32, vp, i64, vp, vp], i32),
         "lsmgnn_prefetch_dev": ([vp, vp, i64, vp], i32),
+        "lsmgnn_graph_capture": ([vp, vp, i32, vp, vp], i32),
+        "lsmgnn_graph_replay": ([vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -204,6 +206,22 @@ class LsmGnn:
         arr = (Stats * max(count, 1))()
         _check(_LIB.lsmgnn_stats_history(arr, first, count))
         return np.stack([arr[i].as_array() for i in range(count)]) if count else np.zeros((0, 24), np.uint64)
+
+    def graph_capture(self, batches, out, stream=None):
+        """CUDA-graph step (G = 1): capture gather(t) + window feed of t+1+W over the ring of
+        device batches `batches` (iteration k uses batches[k % len]); returns nothing — replay
+        with graph_replay(). Keeps the pointer/count tables alive."""
+        import torch
+        dev = out.device
+        self._ring_ptrs = torch.tensor([b.data_ptr() for b in batches], dtype=torch.int64, device=dev)
+        self._ring_n = torch.tensor([b.numel() for b in batches], dtype=torch.int64, device=dev)
+        self._ring_keep = list(batches)
+        _check(_LIB.lsmgnn_graph_capture(ctypes.c_void_p(self._ring_ptrs.data_ptr()),
+                                         ctypes.c_void_p(self._ring_n.data_ptr()), len(batches),
+                                         ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))))
+
+    def graph_replay(self, stream=None) -> None:
+        _check(_LIB.lsmgnn_graph_replay(ctypes.c_void_p(_stream_ptr(stream))))
 
     @staticmethod
     def profile(enable: bool) -> None:

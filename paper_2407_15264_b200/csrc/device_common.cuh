@@ -53,6 +53,27 @@ struct Scratch {
   uint32_t pad[7];
 };
 
+// Per-iteration values, resident on the device. k_begin / k_win_begin write them (from host
+// arguments, or — when a captured CUDA graph replays — from the device's own counters and the
+// caller's ring of batch pointers); every other kernel reads them, so a whole step can be
+// replayed without any per-iteration host parameter.
+constexpr uint32_t kHist = 4096;  // per-iteration records kept on the device
+struct IterState {
+  uint64_t t;                 // iteration of the current gather
+  uint64_t t_next;            // graph replay: the next gather iteration
+  const int64_t* ids;         // this rank's request IDs of gather t (device)
+  int64_t n;                  // their count
+  uint32_t stamp, p0, par, upd;  // t+1; (t+1) mod (W+1); t & 1; periodic scan at t
+  uint32_t rec_idx;           // t mod kHist (history record)
+  uint32_t stage_base;        // pool row of the PVP staging buffer for parity t & 1
+  // window feed (lsmgnn_prefetch): the batch of iteration wk
+  uint64_t wk, wk_next;
+  const int64_t* wids;
+  int64_t wn;
+  uint32_t wslot;             // wk mod (W+1): ring slot and mask bit
+  uint32_t done;              // grid-completion counter (k_mask_clear)
+};
+
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // Warp-aggregated atomicAdd of `inc` per lane: one atomic per warp. Must be called

@@ -19,12 +19,41 @@
 namespace lsm {
 
 // ------------------------------------------------------------------------------ S9
-// Zero this iteration's record and the per-batch scratch counters.
-__global__ void k_begin(unsigned long long* rec, Scratch* scr, uint64_t t) {
+// Start gather t: publish the iteration's values (IterState), zero its record, the per-batch
+// scratch counters and the local inbox count. t_host >= 0: t and the batch come from the
+// host; t_host < 0 (graph replay): t = it->t_next, batch = ids_ring[t mod ring_len].
+struct BeginArgs {
+  int64_t t_host;
+  const int64_t* ids_host;
+  int64_t n_host;
+  const int64_t* const* ids_ring;  // graph replay: device array of batch pointers
+  const int64_t* n_ring;           // and their lengths
+  uint32_t ring_len;
+  uint32_t Wp1, period, L, C;
+  uint32_t* inbox_cnt;             // zeroed (G = 1), may be null
+};
+__global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, BeginArgs a) {
+  const uint64_t t = a.t_host >= 0 ? (uint64_t)a.t_host : it->t_next;
+  unsigned long long* rec = hist + (size_t)(t % kHist) * F_NFIELDS;
   const int i = threadIdx.x;
   if (i < F_NFIELDS) rec[i] = 0;
   __syncthreads();
   if (i == 0) {
+    it->t = t;
+    if (a.t_host >= 0) {
+      it->ids = a.ids_host;
+      it->n = a.n_host;
+    } else {
+      const uint32_t k = (uint32_t)(t % a.ring_len);
+      it->ids = a.ids_ring[k];
+      it->n = a.n_ring[k];
+    }
+    it->stamp = (uint32_t)(t + 1);
+    it->p0 = (uint32_t)((t + 1) % a.Wp1);
+    it->par = (uint32_t)(t & 1);
+    it->upd = a.period <= 1 || t % a.period == 0;
+    it->rec_idx = (uint32_t)(t % kHist);
+    it->stage_base = a.L + (uint32_t)(t & 1) * a.C;
     rec[F_ITER] = t;
     rec[F_PREF] = scr->staged[t & 1];
     scr->nuniq = 0;
@@ -32,14 +61,18 @@ __global__ void k_begin(unsigned long long* rec, Scratch* scr, uint64_t t) {
     scr->ncand = 0;
     scr->nbypass = 0;
     scr->nreq = 0;
+    if (a.inbox_cnt) *a.inbox_cnt = 0;
   }
 }
 
 // Close the record: algorithmic bytes per tier, cumulative sums; the staging count of
-// the next parity is reset so that a missing PVP call stages nothing.
-__global__ void k_end(unsigned long long* rec, unsigned long long* cum, Scratch* scr, uint64_t t,
-                      uint32_t R) {
+// the next parity is reset so that a missing PVP call stages nothing. The ERANGE counter is
+// mirrored to pinned host memory; a graph replay advances it->t_next.
+__global__ void k_end(IterState* it, unsigned long long* hist, unsigned long long* cum, Scratch* scr, uint32_t R,
+                      volatile uint32_t* bad_mirror, uint32_t advance) {
   if (threadIdx.x != 0) return;
+  const uint64_t t = it->t;
+  unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
   rec[F_UNIQUE] = scr->nuniq;
   rec[F_REQ] = scr->nreq;
   rec[F_BOUT] = rec[F_REQ] * R;
@@ -50,13 +83,42 @@ __global__ void k_end(unsigned long long* rec, unsigned long long* cum, Scratch*
   for (int f = 1; f < F_NFIELDS; ++f) cum[f] += rec[f];
   cum[F_ITER] = t;
   scr->staged[(t + 1) & 1] = 0;
+  *bad_mirror = scr->bad_ids;
+  it->t_next = t + 1;  // direct calls and graph replays may be mixed
+  (void)advance;
+}
+
+// Start the window feed of one batch (iteration wk): k_host >= 0 from the host, else (graph
+// replay) wk = it->wk_next with the batch from the ring.
+__global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host,
+                            const int64_t* n_dev, const int64_t* const* ids_ring, const int64_t* n_ring,
+                            uint32_t ring_len, uint32_t Wp1) {
+  if (threadIdx.x != 0) return;
+  const uint64_t k = k_host >= 0 ? (uint64_t)k_host : it->wk_next;
+  it->wk = k;
+  it->wslot = (uint32_t)(k % Wp1);
+  if (k_host >= 0) {
+    it->wids = ids_host;
+    it->wn = n_dev ? *n_dev : n_host;  // n_dev: a length produced on the device (lsmgnn_sample)
+  } else {
+    const uint32_t j = (uint32_t)(k % ring_len);
+    it->wids = ids_ring[j];
+    it->wn = n_ring[j];
+  }
+  it->wk_next = k + 1;
 }
 
 // ------------------------------------------------------------------------------ S1 (G = 1)
-// Validate the caller's int64 IDs and write them (u32) into this home's inbox.
-__global__ void k_route_local(const int64_t* __restrict__ ids, int64_t n, uint64_t N,
-                              uint32_t* __restrict__ inbox, uint32_t* __restrict__ inbox_cnt,
-                              Scratch* scr, uint32_t* __restrict__ inbox_i) {
+// Validate the caller's int64 IDs and write them (u32) into this home's inbox (gather) or a
+// window ring slot (prefetch): ids/n = it->ids/n or it->wids/wn; output slot = *slot_ptr.
+__global__ void k_route_local(const IterState* it, uint32_t window, uint64_t N, uint32_t* __restrict__ out_base,
+                              uint64_t out_stride, uint32_t* __restrict__ cnt_base, Scratch* scr,
+                              uint32_t* __restrict__ inbox_i) {
+  const int64_t* __restrict__ ids = window ? it->wids : it->ids;
+  const int64_t n = window ? it->wn : it->n;
+  const uint32_t slot = window ? it->wslot : 0u;
+  uint32_t* __restrict__ inbox = out_base + (size_t)slot * out_stride;
+  uint32_t* inbox_cnt = cnt_base + slot;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -76,26 +138,6 @@ __global__ void k_route_local(const int64_t* __restrict__ ids, int64_t n, uint64
   }
 }
 
-// Same, with the length read on the device (*n_dev), grid sized by the host's bound.
-__global__ void k_route_local_dev(const int64_t* __restrict__ ids, const int64_t* n_dev, int64_t bound, uint64_t N,
-                                  uint32_t* __restrict__ inbox, uint32_t* __restrict__ inbox_cnt, Scratch* scr) {
-  const int64_t n = min(*n_dev, bound);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    bool ok = false;
-    uint32_t v = 0;
-    if (i < n) {
-      const int64_t x = ids[i];
-      ok = x >= 0 && (uint64_t)x < N;
-      v = (uint32_t)x;
-      if (!ok) atomicAdd(&scr->bad_ids, 1u);
-    }
-    const uint32_t pos = warp_reserve(inbox_cnt, ok ? 1u : 0u);
-    if (ok) inbox[pos] = v;
-  }
-}
-
 // ------------------------------------------------------------------------------ S1 (G > 1)
 // Requester side of the communication layer: bucket each valid ID by its
 // home g = v mod G and store it straight into home g's inbox slot [me] through the
@@ -105,9 +147,10 @@ struct RouteArgs {
   uint32_t* route_cnt; // [G] local counters
   uint32_t G;
 };
-__global__ void k_route_peer(const int64_t* __restrict__ ids, int64_t n, uint64_t N, RouteArgs a,
-                             Scratch* scr) {
+__global__ void k_route_peer(const IterState* it, uint32_t window, uint64_t N, RouteArgs a, Scratch* scr) {
   __shared__ uint32_t s_cnt[8], s_base[8];
+  const int64_t* __restrict__ ids = window ? it->wids : it->ids;
+  const int64_t n = window ? it->wn : it->n;
   const int64_t tile = blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * tile; base < n; base += (int64_t)gridDim.x * tile) {
     if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
@@ -151,9 +194,11 @@ __global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
 // its node's list: head[q] = stamp<<32 | last position, nxt[pos] = previous (kInvalid = end).
 __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
                         uint32_t nsrc, uint32_t cap, uint32_t me, uint32_t G, uint32_t S,
-                        uint32_t stamp, uint32_t* __restrict__ mark, uint32_t* __restrict__ uniq,
-                        uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* rec,
+                        const IterState* it, uint32_t* __restrict__ mark, uint32_t* __restrict__ uniq,
+                        uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* hist,
                         unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt) {
+  const uint32_t stamp = it->stamp;
+  unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
   uint32_t nreq = 0, npeer = 0;
   for (uint32_t r = 0; r < nsrc; ++r) {
     const uint32_t n = inbox_cnt[r];
@@ -189,10 +234,11 @@ __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __re
 
 // Exclusive scan of set_cnt[0..S) into set_off[0..S] by one CTA (1024 threads).
 // The same CTA counts staged PVP rows that this batch did not request (pvp_unused).
+// stg_base (null when there is no PVP): the two staging node lists, C entries each.
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off,
-                                               uint32_t n, const uint32_t* __restrict__ stg_nodes,
-                                               const uint32_t* staged_count, const uint32_t* __restrict__ mark,
-                                               uint32_t stamp, uint32_t G, unsigned long long* rec) {
+                                               uint32_t n, const uint32_t* __restrict__ stg_base, uint32_t C,
+                                               const Scratch* scr, const uint32_t* __restrict__ mark,
+                                               const IterState* it, uint32_t G, unsigned long long* hist) {
   __shared__ uint32_t s_warp[32];
   const uint32_t tid = threadIdx.x;
   const uint32_t per = (n + 1023) / 1024;
@@ -225,12 +271,15 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt,
   }
   if (tid == 1023) off[n] = run;
   // pvp_unused: staged rows whose node this batch did not request
-  if (stg_nodes) {
-    const uint32_t ns = *staged_count;
+  if (stg_base) {
+    const uint32_t par = it->par, stamp = it->stamp;
+    const uint32_t* stg_nodes = stg_base + (size_t)par * C;
+    const uint32_t ns = scr->staged[par];
     uint32_t unused = 0;
     for (uint32_t j = tid; j < ns; j += 1024) unused += mark[stg_nodes[j] / G] != stamp;
     unused = __reduce_add_sync(0xffffffffu, unused);
-    if ((tid & 31) == 0 && unused) atomicAdd(&rec[F_UNUSED], (unsigned long long)unused);
+    if ((tid & 31) == 0 && unused)
+      atomicAdd(&hist[(size_t)it->rec_idx * F_NFIELDS + F_UNUSED], (unsigned long long)unused);
   }
 }
 
@@ -252,7 +301,9 @@ __global__ void k_bucket(const uint32_t* __restrict__ uniq, const Scratch* scr, 
 // determine the next reuse iteration for the cache-lines that currently reside in the cache
 // before the feature aggregation stage"), run every P-th iteration.
 __global__ void k_snapshot(const uint32_t* __restrict__ tags, uint32_t L, uint32_t G, const uint32_t* __restrict__ mask,
-                           uint32_t MW, uint32_t p0, uint32_t W, uint32_t t, uint32_t* __restrict__ line_info) {
+                           uint32_t MW, uint32_t W, const IterState* it, uint32_t* __restrict__ line_info) {
+  if (!it->upd) return;  // not a scan iteration (t mod P != 0)
+  const uint32_t p0 = it->p0, t = (uint32_t)it->t;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
     const uint32_t x = tags[i];
     uint32_t info = kInfoNone;
@@ -279,15 +330,14 @@ struct SetParams {
   FillEnt* fills;
   Cand* cands;
   Scratch* scr;
-  unsigned long long* rec;
+  const IterState* it;       // t, stamp, p0, staging parity, record of this iteration
+  unsigned long long* hist;
   uint32_t S, A, G, W, T, MW;
   uint32_t policy, pvp, reinsert;
-  uint32_t t, stamp, p0;
   uint32_t P;            // per-warp capacity (power of two >= max bucket)
   uint32_t period;       // dynamic-information update period; 1 = exact every batch
   uint32_t* line_info;   // period > 1: per-line snapshot (reuse iteration / kInfoNone / kInfoFresh)
   uint32_t warp_bytes;   // per-warp shared memory
-  uint32_t stage_base;   // pool row of this iteration's PVP staging buffer
   uint32_t bypass_base;  // pool row of the bypass staging area
   uint32_t deliver;      // kDelivered when k_serve delivers filled rows (G = 1), else 0
 };
@@ -351,7 +401,10 @@ __global__ void k_set(SetParams p) {
   uint32_t* svict = stag + 32;
   int* sd = reinterpret_cast<int*>(svict + 32);
   int* scls = sd + 32;
-  const bool upd = p.period <= 1 || p.t % p.period == 0;  // exact information for incoming misses
+  // per-iteration values (device-resident, written by k_begin)
+  const uint32_t t_ = (uint32_t)p.it->t, stamp_ = p.it->stamp, p0_ = p.it->p0, stage_base_ = p.it->stage_base;
+  unsigned long long* rec_ = p.hist + (size_t)p.it->rec_idx * F_NFIELDS;
+  const bool upd = p.it->upd != 0;  // exact information for incoming misses
 
   uint32_t ctr[C_N];
 #pragma unroll
@@ -375,10 +428,10 @@ __global__ void k_set(SetParams p) {
     int d = 0, cls = kNoReuse;  // next reuse distance (0 = none) and class of the resident line
     if (tg != kInvalid) {
       if (p.period <= 1) {  // exact, from the window bitmask (P = 1)
-        d = next_reuse_d(p.mask + (size_t)(tg / G) * p.MW, p.p0, p.W);
+        d = next_reuse_d(p.mask + (size_t)(tg / G) * p.MW, p0_, p.W);
         cls = class_of(d, p.T);
       } else {              // the last window scan's snapshot
-        cls = class_of_info(p.line_info[s * A + lane], p.t, p.T, &d);
+        cls = class_of_info(p.line_info[s * A + lane], t_, p.T, &d);
       }
     }
     sd[lane] = d;
@@ -401,7 +454,7 @@ __global__ void k_set(SetParams p) {
           protm |= 1u << way;
           p.node_loc[q] = s * A + (uint32_t)way;
           ++ctr[C_HIT];
-        } else if (p.vst_stamp[q] == p.stamp) {
+        } else if (p.vst_stamp[q] == stamp_) {
           kind = kVHit;
           ++ctr[C_VHIT];
         } else {
@@ -415,7 +468,7 @@ __global__ void k_set(SetParams p) {
     protm = __reduce_or_sync(0xffffffffu, protm);
     __syncwarp();
     const uint32_t nH = __popc(protm);
-    if ((protm >> lane) & 1u) p.last_use[s * A + lane] = p.t;  // hits are protected, last use = t
+    if ((protm >> lane) & 1u) p.last_use[s * A + lane] = t_;  // hits are protected, last use = t
 
     // ---- M = misses to insert, ascending node order
     uint32_t nM = 0;
@@ -439,10 +492,10 @@ __global__ void k_set(SetParams p) {
           const uint32_t v = sv[sidx[k]];
           int dv = 0, cv = kFresh;  // a miss has no information until the next scan ...
           if (upd && (p.policy == 0 || p.policy == 4)) {  // ... except at a scan iteration
-            dv = next_reuse_d(p.mask + (size_t)(v / G) * p.MW, p.p0, p.W);
+            dv = next_reuse_d(p.mask + (size_t)(v / G) * p.MW, p0_, p.W);
             cv = class_of(dv, p.T);
           }
-          key = policy_key(p, v, p.t, cv, dv);
+          key = policy_key(p, v, t_, cv, dv);
         }
         skey[k] = key;
       }
@@ -536,7 +589,7 @@ __global__ void k_set(SetParams p) {
         ++ctr[C_EV0 + cx];
         if (p.pvp && (cx == kNear || cx == kFar)) {
           is_cand = true;
-          reuse = p.t + (uint32_t)dx;
+          reuse = t_ + (uint32_t)dx;
         } else {
           ++ctr[C_ENR];
         }
@@ -546,14 +599,14 @@ __global__ void k_set(SetParams p) {
       if (act) {
         const uint32_t slot = s * A + way;
         FillEnt f;
-        f.src = kind == kVHit ? p.stage_base + p.vst_idx[q] : (kHostBit | q);
+        f.src = kind == kVHit ? stage_base_ + p.vst_idx[q] : (kHostBit | q);
         f.dst = slot;
         f.victim = kInvalid;
         f.node = v;
         p.fills[fidx] = f;
         p.node_loc[q] = slot | p.deliver;
         p.tags[slot] = v;
-        p.last_use[slot] = p.t;
+        p.last_use[slot] = t_;
         if (p.period > 1) p.line_info[slot] = kInfoFresh;
         ++ctr[C_INS];
         if (is_cand) {
@@ -578,7 +631,7 @@ __global__ void k_set(SetParams p) {
         const uint32_t kind = info & 3u;
         const bool inM = (info >> 10) & 1u, byp = (info >> 11) & 1u;
         v = sv[j];
-        if (kind == kVHit && (!inM || byp)) p.node_loc[v / G] = p.stage_base + p.vst_idx[v / G];
+        if (kind == kVHit && (!inM || byp)) p.node_loc[v / G] = stage_base_ + p.vst_idx[v / G];
         bs = kind == kStorage && byp;
       }
       const uint32_t b = warp_reserve(&p.scr->nbypass, bs ? 1u : 0u);
@@ -603,7 +656,7 @@ __global__ void k_set(SetParams p) {
     if (lane == 0 && x) atomicAdd(&s_ctr[c], (unsigned long long)x);
   }
   __syncthreads();
-  if (threadIdx.x < C_N && s_ctr[threadIdx.x]) atomicAdd(&p.rec[kCtrField[threadIdx.x]], s_ctr[threadIdx.x]);
+  if (threadIdx.x < C_N && s_ctr[threadIdx.x]) atomicAdd(&rec_[kCtrField[threadIdx.x]], s_ctr[threadIdx.x]);
 }
 
 // ------------------------------------------------------------------------------ S5: admission
@@ -629,8 +682,10 @@ __global__ void k_qscatter(const Cand* __restrict__ cands, const Scratch* scr, u
 __global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, const uint32_t* __restrict__ qoff,
                                                const uint32_t* __restrict__ qb, uint32_t* __restrict__ qlen,
                                                uint32_t* __restrict__ qnode, uint32_t* __restrict__ qreuse,
-                                               FillEnt* __restrict__ fills, uint32_t C, unsigned long long* rec) {
+                                               FillEnt* __restrict__ fills, uint32_t C, const IterState* it,
+                                               unsigned long long* rec_hist) {
   __shared__ uint32_t hist[256];
+  unsigned long long* rec = rec_hist + (size_t)it->rec_idx * F_NFIELDS;
   __shared__ uint32_t s_prefix, s_want, s_taken;
   const uint32_t k = blockIdx.x;
   const uint32_t lo = qoff[k], nk = qoff[k + 1] - lo;
@@ -722,8 +777,9 @@ struct PullArgs {
   uint32_t G;
 };
 template <int UNROLL, int OUT>
-__global__ void k_pull(const int64_t* __restrict__ ids, int64_t n, uint64_t N, PullArgs a,
-                       uint4* __restrict__ out, uint32_t nvec) {
+__global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __restrict__ out, uint32_t nvec) {
+  const int64_t* __restrict__ ids = it->ids;
+  const int64_t n = it->n;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < n; i += nwarps) {
@@ -750,8 +806,11 @@ template <int UNROLL, int OUT>
 __global__ void k_serve(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
                         const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
                         const unsigned long long* __restrict__ head, const uint32_t* __restrict__ nxt,
-                        const uint32_t* __restrict__ inbox_i, uint32_t stamp, const int64_t* __restrict__ ids,
-                        int64_t n, uint64_t N, const uint32_t* __restrict__ node_loc, uint4* __restrict__ out) {
+                        const uint32_t* __restrict__ inbox_i, const IterState* it, uint64_t N,
+                        const uint32_t* __restrict__ node_loc, uint4* __restrict__ out) {
+  const uint32_t stamp = it->stamp;
+  const int64_t* __restrict__ ids = it->ids;
+  const int64_t n = it->n;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t npull = nw >= 8 ? nw / 8 : 1;
@@ -804,26 +863,42 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, const Scratch* scr, u
 }
 
 // ------------------------------------------------------------------------------ S10
-// Window feed. Bit (k mod (W+1)) of mask[q] is set when node q*G+me is in B_k.
-// k_mask_clear drops iteration k's bits (the list stored in its ring slot); k_win_store
-// stores the new batch (u32) into the slot and sets its bits.
-__global__ void k_mask_clear(const uint32_t* __restrict__ list, const uint32_t* len, uint32_t G,
-                             uint32_t MW, uint32_t bit, uint32_t* __restrict__ mask) {
-  const uint32_t n = *len;
+// Window feed. Bit (k mod (W+1)) of mask[q] is set when node q*G+me is in B_k. The ring slot
+// and bit of the batch being fed is it->wslot. k_mask_clear drops the bits of the iteration
+// that last used the slot (its stored list) and then — last CTA out — empties the slot;
+// k_route_local / k_win_gather store the new batch; k_mask_set sets its bits.
+__global__ void k_mask_clear(const uint32_t* __restrict__ ring, uint64_t stride, uint32_t* ring_len, IterState* it,
+                             uint32_t G, uint32_t MW, uint32_t* __restrict__ mask) {
+  const uint32_t bit = it->wslot;
+  const uint32_t* __restrict__ list = ring + (size_t)bit * stride;
+  const uint32_t n = ring_len[bit];
   const uint32_t m = ~(1u << (bit & 31));
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     atomicAnd(&mask[(size_t)(list[i] / G) * MW + (bit >> 5)], m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&it->done, 1u) == gridDim.x - 1) {
+      ring_len[bit] = 0;
+      it->done = 0;
+    }
+  }
 }
-__global__ void k_mask_set(const uint32_t* __restrict__ list, const uint32_t* len, uint32_t G,
-                           uint32_t MW, uint32_t bit, uint32_t* __restrict__ mask) {
-  const uint32_t n = *len;
+__global__ void k_mask_set(const uint32_t* __restrict__ ring, uint64_t stride, const uint32_t* ring_len,
+                           const IterState* it, uint32_t G, uint32_t MW, uint32_t* __restrict__ mask) {
+  const uint32_t bit = it->wslot;
+  const uint32_t* __restrict__ list = ring + (size_t)bit * stride;
+  const uint32_t n = ring_len[bit];
   const uint32_t m = 1u << (bit & 31);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     atomicOr(&mask[(size_t)(list[i] / G) * MW + (bit >> 5)], m);
 }
-// Copy the inboxes of all sources (window IDs routed to this home) into one ring slot.
+// Copy the inboxes of all sources (window IDs routed to this home) into the ring slot.
 __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
-                             uint32_t nsrc, uint32_t cap, uint32_t* __restrict__ slot, uint32_t* slot_len) {
+                             uint32_t nsrc, uint32_t cap, uint32_t* __restrict__ ring, uint64_t stride,
+                             uint32_t* ring_len, const IterState* it) {
+  const uint32_t slot_i = it->wslot;
+  uint32_t* __restrict__ slot = ring + (size_t)slot_i * stride;
   uint32_t base = 0;
   for (uint32_t r = 0; r < nsrc; ++r) {
     const uint32_t n = inbox_cnt[r];
@@ -831,7 +906,7 @@ __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t*
       slot[base + i] = inbox[(size_t)r * cap + i];
     base += n;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *slot_len = base;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ring_len[slot_i] = base;
 }
 
 // ------------------------------------------------------------------------------ S11
@@ -839,18 +914,23 @@ __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t*
 // staging buffer and publish the staging directory (vst_stamp/vst_idx) for gather(t+1).
 // Entries whose recorded reuse is not t+1 are dropped (R17). The last CTA empties the queue.
 template <int UNROLL>
-__global__ void k_pvp(uint32_t k, uint32_t t1, uint32_t stamp1, uint32_t C, uint32_t G,
+__global__ void k_pvp(const IterState* it, uint32_t W, uint32_t L, uint32_t C, uint32_t G,
                       uint32_t* __restrict__ qlen, const uint32_t* __restrict__ qnode,
                       const uint32_t* __restrict__ qreuse, const uint4* __restrict__ hostq,
-                      uint4* __restrict__ pool, uint32_t stage_base, uint32_t* __restrict__ stg_nodes,
+                      uint4* __restrict__ pool, uint32_t* __restrict__ stg_base,
                       uint32_t* __restrict__ vst_stamp, uint32_t* __restrict__ vst_idx, Scratch* scr,
-                      uint32_t par, uint32_t nvec) {
+                      uint32_t nvec) {
+  // runs after gather(t): stage victim queue (t+1) mod W for iteration t+1
+  const uint64_t t1 = it->t + 1;
+  const uint32_t k = (uint32_t)(t1 % W), stamp1 = (uint32_t)(t1 + 1), par = (uint32_t)(t1 & 1);
+  const uint32_t stage_base = L + par * C;
+  uint32_t* __restrict__ stg_nodes = stg_base + (size_t)par * C;
   const uint32_t n = qlen[k];
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t j = warp; j < n; j += nwarps) {
     const size_t e = (size_t)k * C + j;
-    if (qreuse[e] != t1) continue;
+    if (qreuse[e] != (uint32_t)t1) continue;
     uint32_t m = 0;
     if (lane_id() == 0) m = atomicAdd(&scr->staged[par], 1u);
     m = __shfl_sync(0xffffffffu, m, 0);

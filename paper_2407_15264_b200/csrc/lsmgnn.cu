@@ -26,7 +26,6 @@ using namespace lsm;
 namespace {
 
 constexpr int kMaxG = 8;
-constexpr int64_t kHist = 4096;  // per-iteration records kept on the device
 
 struct Handle {  // exported per rank for lsmgnn_connect
   cudaIpcMemHandle_t ipc;
@@ -72,7 +71,15 @@ struct Ctx {
   FillEnt* fills = nullptr;
   Cand* cands = nullptr;
   Scratch* scr = nullptr;
+  IterState* it = nullptr;  // per-iteration values on the device (kernels read, k_begin writes)
   unsigned long long *hist = nullptr, *cum = nullptr;
+
+  // captured CUDA graph of one step (G = 1)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  int64_t graph_launches = 0;  // kernels per replay
+  bool graph_out_host = false;
 
   // host tiers
   uint8_t* qrows_host = nullptr;  // pinned victim queues [W*C][R]
@@ -199,7 +206,7 @@ int flag_wait(cudaStream_t st, uint32_t* addr, uint32_t value) {
 
 // Route `n` int64 IDs of this requester to the homes' inboxes (gather: win=false) and run the
 // flag exchange so that, on return (stream order), every home's inbox for this round is full.
-int exchange_ids(const int64_t* ids, int64_t n, bool win, uint32_t seq, cudaStream_t st) {
+int exchange_ids(int64_t n_bound, bool win, uint32_t seq, cudaStream_t st) {
   const int G = g.world;
   uint32_t* myflags = flags_of(g.arena);
   if (win) {  // the homes must have consumed the previous window round
@@ -218,8 +225,8 @@ int exchange_ids(const int64_t* ids, int64_t n, bool win, uint32_t seq, cudaStre
   ra.G = (uint32_t)G;
   pa.G = (uint32_t)G;
   pa.me = (uint32_t)g.rank;
-  if (n > 0) {
-    k_route_peer<<<grid_for(n, 256, 4), 256, 0, st>>>(ids, n, g.N, ra, g.scr);
+  if (n_bound > 0) {
+    k_route_peer<<<grid_for(n_bound, 256, 4), 256, 0, st>>>(g.it, win ? 1u : 0u, g.N, ra, g.scr);
     LAUNCHED();
   }
   k_route_publish<<<1, 32, 0, st>>>(g.route_cnt, pa);
@@ -261,7 +268,7 @@ int free_all() {
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off,
                   g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
                   g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.head, g.nxt, g.inbox_i, g.line_info, g.score, g.fills, g.cands,
-                  g.scr, g.hist,
+                  g.scr, g.it, g.hist,
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -275,6 +282,9 @@ int free_all() {
   if (g.qrows_host) cudaFreeHost(g.qrows_host);
   if (g.bad_host) cudaFreeHost((void*)g.bad_host);
   if (g.table_registered) cudaHostUnregister((void*)g.table_host);
+  if (g.graph_exec) cudaGraphExecDestroy(g.graph_exec);
+  if (g.graph) cudaGraphDestroy(g.graph);
+  if (g.cap_stream) cudaStreamDestroy(g.cap_stream);
   if (g.side) cudaStreamDestroy(g.side);
   if (g.ev_main) cudaEventDestroy(g.ev_main);
   if (g.ev_pvp) cudaEventDestroy(g.ev_pvp);
@@ -306,6 +316,249 @@ lsmgnn_options default_options() {
   o.reinsert_victims = 1;
   o.max_batch_ids = 1 << 20;
   return o;
+}
+
+// ---- one step's launches. Per-iteration values reach the kernels through g.it (written by
+// k_begin / k_win_begin), so the same sequence serves direct calls and CUDA-graph capture.
+BeginArgs begin_args(int64_t t_host, const int64_t* ids, int64_t n, const int64_t* const* ids_ring,
+                     const int64_t* n_ring, uint32_t ring_len) {
+  BeginArgs a{};
+  a.t_host = t_host;
+  a.ids_host = ids;
+  a.n_host = n;
+  a.ids_ring = ids_ring;
+  a.n_ring = n_ring;
+  a.ring_len = ring_len ? ring_len : 1;
+  a.Wp1 = g.Wp1;
+  a.period = (uint32_t)std::max(1, g.opt.update_period);
+  a.L = (uint32_t)g.stage_base0;
+  a.C = (uint32_t)g.C;
+  a.inbox_cnt = g.world == 1 ? g.local_inbox_cnt : nullptr;
+  return a;
+}
+
+// gather kernels; n_bound = host bound of this rank's request count (grid sizing only);
+// stamp_host = t + 1 for the G > 1 flag protocol (direct calls only).
+int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host, bool graph, uint32_t stamp_host,
+                  cudaStream_t st) {
+  const int G = g.world;
+  k_begin<<<1, 32, 0, st>>>(g.it, g.hist, g.scr, ba);
+  LAUNCHED();
+  // ---- S1/S2 route + exchange (P:296-299, P:311-312)
+  prof_begin(0, st);
+  const uint32_t* inbox = inbox_of(g.arena);
+  const uint32_t* inbox_cnt;
+  if (G == 1) {
+    if (n_bound > 0) {
+      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, 0u, g.N, inbox_of(g.arena), 0, g.local_inbox_cnt,
+                                                            g.scr, g.inbox_i);
+      LAUNCHED();
+    }
+    inbox_cnt = g.local_inbox_cnt;
+  } else {
+    if (int rc = exchange_ids(n_bound, false, stamp_host, st)) return rc;
+    inbox_cnt = icnt_of(g.arena);
+  }
+  prof_end(0, st);
+  // ---- S3 dedup + set grouping
+  prof_begin(1, st);
+  const int64_t maxreq = (int64_t)g.cap * G;
+  k_dedup<<<grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st>>>(
+      inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, g.it, g.mark,
+      g.uniq, g.set_cnt, g.scr, g.hist, G == 1 ? g.head : nullptr, g.nxt);
+  LAUNCHED();
+  k_scan<<<1, 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr, (uint32_t)g.C, g.scr,
+                             g.mark, g.it, (uint32_t)G, g.hist);
+  LAUNCHED();
+  k_bucket<<<grid_for(std::max<int64_t>(n_bound, 1) * G, 256, 4), 256, 0, st>>>(g.uniq, g.scr, (uint32_t)G,
+                                                                                 (uint32_t)g.S, g.set_off, g.set_cnt,
+                                                                                 g.bucket);
+  LAUNCHED();
+  prof_end(1, st);
+  // ---- S4/S5 probe + replacement
+  prof_begin(2, st);
+  SetParams sp{};
+  sp.set_off = g.set_off;
+  sp.bucket = g.bucket;
+  sp.tags = g.tags;
+  sp.last_use = g.last_use;
+  sp.rr = g.rr;
+  sp.score = g.score;
+  sp.mask = g.mask;
+  sp.node_loc = loc_of(g.arena);
+  sp.vst_stamp = g.vst_stamp;
+  sp.vst_idx = g.vst_idx;
+  sp.fills = g.fills;
+  sp.cands = g.cands;
+  sp.scr = g.scr;
+  sp.it = g.it;
+  sp.hist = g.hist;
+  sp.S = (uint32_t)g.S;
+  sp.A = g.A;
+  sp.G = (uint32_t)G;
+  sp.W = g.W;
+  sp.T = g.T;
+  sp.MW = g.MW;
+  sp.policy = (uint32_t)g.opt.policy;
+  sp.pvp = (uint32_t)g.opt.pvp;
+  sp.reinsert = (uint32_t)g.opt.reinsert_victims;
+  sp.P = g.P;
+  sp.warp_bytes = g.warp_bytes;
+  sp.bypass_base = (uint32_t)g.bypass_base;
+  sp.deliver = G == 1 ? kDelivered : 0u;
+  sp.period = (uint32_t)std::max(1, g.opt.update_period);
+  sp.line_info = g.line_info;
+  if (sp.period > 1) {  // the periodic window scan; k_snapshot exits when t mod P != 0
+    k_snapshot<<<grid_for((int64_t)g.L, 256, 4), 256, 0, st>>>(g.tags, (uint32_t)g.L, (uint32_t)G, g.mask, g.MW, g.W,
+                                                                g.it, g.line_info);
+    LAUNCHED();
+  }
+  {
+    const int64_t blocks =
+        std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(8, g.geom_per_sm));
+    k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);
+    LAUNCHED();
+  }
+  prof_end(2, st);
+  // ---- S5 victim admission (PVP)
+  if (g.C) {
+    prof_begin(3, st);
+    const int qg = grid_for(g.ucap, 256, 2);
+    k_qhist<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qcnt);
+    LAUNCHED();
+    k_scan<<<1, 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr);
+    LAUNCHED();
+    k_qscatter<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
+    LAUNCHED();
+    k_admit<<<g.W, 256, 0, st>>>(g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint32_t)g.C, g.it,
+                                 g.hist);
+    LAUNCHED();
+    prof_end(3, st);
+  }
+  // ---- S6 fill (victim D2H + storage/staging -> slot) and S7/S8 serve
+  uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
+  const uint4* tab = reinterpret_cast<const uint4*>(g.table_dev);
+  uint4* hq = reinterpret_cast<uint4*>(g.qrows_dev);
+  uint4* o4 = reinterpret_cast<uint4*>(out);
+  const bool wide = g.nvec >= 256;
+  if (G == 1) {
+    // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits
+    prof_begin(4, st);
+    const int blocks = g.sms * std::min(4, g.geom_per_sm);
+#define SERVE(U, O)                                                                                                  \
+  k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.inbox_i, g.it, g.N, \
+                                        loc_of(g.arena), o4)
+    if (wide && !out_host) SERVE(8, kDev);
+    else if (wide) SERVE(8, kHost);
+    else if (!out_host) SERVE(2, kDev);
+    else SERVE(2, kHost);
+#undef SERVE
+    LAUNCHED();
+    prof_end(4, st);
+    prof_begin(5, st);
+  } else {
+    prof_begin(4, st);
+    const int blocks = g.sms * std::min(4, g.geom_per_sm);
+    if (wide)
+      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
+    else
+      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
+    LAUNCHED();
+    prof_end(4, st);
+    // homes signal "served", requesters wait for every home, then pull
+    prof_begin(5, st);
+    for (int r = 0; r < G; ++r)
+      if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[G + g.rank], stamp_host)) return rc;
+    for (int h = 0; h < G; ++h)
+      if (int rc = flag_wait(st, &flags_of(g.arena)[G + h], stamp_host)) return rc;
+    if (n_bound > 0) {
+      PullArgs pa{};
+      for (int h = 0; h < G; ++h) {
+        pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
+        pa.node_loc[h] = loc_of(g.peer_arena[h]);
+      }
+      pa.G = (uint32_t)G;
+      const int pblocks = grid_for(n_bound * 32, 256, 8);
+      if (wide && !out_host) k_pull<8, kDev><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
+      else if (wide) k_pull<8, kHost><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
+      else if (!out_host) k_pull<2, kDev><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
+      else k_pull<2, kHost><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
+      LAUNCHED();
+    }
+  }
+  prof_end(5, st);
+  k_end<<<1, 32, 0, st>>>(g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev, graph ? 1u : 0u);
+  LAUNCHED();
+  return 0;
+}
+
+// Window feed of one batch (G = 1 local path, or the G > 1 exchange). k_host >= 0: host
+// values; k_host < 0: graph replay (batch from the ring).
+int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* n_dev, const int64_t* const* ids_ring,
+                  const int64_t* n_ring, uint32_t ring_len, int64_t n_bound, cudaStream_t st) {
+  const int G = g.world;
+  k_win_begin<<<1, 32, 0, st>>>(g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1);
+  LAUNCHED();
+  const uint64_t stride = g.cap * G;
+  // drop the bits of the iteration that last used this slot (k - (W+1)), then empty the slot
+  k_mask_clear<<<grid_for((int64_t)stride, 256, 2), 256, 0, st>>>(g.ring, stride, g.ring_len, g.it, (uint32_t)G, g.MW,
+                                                                   g.mask);
+  LAUNCHED();
+  if (G == 1) {
+    if (n_bound > 0) {
+      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, 1u, g.N, g.ring, stride, g.ring_len, g.scr, nullptr);
+      LAUNCHED();
+    }
+  } else {
+    const uint32_t seq = ++g.win_seq;
+    if (int rc = exchange_ids(n_bound, true, seq, st)) return rc;
+    k_win_gather<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(win_of(g.arena), wcnt_of(g.arena), (uint32_t)G,
+                                                                    (uint32_t)g.cap, g.ring, stride, g.ring_len, g.it);
+    LAUNCHED();
+    for (int r = 0; r < G; ++r)  // window inbox consumed
+      if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[3 * G + g.rank], seq)) return rc;
+  }
+  k_mask_set<<<grid_for((int64_t)stride, 256, 2), 256, 0, st>>>(g.ring, stride, g.ring_len, g.it, (uint32_t)G, g.MW,
+                                                                 g.mask);
+  LAUNCHED();
+  return 0;
+}
+
+// S11: PVP copy of victim queue (t+1) mod W on the side stream, after gather(t) (R17).
+int launch_pvp(cudaStream_t st) {
+  CK(cudaEventRecord(g.ev_main, st));
+  CK(cudaStreamWaitEvent(g.side, g.ev_main, 0));
+  uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
+  const int blocks = g.sms * std::min(2, g.geom_per_sm);
+  prof_begin(7, g.side);
+  if (g.nvec >= 256)
+    k_pvp<8><<<blocks, 256, 0, g.side>>>(g.it, g.W, (uint32_t)g.stage_base0, (uint32_t)g.C, (uint32_t)g.world, g.qlen,
+                                         g.qnode, g.qreuse, reinterpret_cast<const uint4*>(g.qrows_dev), pool,
+                                         g.stg_nodes, g.vst_stamp, g.vst_idx, g.scr, g.nvec);
+  else
+    k_pvp<2><<<blocks, 256, 0, g.side>>>(g.it, g.W, (uint32_t)g.stage_base0, (uint32_t)g.C, (uint32_t)g.world, g.qlen,
+                                         g.qnode, g.qreuse, reinterpret_cast<const uint4*>(g.qrows_dev), pool,
+                                         g.stg_nodes, g.vst_stamp, g.vst_idx, g.scr, g.nvec);
+  LAUNCHED();
+  prof_end(7, g.side);
+  CK(cudaEventRecord(g.ev_pvp, g.side));
+  g.pvp_pending = true;
+  return 0;
+}
+
+int resolve_out(void*& out, bool& out_host, int64_t n) {
+  out_host = false;
+  if (n <= 0) return 0;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, out) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
+    cudaGetLastError();
+    return set_err(LSMGNN_EINVAL, "out must be device memory or pinned host memory");
+  }
+  if (at.type == cudaMemoryTypeHost) {  // rows are stored over PCIe
+    out_host = true;
+    out = at.devicePointer;
+  }
+  return 0;
 }
 
 }  // namespace
@@ -447,6 +700,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.fills, g.ucap);
   DA(g.cands, g.ucap);
   DA(g.scr, 1);
+  DA(g.it, 1);
   DA(g.hist, (size_t)kHist * F_NFIELDS);
   DA(g.cum, F_NFIELDS);
 #undef DA
@@ -558,185 +812,16 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
   if (n > 0 && (!node_ids || !out)) return set_err(LSMGNN_EINVAL, "null ids/out");
   if (reinterpret_cast<uintptr_t>(out) % 16) return set_err(LSMGNN_EINVAL, "out must be 16-byte aligned");
   if (int rc = check_sticky()) return rc;
-  // `out` may be device memory or pinned (mapped) host memory: rows are then stored over PCIe
   bool out_host = false;
-  if (n > 0) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, out) != cudaSuccess || at.type == cudaMemoryTypeUnregistered) {
-      cudaGetLastError();
-      return set_err(LSMGNN_EINVAL, "out must be device memory or pinned host memory");
-    }
-    if (at.type == cudaMemoryTypeHost) {
-      out_host = true;
-      out = at.devicePointer;
-    }
-  }
+  if (int rc = resolve_out(out, out_host, n)) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int G = g.world;
   const int64_t t = g.t_next;
-  const uint32_t stamp = (uint32_t)(t + 1);
-  unsigned long long* rec = g.hist + (size_t)(t % kHist) * F_NFIELDS;
-
   if (g.pvp_pending) {
     CK(cudaStreamWaitEvent(st, g.ev_pvp, 0));
     g.pvp_pending = false;
   }
-  k_begin<<<1, 32, 0, st>>>(rec, g.scr, (uint64_t)t);
-  LAUNCHED();
-
-  // ---- S1/S2 route + exchange (P:296-299, P:311-312)
-  prof_begin(0, st);
-  const uint32_t* inbox;
-  const uint32_t* inbox_cnt;
-  if (G == 1) {
-    CK(cudaMemsetAsync(g.local_inbox_cnt, 0, sizeof(uint32_t), st));
-    if (n > 0) {
-      k_route_local<<<grid_for(n, 256), 256, 0, st>>>(node_ids, n, g.N, inbox_of(g.arena), g.local_inbox_cnt, g.scr,
-                                                      g.inbox_i);
-      LAUNCHED();
-    }
-    inbox = inbox_of(g.arena);
-    inbox_cnt = g.local_inbox_cnt;
-  } else {
-    if (int rc = exchange_ids(node_ids, n, false, stamp, st)) return rc;
-    inbox = inbox_of(g.arena);
-    inbox_cnt = icnt_of(g.arena);
-  }
-
-  prof_end(0, st);
-  // ---- S3 dedup + set grouping
-  prof_begin(1, st);
-  const int64_t maxreq = (int64_t)g.cap * G;
-  k_dedup<<<grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n, 1) * G), 256, 4), 256, 0, st>>>(
-      inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, stamp, g.mark,
-      g.uniq, g.set_cnt, g.scr, rec, G == 1 ? g.head : nullptr, g.nxt);
-  LAUNCHED();
-  const uint32_t par = (uint32_t)(t & 1);
-  k_scan<<<1, 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes + par * g.C : nullptr,
-                             &g.scr->staged[par], g.mark, stamp, (uint32_t)G, rec);
-  LAUNCHED();
-  k_bucket<<<grid_for(std::max<int64_t>(n, 1) * G, 256, 4), 256, 0, st>>>(g.uniq, g.scr, (uint32_t)G, (uint32_t)g.S,
-                                                                           g.set_off, g.set_cnt, g.bucket);
-  LAUNCHED();
-
-  prof_end(1, st);
-  // ---- S4/S5 probe + replacement
-  prof_begin(2, st);
-  SetParams sp{};
-  sp.set_off = g.set_off;
-  sp.bucket = g.bucket;
-  sp.tags = g.tags;
-  sp.last_use = g.last_use;
-  sp.rr = g.rr;
-  sp.score = g.score;
-  sp.mask = g.mask;
-  sp.node_loc = loc_of(g.arena);
-  sp.vst_stamp = g.vst_stamp;
-  sp.vst_idx = g.vst_idx;
-  sp.fills = g.fills;
-  sp.cands = g.cands;
-  sp.scr = g.scr;
-  sp.rec = rec;
-  sp.S = (uint32_t)g.S;
-  sp.A = g.A;
-  sp.G = (uint32_t)G;
-  sp.W = g.W;
-  sp.T = g.T;
-  sp.MW = g.MW;
-  sp.policy = (uint32_t)g.opt.policy;
-  sp.pvp = (uint32_t)g.opt.pvp;
-  sp.reinsert = (uint32_t)g.opt.reinsert_victims;
-  sp.t = (uint32_t)t;
-  sp.stamp = stamp;
-  sp.p0 = (uint32_t)((t + 1) % g.Wp1);
-  sp.P = g.P;
-  sp.warp_bytes = g.warp_bytes;
-  sp.stage_base = (uint32_t)(g.stage_base0 + par * g.C);
-  sp.bypass_base = (uint32_t)g.bypass_base;
-  sp.deliver = G == 1 ? kDelivered : 0u;
-  sp.period = (uint32_t)std::max(1, g.opt.update_period);
-  sp.line_info = g.line_info;
-  if (sp.period > 1 && t % sp.period == 0) {  // the periodic window scan
-    k_snapshot<<<grid_for((int64_t)g.L, 256, 4), 256, 0, st>>>(g.tags, (uint32_t)g.L, (uint32_t)G, g.mask, g.MW,
-                                                                sp.p0, g.W, (uint32_t)t, g.line_info);
-    LAUNCHED();
-  }
-  {
-    const int64_t blocks =
-        std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(8, g.geom_per_sm));
-    k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);
-    LAUNCHED();
-  }
-  prof_end(2, st);
-  // ---- S5 victim admission (PVP)
-  if (g.C) {
-    prof_begin(3, st);
-    const int qg = grid_for(g.ucap, 256, 2);
-    k_qhist<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qcnt);
-    LAUNCHED();
-    k_scan<<<1, 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, nullptr, nullptr, 0, 1, nullptr);
-    LAUNCHED();
-    k_qscatter<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
-    LAUNCHED();
-    k_admit<<<g.W, 256, 0, st>>>(g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint32_t)g.C, rec);
-    LAUNCHED();
-    prof_end(3, st);
-  }
-  // ---- S6 fill (victim D2H + storage/staging -> slot) and S7/S8 serve
-  uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
-  const uint4* tab = reinterpret_cast<const uint4*>(g.table_dev);
-  uint4* hq = reinterpret_cast<uint4*>(g.qrows_dev);
-  uint4* o4 = reinterpret_cast<uint4*>(out);
-  const bool wide = g.nvec >= 256;
-  if (G == 1) {
-    // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits
-    prof_begin(4, st);
-    const int blocks = g.sms * std::min(4, g.geom_per_sm);
-#define SERVE(U, O)                                                                                              \
-  k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.inbox_i, stamp, \
-                                        node_ids, n, g.N, loc_of(g.arena), o4)
-    if (wide && !out_host) SERVE(8, kDev);
-    else if (wide) SERVE(8, kHost);
-    else if (!out_host) SERVE(2, kDev);
-    else SERVE(2, kHost);
-#undef SERVE
-    LAUNCHED();
-    prof_end(4, st);
-    prof_begin(5, st);
-  } else {
-    prof_begin(4, st);
-    const int blocks = g.sms * std::min(4, g.geom_per_sm);
-    if (wide)
-      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
-    else
-      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
-    LAUNCHED();
-    prof_end(4, st);
-    // homes signal "served", requesters wait for every home, then pull
-    prof_begin(5, st);
-    for (int r = 0; r < G; ++r)
-      if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[G + g.rank], stamp)) return rc;
-    for (int h = 0; h < G; ++h)
-      if (int rc = flag_wait(st, &flags_of(g.arena)[G + h], stamp)) return rc;
-    if (n > 0) {
-      PullArgs pa{};
-      for (int h = 0; h < G; ++h) {
-        pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
-        pa.node_loc[h] = loc_of(g.peer_arena[h]);
-      }
-      pa.G = (uint32_t)G;
-      const int pblocks = grid_for(n * 32, 256, 8);
-      if (wide && !out_host) k_pull<8, kDev><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
-      else if (wide) k_pull<8, kHost><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
-      else if (!out_host) k_pull<2, kDev><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
-      else k_pull<2, kHost><<<pblocks, 256, 0, st>>>(node_ids, n, g.N, pa, o4, g.nvec);
-      LAUNCHED();
-    }
-  }
-  prof_end(5, st);
-  k_end<<<1, 32, 0, st>>>(rec, g.cum, g.scr, (uint64_t)t, g.R);
-  LAUNCHED();
-  CK(cudaMemcpyAsync(g.bad_dev, &g.scr->bad_ids, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  const BeginArgs ba = begin_args(t, node_ids, n, nullptr, nullptr, 0);
+  if (int rc = launch_gather(ba, n, out, out_host, false, (uint32_t)(t + 1), st)) return rc;
   g.t_next = t + 1;
   g.last_stream = st;
   return 0;
@@ -751,66 +836,20 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
                    (long long)g.feed_next);
   if (int rc = check_sticky()) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int G = g.world;
   if (num_batches > 0) prof_begin(6, st);
   for (int32_t b = 0; b < num_batches; ++b) {
     const int64_t k = first_iter + b;
     const int64_t n = offsets[b + 1] - offsets[b];
     if (n < 0 || (uint64_t)n > g.cap) return set_err(LSMGNN_EINVAL, "window batch of %lld ids", (long long)n);
     if (k > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
-    const uint32_t slot = (uint32_t)(k % g.Wp1);
-    uint32_t* ring_slot = g.ring + (size_t)slot * g.cap * G;
-    // drop the bits of the iteration that last used this slot (k - (W+1))
-    k_mask_clear<<<grid_for((int64_t)g.cap * G, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, (uint32_t)G,
-                                                                        g.MW, slot, g.mask);
-    LAUNCHED();
-    if (G == 1) {
-      CK(cudaMemsetAsync(g.ring_len + slot, 0, sizeof(uint32_t), st));
-      if (n > 0) {
-        k_route_local<<<grid_for(n, 256), 256, 0, st>>>(ids + offsets[b], n, g.N, ring_slot, g.ring_len + slot, g.scr,
-                                                        nullptr);
-        LAUNCHED();
-      }
-    } else {
-      const uint32_t seq = ++g.win_seq;
-      if (int rc = exchange_ids(n > 0 ? ids + offsets[b] : nullptr, n, true, seq, st)) return rc;
-      k_win_gather<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(win_of(g.arena), wcnt_of(g.arena), (uint32_t)G,
-                                                                      (uint32_t)g.cap, ring_slot, g.ring_len + slot);
-      LAUNCHED();
-      for (int r = 0; r < G; ++r)  // window inbox consumed
-        if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[3 * G + g.rank], seq)) return rc;
-    }
-    k_mask_set<<<grid_for((int64_t)g.cap * G, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, (uint32_t)G, g.MW,
-                                                                      slot, g.mask);
-    LAUNCHED();
+    if (int rc = launch_window(k, n > 0 ? ids + offsets[b] : nullptr, n, nullptr, nullptr, nullptr, 0, n, st))
+      return rc;
     g.feed_next = k + 1;
   }
   if (num_batches > 0) prof_end(6, st);
   // ---- S11 PVP copy for iteration t+1 on the side stream (after gather(t))
-  if (g.C && g.t_next > 0 && !g.pvp_pending) {
-    const int64_t t1 = g.t_next;  // = t + 1
-    const uint32_t par = (uint32_t)(t1 & 1);
-    CK(cudaEventRecord(g.ev_main, st));
-    CK(cudaStreamWaitEvent(g.side, g.ev_main, 0));
-    const uint32_t kq = (uint32_t)(t1 % g.W);
-    uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
-    const int blocks = g.sms * std::min(2, g.geom_per_sm);
-    prof_begin(7, g.side);
-    if (g.nvec >= 256)
-      k_pvp<8><<<blocks, 256, 0, g.side>>>(kq, (uint32_t)t1, (uint32_t)(t1 + 1), (uint32_t)g.C, (uint32_t)G, g.qlen,
-                                           g.qnode, g.qreuse, reinterpret_cast<const uint4*>(g.qrows_dev), pool,
-                                           (uint32_t)(g.stage_base0 + par * g.C), g.stg_nodes + par * g.C,
-                                           g.vst_stamp, g.vst_idx, g.scr, par, g.nvec);
-    else
-      k_pvp<2><<<blocks, 256, 0, g.side>>>(kq, (uint32_t)t1, (uint32_t)(t1 + 1), (uint32_t)g.C, (uint32_t)G, g.qlen,
-                                           g.qnode, g.qreuse, reinterpret_cast<const uint4*>(g.qrows_dev), pool,
-                                           (uint32_t)(g.stage_base0 + par * g.C), g.stg_nodes + par * g.C,
-                                           g.vst_stamp, g.vst_idx, g.scr, par, g.nvec);
-    LAUNCHED();
-    prof_end(7, g.side);
-    CK(cudaEventRecord(g.ev_pvp, g.side));
-    g.pvp_pending = true;
-  }
+  if (g.C && g.t_next > 0 && !g.pvp_pending)
+    if (int rc = launch_pvp(st)) return rc;
   g.last_stream = st;
   return 0;
 }
@@ -991,23 +1030,80 @@ int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, i
 int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t first_iter, void* stream) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
   if (g.world != 1) return set_err(LSMGNN_EINVAL, "prefetch_dev is single-home only");
+  if (!count_dev) return set_err(LSMGNN_EINVAL, "null count");
   if (first_iter != g.feed_next) return set_err(LSMGNN_ESTATE, "window iteration out of order");
   if (first_iter > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const uint32_t slot = (uint32_t)(first_iter % g.Wp1);
-  uint32_t* ring_slot = g.ring + (size_t)slot * g.cap;
   prof_begin(6, st);
-  k_mask_clear<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, 1, g.MW, slot, g.mask);
-  LAUNCHED();
-  CK(cudaMemsetAsync(g.ring_len + slot, 0, sizeof(uint32_t), st));
-  k_route_local_dev<<<grid_for((int64_t)g.cap, 256), 256, 0, st>>>(ids, count_dev, (int64_t)g.cap, g.N, ring_slot,
-                                                                   g.ring_len + slot, g.scr);
-  LAUNCHED();
-  k_mask_set<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(ring_slot, g.ring_len + slot, 1, g.MW, slot, g.mask);
-  LAUNCHED();
+  if (int rc = launch_window(first_iter, ids, 0, count_dev, nullptr, nullptr, 0, (int64_t)g.cap, st)) return rc;
   prof_end(6, st);
   g.feed_next = first_iter + 1;
   // the PVP copy for t+1 is issued by lsmgnn_prefetch; call it with num_batches = 0 when needed
+  g.last_stream = st;
+  return 0;
+}
+
+// ------------------------------------------------------------------ CUDA-graph step (G = 1)
+int lsmgnn_graph_capture(const int64_t* const* ids_ring, const int64_t* n_ring, int32_t ring_len, void* out,
+                         void* stream) {
+  if (!g.inited || !g.table_dev) return set_err(LSMGNN_ESTATE, "graph_capture before init/attach_storage");
+  if (g.world != 1) return set_err(LSMGNN_EINVAL, "graph mode is single-home (G = 1) only");
+  if (!ids_ring || !n_ring || !out || ring_len < (int32_t)g.W + 2)
+    return set_err(LSMGNN_EINVAL, "graph_capture needs a ring of >= W+2 batches and an out buffer");
+  if (g.feed_next != g.t_next + (int64_t)g.W + 1)
+    return set_err(LSMGNN_ESTATE, "feed the window through t+W before capturing");
+  if (int rc = check_sticky()) return rc;
+  bool out_host = false;
+  if (int rc = resolve_out(out, out_host, 1)) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaStreamSynchronize(st));
+  if (g.graph_exec) {
+    cudaGraphExecDestroy(g.graph_exec);
+    g.graph_exec = nullptr;
+  }
+  if (g.graph) {
+    cudaGraphDestroy(g.graph);
+    g.graph = nullptr;
+  }
+  if (!g.cap_stream) CK(cudaStreamCreateWithFlags(&g.cap_stream, cudaStreamNonBlocking));
+  const bool prof = g.prof;
+  g.prof = false;  // no host-side event spans inside a graph
+  const int64_t l0 = g.launches;
+  CK(cudaStreamBeginCapture(g.cap_stream, cudaStreamCaptureModeThreadLocal));
+  const BeginArgs ba = begin_args(-1, nullptr, 0, ids_ring, n_ring, (uint32_t)ring_len);
+  int rc = launch_gather(ba, (int64_t)g.cap, out, out_host, true, 0, g.cap_stream);
+  if (!rc) rc = launch_window(-1, nullptr, 0, nullptr, ids_ring, n_ring, (uint32_t)ring_len, (int64_t)g.cap, g.cap_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(g.cap_stream, &graph);
+  g.prof = prof;
+  g.graph_launches = g.launches - l0;
+  g.launches = l0;
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return set_err(LSMGNN_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+  g.graph = graph;
+  CK(cudaGraphInstantiate(&g.graph_exec, g.graph, 0));
+  g.graph_out_host = out_host;
+  return 0;
+}
+
+int lsmgnn_graph_replay(void* stream) {
+  if (!g.graph_exec) return set_err(LSMGNN_ESTATE, "no captured graph");
+  if (g.feed_next != g.t_next + (int64_t)g.W + 1) return set_err(LSMGNN_ESTATE, "window/iteration out of step");
+  if (int rc = check_sticky()) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (g.pvp_pending) {
+    CK(cudaStreamWaitEvent(st, g.ev_pvp, 0));
+    g.pvp_pending = false;
+  }
+  CK(cudaGraphLaunch(g.graph_exec, st));
+  g.launches += g.graph_launches;
+  g.t_next += 1;
+  g.feed_next += 1;
+  if (g.C)
+    if (int rc = launch_pvp(st)) return rc;
   g.last_stream = st;
   return 0;
 }

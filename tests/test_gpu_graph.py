@@ -1,0 +1,43 @@
+"""CUDA-graph step (-m gpu): one captured launch per iteration (gather + window feed, all
+per-iteration values on the device) gives exactly the oracle's counters and F(v) rows, also
+when mixed with direct gather/prefetch calls and with the PVP / periodic update on."""
+import numpy as np
+import pytest
+
+import synth
+
+from .harness import run_oracle, small_workload, table_for
+from .test_gpu_parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("policy,pvp,P", [("hybrid", 0, 1), ("hybrid", 1, 1), ("lru", 1, 2), ("dynamic", 0, 3)])
+def test_graph_replay_parity(policy, pvp, P):
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    N, D, W = 16384, 128, 8
+    g, tr, sc = small_workload(N, 8, G=1, batch=256, fanout=(10, 5), iters=20)
+    K = len(tr)
+    kw = dict(N=N, D=D, L=1024, A=8, scores=sc, policy=policy, pvp=pvp, W=W, V=512, P=P)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    mb = max(len(x[0]) for x in tr)
+    c = LsmGnn(N, D, 1024, 8, 512, sc, policy=policy, pvp=pvp, window=W, max_batch_ids=mb, period=P)
+    c.attach_storage(table_for(N, D, pinned=True))
+    ring = [torch.from_numpy(np.asarray(tr[k][0], np.int64)).cuda() if k < K else
+            torch.zeros(0, dtype=torch.int64, device="cuda") for k in range(K + W + 1)]
+    out = torch.empty((mb, 4 * D), dtype=torch.uint8, device="cuda")
+    c.prefetch(ring[1:W + 1], first_iter=1)
+    # two direct steps, then capture and replay the rest (the styles mix)
+    for t in range(2):
+        c.gather(ring[t], out)
+        c.prefetch([ring[t + 1 + W]], first_iter=t + 1 + W)
+    c.graph_capture(ring, out)
+    for t in range(2, K):
+        c.graph_replay()
+        n = ring[t].numel()
+        rows = out[:n].cpu().numpy().view(np.uint32).reshape(n, D)
+        assert synth.check_rows(rows, tr[t][0], D)[0] == 0, t
+    torch.cuda.synchronize()
+    compare(c.history(0, K), ho, f"graph {policy}/pvp{pvp}/P{P}")
+    c.close()
