@@ -1,0 +1,41 @@
+"""Randomised parity (-m gpu): many small random configurations — ways, sets, window,
+threshold, policy, PVP, victim capacity, re-insertion, update period, row size, batch
+shapes with duplicates and empty batches — each compared with the oracle counter by counter
+and row by row. A net for corner cases the structured tests do not enumerate."""
+import numpy as np
+import pytest
+
+from .harness import run_gpu, run_oracle
+from .test_gpu_parity import compare
+
+pytestmark = pytest.mark.gpu
+
+POLICIES = ["hybrid", "static", "lru", "rr", "dynamic"]
+
+
+def random_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    A = int(rng.choice([1, 2, 3, 4, 7, 8, 16, 32]))
+    S = int(rng.integers(1, 40))
+    N = int(rng.integers(max(2, A * S // 2), A * S * 6 + 50))
+    W = int(rng.integers(1, 12))
+    cfg = dict(N=N, D=int(rng.choice([4, 8, 32])), L=A * S, A=A, policy=str(rng.choice(POLICIES)),
+               pvp=int(rng.integers(0, 2)), W=W, T=int(rng.integers(0, W + 1)), V=int(rng.integers(W, 8 * W)),
+               reinsert=int(rng.integers(0, 2)), P=int(rng.choice([1, 1, 2, 3])))
+    K = int(rng.integers(5, 30))
+    tr = []
+    for _ in range(K):
+        n = int(rng.integers(0, 3 * A * S + 5)) if rng.random() > 0.1 else 0
+        x = rng.zipf(1.3, n) % N if rng.random() < 0.5 else rng.integers(0, N, n)
+        tr.append([np.asarray(x, np.int64)])
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    return cfg, tr, sc
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_parity(seed):
+    cfg, tr, sc = random_case(seed)
+    hg, _, bad = run_gpu(tr, scores=sc, max_batch_ids=max(1, max(len(x[0]) for x in tr)), **cfg)
+    ho = run_oracle(tr, G=1, scores=sc, **cfg)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"fuzz {seed}: {cfg}")
