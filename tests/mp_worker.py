@@ -40,6 +40,20 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         return
+    if mode == "fuzz":  # many random small cases in one launch (the library re-initialises per case)
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+        from tests.harness import run_gpu
+        from tests.test_gpu_multiproc import random_mp_case
+        ncases = int(sys.argv[3])
+        for case in range(ncases):
+            cfg, tr, sc = random_mp_case(case, world)
+            hist, _, bad = run_gpu(tr, scores=sc, rank=rank, world=world, group=dist.group.WORLD,
+                                   max_batch_ids=max(1, max(len(x) for row in tr for x in row)), **cfg)
+            np.save(os.path.join(outdir, f"fz{case}_h{rank}.npy"), hist)
+            assert bad == 0, (case, rank)
+            dist.barrier()
+        dist.destroy_process_group()
+        return
     if mode == "edge":  # ragged / empty / duplicate-heavy batches across ranks, tiny victim queues
         torch.cuda.set_device(rank % torch.cuda.device_count())
         from tests.harness import run_gpu

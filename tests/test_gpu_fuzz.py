@@ -2,6 +2,8 @@
 threshold, policy, PVP, victim capacity, re-insertion, update period, row size, batch
 shapes with duplicates and empty batches — each compared with the oracle counter by counter
 and row by row. A net for corner cases the structured tests do not enumerate."""
+import os
+
 import numpy as np
 import pytest
 
@@ -32,7 +34,7 @@ def random_case(seed):
     return cfg, tr, sc
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("LSMGNN_FUZZ", "40"))))
 def test_fuzz_parity(seed):
     cfg, tr, sc = random_case(seed)
     hg, _, bad = run_gpu(tr, scores=sc, max_batch_ids=max(1, max(len(x[0]) for x in tr)), **cfg)

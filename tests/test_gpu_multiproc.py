@@ -35,6 +35,37 @@ def launch(G, tmp, *args, timeout=600):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
 
 
+def random_mp_case(seed, G):
+    """A random small G-home case (same for every rank: derived from the seed only)."""
+    rng = np.random.default_rng(5000 + 37 * seed + G)
+    A = int(rng.choice([1, 2, 4, 8, 32]))
+    S = int(rng.integers(1, 20))
+    N = int(rng.integers(G * A * S // 2 + G, G * A * S * 5 + 50))
+    W = int(rng.integers(1, 10))
+    cfg = dict(N=N, D=int(rng.choice([4, 16])), L=A * S, A=A,
+               policy=str(rng.choice(["hybrid", "static", "lru", "rr", "dynamic"])), pvp=int(rng.integers(0, 2)),
+               W=W, T=int(rng.integers(0, W + 1)), V=int(rng.integers(W, 6 * W)), reinsert=int(rng.integers(0, 2)),
+               P=int(rng.choice([1, 1, 2])))
+    K = int(rng.integers(4, 16))
+    tr = [[np.asarray(rng.integers(0, N, int(rng.integers(0, 2 * A * S * G + 3))) if rng.random() > 0.15
+                      else np.zeros(0, np.int64), np.int64) for _ in range(G)] for _ in range(K)]
+    return cfg, tr, rng.integers(0, 256, N).astype(np.uint8)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_multiprocess_fuzz(tmp_path, G):
+    """Random small G-home cases (one process launch runs them all): every home's counters
+    equal the oracle's."""
+    n = int(os.environ.get("LSMGNN_MP_FUZZ", "12"))
+    launch(G, tmp_path, "fuzz", str(tmp_path), str(n), timeout=1200)
+    for case in range(n):
+        cfg, tr, sc = random_mp_case(case, G)
+        ho = run_oracle(tr, G=G, scores=sc, **cfg)
+        for r in range(G):
+            hg = np.load(tmp_path / f"fz{case}_h{r}.npy")
+            assert np.array_equal(hg, ho[:, r, :]), (case, r, cfg, np.argwhere(hg != ho[:, r, :])[:3])
+
+
 @pytest.mark.parametrize("G,case", [(2, "ragged"), (3, "dups"), (2, "period"), (4, "rr")])
 def test_multiprocess_edge_cases(tmp_path, G, case):
     """Ranks with empty batches, cross-rank duplicates, raw lists, victim-queue overflow,
