@@ -897,9 +897,13 @@ int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count)
   if (count < 0 || first < 0 || first + count > g.t_next || (g.t_next - first) > kHist)
     return set_err(LSMGNN_EINVAL, "history range [%lld,+%lld) unavailable", (long long)first, (long long)count);
   CK(cudaDeviceSynchronize());
-  for (int64_t i = 0; i < count; ++i)
-    CK(cudaMemcpy(out_host + i, g.hist + (size_t)((first + i) % kHist) * F_NFIELDS, sizeof(lsmgnn_stats_t),
-                  cudaMemcpyDeviceToHost));
+  // the ring [first, first+count) is at most two contiguous pieces
+  for (int64_t i = 0; i < count;) {
+    const int64_t slot = (first + i) % kHist;
+    const int64_t run = std::min<int64_t>(count - i, (int64_t)kHist - slot);
+    CK(cudaMemcpy(out_host + i, g.hist + (size_t)slot * F_NFIELDS, run * sizeof(lsmgnn_stats_t), cudaMemcpyDeviceToHost));
+    i += run;
+  }
   return check_sticky();
 }
 
