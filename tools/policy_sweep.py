@@ -84,6 +84,7 @@ def main():
     ap.add_argument("--gpus", default="2,4,8")
     ap.add_argument("--sizes", default="1,2,5,10,20")
     ap.add_argument("--policies", default="hybrid,static,lru,rr,dynamic")
+    ap.add_argument("--private", action="store_true", help="add M-GIDS rows: independent per-GPU caches")
     ap.add_argument("--scores", default="degree", choices=["degree", "rpr"],
                     help="static information: degree, or reverse PageRank (the paper's choice, P:645)")
     args = ap.parse_args()
@@ -125,6 +126,20 @@ def main():
                 r.update({"G": G, "cache_pct": pct, "lines_per_gpu": lines_total // G, "policy": pol, "pvp": pvp})
                 results["points"].append(r)
                 print(json.dumps(r), flush=True)
+            # M-GIDS baseline: G independent PRIVATE caches of L lines each, every
+            # GPU caching its own requests (no communication layer) — RR as in the paper, and hybrid
+            if args.private:
+                for pol in ("rr", "hybrid"):
+                    tot = None
+                    for rk in range(G):
+                        mine = [row[rk] for row in tr]
+                        pr = run_point(mine, N, lines_total // G, ways, scores, pol, 0, W, 0, ipe)
+                        tot = pr if tot is None else {k: tot[k] + pr[k] for k in tot if k != "hit_ratio"}
+                    tot["hit_ratio"] = round((tot["hits"] + tot["victim_hits"]) / max(tot["unique"], 1), 4)
+                    tot.update({"G": G, "cache_pct": pct, "lines_per_gpu": lines_total // G, "policy": "private_" + pol,
+                                "pvp": 0})
+                    results["points"].append(tot)
+                    print(json.dumps(tot), flush=True)
         json.dump(results, open(args.out, "w"), indent=1)
     json.dump(results, open(args.out, "w"), indent=1)
 
