@@ -232,44 +232,69 @@ __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __re
   }
 }
 
-// Exclusive scan of set_cnt[0..S) into set_off[0..S] by one CTA (1024 threads).
-// The same CTA counts staged PVP rows that this batch did not request (pvp_unused).
-// stg_base (null when there is no PVP): the two staging node lists, C entries each.
-__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off,
-                                               uint32_t n, const uint32_t* __restrict__ stg_base, uint32_t C,
-                                               const Scratch* scr, const uint32_t* __restrict__ mark,
-                                               const IterState* it, uint32_t G, unsigned long long* hist) {
-  __shared__ uint32_t s_warp[32];
+// Exclusive prefix of one value per thread over a 1024-thread CTA.
+__device__ __forceinline__ uint32_t block_exclusive_1024(uint32_t v, uint32_t* s_warp) {
   const uint32_t tid = threadIdx.x;
-  const uint32_t per = (n + 1023) / 1024;
-  const uint32_t lo = tid * per, hi = min(n, lo + per);
-  uint32_t sum = 0;
-  for (uint32_t i = lo; i < hi; ++i) sum += cnt[i];
-  // block exclusive scan of `sum`
-  uint32_t x = sum;
+  uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if ((tid & 31) >= (uint32_t)o) x += y;
   }
+  __syncthreads();
   if ((tid & 31) == 31) s_warp[tid >> 5] = x;
   __syncthreads();
   if (tid < 32) {
     uint32_t w = s_warp[tid];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (tid >= (uint32_t)o) w += y;
     }
     s_warp[tid] = w;
   }
   __syncthreads();
-  uint32_t run = x - sum + ((tid >> 5) ? s_warp[(tid >> 5) - 1] : 0);
+  return x - v + ((tid >> 5) ? s_warp[(tid >> 5) - 1] : 0u);
+}
+__device__ __forceinline__ uint32_t pow2_at_least_32(uint32_t m) {
+  uint32_t p = 32;
+  while (p < m) p <<= 1;
+  return p;
+}
+
+// Exclusive scan of set_cnt[0..S) into set_off[0..S] by one CTA (1024 threads). With poff,
+// also the offsets of the global scratch of the sets too large for k_set's shared memory
+// (bucket > big_P): each gets a power-of-two region. The same CTA counts staged PVP rows
+// that this batch did not request (pvp_unused).
+__global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off,
+                                               uint32_t n, const uint32_t* __restrict__ stg_base, uint32_t C,
+                                               const Scratch* scr, const uint32_t* __restrict__ mark,
+                                               const IterState* it, uint32_t G, unsigned long long* hist,
+                                               uint32_t* __restrict__ poff, uint32_t big_P) {
+  __shared__ uint32_t s_warp[32];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t per = (n + 1023) / 1024;
+  const uint32_t lo = tid * per, hi = min(n, lo + per);
+  uint32_t sum = 0, psum = 0;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const uint32_t m = cnt[i];
+    sum += m;
+    if (m > big_P) psum += pow2_at_least_32(m);
+  }
+  uint32_t run = block_exclusive_1024(sum, s_warp);
   for (uint32_t i = lo; i < hi; ++i) {
     off[i] = run;
     run += cnt[i];
   }
   if (tid == 1023) off[n] = run;
+  if (poff) {
+    uint32_t prun = block_exclusive_1024(psum, s_warp);
+    for (uint32_t i = lo; i < hi; ++i) {
+      const uint32_t m = cnt[i];
+      poff[i] = prun;
+      if (m > big_P) prun += pow2_at_least_32(m);
+    }
+  }
   // pvp_unused: staged rows whose node this batch did not request
   if (stg_base) {
     const uint32_t par = it->par, stamp = it->stamp;
@@ -334,7 +359,10 @@ struct SetParams {
   unsigned long long* hist;
   uint32_t S, A, G, W, T, MW;
   uint32_t policy, pvp, reinsert;
-  uint32_t P;            // per-warp capacity (power of two >= max bucket)
+  uint32_t P;            // per-warp shared capacity (power of two); larger buckets use g_* scratch
+  const uint32_t* poff;  // global scratch offset of each oversized set (k_scan)
+  uint32_t *g_sv, *g_sk, *g_sidx;
+  unsigned long long* g_skey;
   uint32_t period;       // dynamic-information update period; 1 = exact every batch
   uint32_t* line_info;   // period > 1: per-line snapshot (reuse iteration / kInfoNone / kInfoFresh)
   uint32_t warp_bytes;   // per-warp shared memory
@@ -393,11 +421,11 @@ __global__ void k_set(SetParams p) {
   __syncthreads();
 
   unsigned char* wbase = smem + (size_t)wib * p.warp_bytes;
-  uint32_t* sv = reinterpret_cast<uint32_t*>(wbase);  // sorted nodes of the set
-  uint32_t* sk = sv + p.P;                           // per node: kind | way<<2 | inM<<10 | byp<<11
-  uint32_t* sidx = sk + p.P;                         // M list, then insert list (indices into sv)
-  unsigned long long* skey = reinterpret_cast<unsigned long long*>(sidx + p.P);
-  uint32_t* stag = reinterpret_cast<uint32_t*>(skey + p.P);
+  uint32_t* sv_s = reinterpret_cast<uint32_t*>(wbase);  // sorted nodes of the set
+  uint32_t* sk_s = sv_s + p.P;                         // per node: kind | way<<2 | inM<<10 | byp<<11
+  uint32_t* sidx_s = sk_s + p.P;                       // M list, then insert list (indices into sv)
+  unsigned long long* skey_s = reinterpret_cast<unsigned long long*>(sidx_s + p.P);
+  uint32_t* stag = reinterpret_cast<uint32_t*>(skey_s + p.P);
   uint32_t* svict = stag + 32;
   int* sd = reinterpret_cast<int*>(svict + 32);
   int* scls = sd + 32;
@@ -417,6 +445,19 @@ __global__ void k_set(SetParams p) {
     if (m == 0) continue;
     uint32_t Pm = 32;
     while (Pm < m) Pm <<= 1;
+    // a bucket larger than the warp's shared-memory capacity works in its own power-of-two
+    // region of global scratch (rare: only when one set receives > P distinct nodes)
+    uint32_t* sv = sv_s;
+    uint32_t* sk = sk_s;
+    uint32_t* sidx = sidx_s;
+    unsigned long long* skey = skey_s;
+    if (m > p.P) {
+      const uint32_t po = p.poff[s];
+      sv = p.g_sv + po;
+      sk = p.g_sk + po;
+      sidx = p.g_sidx + po;
+      skey = p.g_skey + po;
+    }
     for (uint32_t j = lane; j < Pm; j += 32) sv[j] = j < m ? p.bucket[off + j] : kInvalid;
     // resident lines of the set: lane w holds way w
     uint32_t tg = kInvalid, lu = 0;

@@ -62,6 +62,9 @@ struct Ctx {
   uint32_t *tags = nullptr, *last_use = nullptr, *rr = nullptr, *mask = nullptr, *mark = nullptr;
   uint32_t *vst_stamp = nullptr, *vst_idx = nullptr, *set_cnt = nullptr, *set_off = nullptr;
   uint32_t *bucket = nullptr, *uniq = nullptr, *ring = nullptr, *ring_len = nullptr;
+  // global scratch for cache sets whose bucket exceeds k_set's shared-memory capacity
+  uint32_t *poff = nullptr, *g_sv = nullptr, *g_sk = nullptr, *g_sidx = nullptr;
+  unsigned long long* g_skey = nullptr;
   uint32_t *qcnt = nullptr, *qoff = nullptr, *qb = nullptr, *qlen = nullptr, *qnode = nullptr;
   uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr, *local_inbox_cnt = nullptr;
   unsigned long long* head = nullptr;            // G = 1 fused delivery: per-node request list heads
@@ -268,7 +271,7 @@ int free_all() {
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off,
                   g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
                   g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.head, g.nxt, g.inbox_i, g.line_info, g.score, g.fills, g.cands,
-                  g.scr, g.it, g.hist,
+                  g.scr, g.it, g.hist, g.poff, g.g_sv, g.g_sk, g.g_sidx, g.g_skey,
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -368,7 +371,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       g.uniq, g.set_cnt, g.scr, g.hist, G == 1 ? g.head : nullptr, g.nxt);
   LAUNCHED();
   k_scan<<<1, 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr, (uint32_t)g.C, g.scr,
-                             g.mark, g.it, (uint32_t)G, g.hist);
+                             g.mark, g.it, (uint32_t)G, g.hist, g.poff, g.P);
   LAUNCHED();
   k_bucket<<<grid_for(std::max<int64_t>(n_bound, 1) * G, 256, 4), 256, 0, st>>>(g.uniq, g.scr, (uint32_t)G,
                                                                                  (uint32_t)g.S, g.set_off, g.set_cnt,
@@ -403,6 +406,11 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   sp.pvp = (uint32_t)g.opt.pvp;
   sp.reinsert = (uint32_t)g.opt.reinsert_victims;
   sp.P = g.P;
+  sp.poff = g.poff;
+  sp.g_sv = g.g_sv;
+  sp.g_sk = g.g_sk;
+  sp.g_sidx = g.g_sidx;
+  sp.g_skey = g.g_skey;
   sp.warp_bytes = g.warp_bytes;
   sp.bypass_base = (uint32_t)g.bypass_base;
   sp.deliver = G == 1 ? kDelivered : 0u;
@@ -426,7 +434,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     const int qg = grid_for(g.ucap, 256, 2);
     k_qhist<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qcnt);
     LAUNCHED();
-    k_scan<<<1, 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr);
+    k_scan<<<1, 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr, nullptr, 0);
     LAUNCHED();
     k_qscatter<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
     LAUNCHED();
@@ -634,7 +642,8 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   // k_set per-warp shared memory: the largest possible bucket of one set
   const uint64_t maxm = std::min<uint64_t>((g.Q + g.S - 1) / g.S, g.ucap);
   g.P = 32;
-  while (g.P < maxm) g.P <<= 1;
+  while (g.P < maxm && g.P < 1024) g.P <<= 1;  // larger buckets fall back to global scratch
+  const bool big_sets = maxm > g.P;
   g.warp_bytes = (uint32_t)align_up(20ull * g.P + 4 * 32 * 4, 16);
   g.set_warps = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(8, (160 * 1024) / g.warp_bytes));
   if (const char* geo = getenv("LSMGNN_GEOMETRY")) {  // launch-geometry override: results must not change
@@ -643,9 +652,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
       g.geom_per_sm = 1;
     }
   }
-  if ((uint64_t)g.warp_bytes * g.set_warps > 200 * 1024)
-    return set_err(LSMGNN_EINVAL, "a cache set can receive %llu distinct nodes per batch; use more sets",
-                   (unsigned long long)maxm);
+
 
   // ---- shared arena
   size_t o = 0;
@@ -674,6 +681,13 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.vst_idx, g.Q);
   DA(g.set_cnt, g.S);
   DA(g.set_off, g.S + 1);
+  if (big_sets) {  // power-of-two regions per oversized set: at most 2x the unique count
+    DA(g.poff, g.S);
+    DA(g.g_sv, 2 * g.ucap + 64);
+    DA(g.g_sk, 2 * g.ucap + 64);
+    DA(g.g_sidx, 2 * g.ucap + 64);
+    DA(g.g_skey, 2 * g.ucap + 64);
+  }
   DA(g.bucket, g.ucap);
   DA(g.uniq, g.ucap);
   DA(g.ring, (size_t)g.Wp1 * g.cap * G);

@@ -157,6 +157,21 @@ def test_update_period(cfg1_g1, P, policy, pvp):
     assert not np.array_equal(ho, run_oracle(tr, G=1, **kw1)[:, 0, :])  # the period changes decisions
 
 
+@pytest.mark.parametrize("policy,pvp", [("hybrid", 1), ("lru", 0), ("rr", 0), ("dynamic", 1)])
+def test_oversized_set_buckets(policy, pvp):
+    """A few sets receiving thousands of distinct nodes per batch (more than k_set's shared
+    memory holds): those sets are processed in global scratch — still bit-exact."""
+    rng = np.random.default_rng(11)
+    N, D = 200_000, 4
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    tr = [[rng.integers(0, N, int(rng.integers(3000, 9000)))] for _ in range(12)]
+    kw = dict(N=N, D=D, L=64, A=32, scores=sc, policy=policy, pvp=pvp, W=4, V=400)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"big sets {policy}/pvp{pvp}")
+
+
 def test_determinism_launch_geometry(cfg1_g1, monkeypatch):
     """I9: identical counters and bytes under a different launch geometry (one warp per CTA
     in k_set, one CTA per SM for every grid-stride kernel) — the batch-synchronous rules make
