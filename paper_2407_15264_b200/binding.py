@@ -253,8 +253,13 @@ class Sampler:
         L = load_library()
         self.indptr = torch.from_numpy(np.ascontiguousarray(indptr, np.int64)).pin_memory()
         self.indices = torch.from_numpy(np.ascontiguousarray(indices, np.int32)).pin_memory()
-        _check(L.lsmgnn_sampler_attach(ctypes.c_void_p(self.indptr.data_ptr()), ctypes.c_void_p(self.indices.data_ptr()),
-                                       self.indptr.numel() - 1, self.indices.numel()))
+        self.reattach()
+
+    def reattach(self) -> None:
+        """(Re)register the pinned CSR with the library (lsmgnn_finalize forgets it)."""
+        _check(load_library().lsmgnn_sampler_attach(ctypes.c_void_p(self.indptr.data_ptr()),
+                                                    ctypes.c_void_p(self.indices.data_ptr()),
+                                                    self.indptr.numel() - 1, self.indices.numel()))
 
     @staticmethod
     def bound(nseeds: int, fanout) -> int:

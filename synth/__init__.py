@@ -277,11 +277,14 @@ def _lib():
     global _LIB
     if _LIB is None:
         so = os.path.join(_HERE, "libsynth.so")
-        src = os.path.join(_HERE, "features.c")
-        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        srcs = [os.path.join(_HERE, f) for f in ("features.c", "graphgen.c")]
+        if not os.path.exists(so) or os.path.getmtime(so) < max(os.path.getmtime(p) for p in srcs):
             subprocess.check_call(["gcc", "-O3", "-march=x86-64-v2", "-fopenmp", "-shared", "-fPIC",
-                                   "-o", so, src])
+                                   "-o", so, *srcs, "-lm"])
         L = ctypes.CDLL(so)
+        L.plcite_targets.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double,
+                                     ctypes.c_void_p, ctypes.c_void_p]
+        L.plcite_csr.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.synth_fill_f32.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64]
         L.synth_fill_f32_ids.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64]
         L.synth_check_f32_ids.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
@@ -293,6 +296,20 @@ def _lib():
 
 def build() -> None:
     _lib()
+
+
+def plcite_c(num_nodes: int, m: int, seed_g: int = 1, seed_pi: int = 2, beta: float = 0.8) -> Graph:
+    """plcite() in C (OpenMP) for 100M-node graphs; same recipe and the same permutation
+    (numpy's), int32 neighbour IDs."""
+    N = int(num_nodes)
+    pi = np.random.default_rng(seed_pi).permutation(N).astype(np.int64)
+    tg = np.empty(N * m, np.int32)
+    _lib().plcite_targets(N, m, seed_g, beta, pi.ctypes.data, tg.ctypes.data)
+    del pi
+    indptr = np.empty(N + 1, np.int64)
+    indices = np.empty(2 * N * m, np.int32)
+    _lib().plcite_csr(N, m, tg.ctypes.data, indptr.ctypes.data, indices.ctypes.data)
+    return Graph(N, indptr, indices)
 
 
 def fill_features(ptr: int, v0: int, nrows: int, D: int, seed_f: int = 5) -> None:

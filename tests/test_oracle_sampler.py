@@ -32,3 +32,11 @@ def test_sampler_properties():
     small = [x for x in seeds if g.indptr[x + 1] - g.indptr[x] <= 3]
     for x in small:
         assert nb(x) <= set(out.tolist())
+
+
+def test_c_graph_generator_matches_numpy():
+    """synth.plcite_c (for 100M-node graphs) builds the same CSR as synth.plcite."""
+    for N, m in [(3000, 4), (50000, 12)]:
+        a, b = synth.plcite(N, m), synth.plcite_c(N, m)
+        assert np.array_equal(a.indptr, b.indptr)
+        assert np.array_equal(a.indices.astype(np.int64), b.indices.astype(np.int64))
