@@ -124,6 +124,7 @@ class LsmGnn:
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         self.rank, self.world = rank, world
+        self._group = group
         self.num_nodes, self.feat_dim = int(num_nodes), int(feat_dim)
         self.row_bytes = feat_dim * (4 if dtype == F32 else 2)
         self.window = int(window)
@@ -239,8 +240,16 @@ class LsmGnn:
         return int(load_library().lsmgnn_kernel_launches())
 
     def close(self) -> None:
-        if _LIB is not None:
-            _LIB.lsmgnn_finalize()
+        """Free this rank's home. With G > 1 every rank first drains its GPU work and meets the
+        others at a barrier, so no peer is still pulling from memory about to be freed."""
+        if _LIB is None:
+            return
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self._group)
+        _LIB.lsmgnn_finalize()
 
 
 class Sampler:

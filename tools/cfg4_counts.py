@@ -67,7 +67,7 @@ def main():
 
             def merged(k):
                 if k not in batches:
-                    if k >= K:
+                    if k >= K + W:  # the window of every measured iteration is full
                         batches[k] = torch.zeros(0, dtype=torch.int64, device=dev)
                     else:
                         ts = time.time()
