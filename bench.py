@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--no-ablation", action="store_true", help="skip the PVP on/off ablation")
     p.add_argument("--lines", type=int, default=None, help="override lines per GPU")
     p.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph (G = 1)")
+    p.add_argument("--graph-steps", type=int, default=20, help="extra steps timed as CUDA-graph replays (G = 1)")
     return p.parse_args()
 
 
@@ -211,7 +212,8 @@ def main():
     W = wl.window
     pvp = wl.pvp if args.pvp is None else args.pvp
     lines = args.lines or wl.lines_per_gpu
-    iters = Wu + K + E + W + 1
+    GK = args.graph_steps if (G == 1 and not args.graph) else 0
+    iters = Wu + K + E + GK + W + 1
     g_, trace, scores = build_inputs(wl, G, rank, iters, only_mine=G > 1)
     mine = [np.asarray(trace[t][rank], np.int64) for t in range(iters)]
     max_ids = max(x.size for row in trace for x in row)
@@ -320,6 +322,23 @@ def main():
                "d2h_bytes_per_step": int(d2h / E), "steps": E,
                "what": "lsmgnn_gather_host: pinned host IDs -> device, gather, rows -> pinned host, synchronous"}
 
+    # ---- the same step replayed as one CUDA graph per iteration (device-resident iteration state)
+    graph_replay = None
+    if GK:
+        c.graph_capture(ids_d, out)
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ga.record(st)
+        for i in range(GK):
+            c.graph_replay()
+        gb.record(st)
+        torch.cuda.synchronize()
+        tg = ga.elapsed_time(gb) / 1e3
+        gbytes = sum(mine[Wu + K + E + i].size for i in range(GK)) * wl.R
+        graph_replay = {"steps": GK, "value": round(gbytes / tg / 1e9, 4), "unit": "GB/s",
+                        "ms_per_step": round(tg / GK * 1e3, 4),
+                        "what": "lsmgnn_graph_capture once, then one cudaGraphLaunch per step (gather + window feed)"}
+
     # ---- roofline of the dominant phase, per-tier fractions
     peaks = {}
     try:
@@ -384,6 +403,7 @@ def main():
         "roofline": roof,
         "cpu_baseline": None,
         "e2e": e2e,
+        "graph_replay": graph_replay,
         "per_step_ms": {"median": round(statistics.median(per_step), 4), "min": round(min(per_step), 4),
                         "max": round(max(per_step), 4)},
         "tiers": {"hit_ratio": round(d["hits"] / uniq, 4), "victim_hit_ratio": round(d["victim_hits"] / uniq, 4),
