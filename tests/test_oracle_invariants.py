@@ -182,3 +182,31 @@ def test_invariants_update_period(P, policy, pvp):
                V=C * W, P=P)
     c = run_checked(o, rand_trace(rng, G, N, 30, 25), C)
     assert c[..., F["evict_fresh"]].sum() > 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_north_star_reuse_protected(seed):
+    """The north star's invariant, exact for hybrid with pvp = 0 and P = 1 (R21):
+    a line whose dynamic reuse count is > 0 (Far/Near, key level > 0) is evicted only when no
+    other candidate — no unprotected NoReuse line (level 0) — survives in its set."""
+    rng = np.random.default_rng(seed)
+    G, A, S, W = 2, 4, 3, 8
+    N = 90
+    o = Oracle(G, N, 16, S * A, A, rng.integers(0, 256, N).astype(np.uint8), policy="hybrid", pvp=0, W=W)
+    trace = rand_trace(rng, G, N, 40, 30)
+    K = len(trace)
+    empty = [np.zeros(0, np.int64)] * G
+    for k in range(1, W + 1):
+        o.feed(k, trace[k] if k < K else empty)
+    evicted_with_reuse = 0
+    for t in range(K):
+        o.gather(t, trace[t])
+        ev = o.events()
+        for (g, s) in set(map(tuple, ev[:, :2].tolist())):
+            e = ev[(ev[:, 0] == g) & (ev[:, 1] == s)]
+            if any(r[2] == 0 and r[4] > 0 for r in e):  # a line with reuse was evicted ...
+                evicted_with_reuse += 1
+                assert not any(r[2] == 1 and r[4] == 0 for r in e)  # ... so no NoReuse line survived
+        o.pvp_prefetch(t)
+        o.feed(t + 1 + W, trace[t + 1 + W] if t + 1 + W < K else empty)
+    assert evicted_with_reuse > 0  # the situation occurs

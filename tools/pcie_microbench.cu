@@ -245,6 +245,53 @@ int main(int argc, char** argv) {
     snprintf(nm, 96, "SM host->host relay (read+write) grid=%d", blocks);
     timeit(nm, [&] { k_relay<<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)houtd, R / 16); });
   }
+  // full duplex: SM zero-copy H2D reads (stream A) concurrent with a copy-engine D2H (stream B)
+  {
+    cudaStream_t sa, sb;
+    CK(cudaStreamCreateWithFlags(&sa, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
+    uint8_t* dsrc;
+    CK(cudaMalloc(&dsrc, (size_t)n * R));
+    cudaEvent_t a0, a1, b1;
+    cudaEventCreate(&a0);
+    cudaEventCreate(&a1);
+    cudaEventCreate(&b1);
+    for (int it = 0; it < 3; ++it) {
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(a0, 0);
+      cudaStreamWaitEvent(sa, a0, 0);
+      cudaStreamWaitEvent(sb, a0, 0);
+      k_ldg<8, 0><<<sms, 256, 0, sa>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16);
+      cudaEventRecord(a1, sa);
+      cudaMemcpyAsync(hout, dsrc, (size_t)n * R, cudaMemcpyDeviceToHost, sb);
+      cudaEventRecord(b1, sb);
+      CK(cudaDeviceSynchronize());
+      float ma, mb;
+      cudaEventElapsedTime(&ma, a0, a1);
+      cudaEventElapsedTime(&mb, a0, b1);
+      if (it == 2)
+        printf("duplex: SM H2D reads %.2f GB/s (%.3f ms) || CE D2H %.2f GB/s (%.3f ms)\n", (double)n * R / ma / 1e6, ma,
+               (double)n * R / mb / 1e6, mb);
+    }
+    // and SM reads || SM D2H stores from a different kernel
+    for (int it = 0; it < 3; ++it) {
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(a0, 0);
+      cudaStreamWaitEvent(sa, a0, 0);
+      cudaStreamWaitEvent(sb, a0, 0);
+      k_ldg<8, 0><<<sms, 256, 0, sa>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16);
+      cudaEventRecord(a1, sa);
+      k_d2h<<<sms, 256, 0, sb>>>((const uint4*)dsrc, n, (uint4*)houtd, R / 16);
+      cudaEventRecord(b1, sb);
+      CK(cudaDeviceSynchronize());
+      float ma, mb;
+      cudaEventElapsedTime(&ma, a0, a1);
+      cudaEventElapsedTime(&mb, a0, b1);
+      if (it == 2)
+        printf("duplex: SM H2D reads %.2f GB/s (%.3f ms) || SM D2H stores %.2f GB/s (%.3f ms)\n",
+               (double)n * R / ma / 1e6, ma, (double)n * R / mb / 1e6, mb);
+    }
+  }
   CK(cudaGetLastError());
   // correctness of one row
   std::vector<uint8_t> chk(R);
