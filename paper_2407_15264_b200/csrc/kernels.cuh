@@ -1,18 +1,22 @@
 // kernels.cuh — sm_100a kernels of the LSM-GNN gather hot path.
 //
 // Step names follow SURVEY.md §8(a) (S1..S11) and DESIGN.md §"Kernels":
-//   k_route      S1   requester: validate IDs, bucket by home (v mod G), write home inboxes
-//   k_dedup      S3   home: unique nodes of the batch (node-indexed stamp table) + per-set counts
-//   k_scan       S3   home: exclusive scan of per-set counts; PVP "unused" accounting
-//   k_bucket     S3   home: scatter unique nodes into set buckets
-//   k_set        S4+S5 home: warp per touched set — tag probe, staging probe, bypass selection,
-//                     way assignment by the policy key, eviction classes, victim candidates
+//   k_begin/k_end  S9  per-iteration state (IterState: t, stamps, batch pointer) and counters
+//   k_route_local  S1  G = 1: validate IDs, write the home inbox (or a window ring slot)
+//   k_route_peer   S1  G > 1: bucket by home (v mod G), store into the homes' inboxes (P2P)
+//   k_dedup        S3  home: unique nodes (node-indexed stamp table) + per-set counts (+ request lists)
+//   k_scan         S3  home: exclusive scan of per-set counts; oversized-set scratch; PVP "unused"
+//   k_bucket       S3  home: scatter unique nodes into set buckets
+//   k_snapshot     S4  period > 1: the paper's periodic window scan of every resident line
+//   k_set          S4+S5 home: warp per touched set — tag probe, staging probe, bypass selection,
+//                       way assignment by the policy key, eviction classes, victim candidates
 //   k_qhist/k_qscatter/k_admit  S5  victim admission per queue (PVP)
-//   k_fill       S6   home: victim row D2H (old slot content) then new row -> slot / staging
-//   k_pull       S7+S8 requester: location lookup at the home + row copy into `out`
-//   k_begin/k_end S9  per-iteration counters
-//   k_mask_*     S10  window feed: reuse bitmask update
-//   k_pvp        S11  PVP copy of victim queue (t+1) mod W into home staging (side stream)
+//   k_serve        S6+S8 G = 1: fill (victim D2H, storage/staging row -> slot) fused with delivery
+//                       to every requester; 1 warp in 8 copies the hits
+//   k_fill         S6  G > 1: victim row D2H then new row -> slot / bypass staging
+//   k_pull         S7+S8 G > 1: location lookup at the home + row copy (local or peer HBM)
+//   k_win_begin, k_mask_clear, k_mask_set, k_win_gather  S10  window feed (reuse bitmask)
+//   k_pvp          S11 PVP copy of victim queue (t+1) mod W into home staging (side stream)
 #pragma once
 #include "device_common.cuh"
 
