@@ -28,6 +28,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "effective feature-gather GB/s (box, device-timed)"
+SM_PCIE_CEILING = 51.47  # GB/s, profiles/r01_pcie_microbench.txt
 
 
 def parse():
@@ -378,7 +379,12 @@ def main():
                                "link is the bound of the storage tier); SM-initiated reads of scattered 4 KiB "
                                "host rows top out at 51.5 GB/s on this box (profiles/r01_pcie_microbench.txt)",
                 "per_launch": {"algorithmic_bytes": int(fill_pcie / K), "units": "storage rows x R (H2D)",
-                               "avg_ms": round(fill_ms / K, 4)}}
+                               "avg_ms": round(fill_ms / K, 4)},
+                # context: the best any SM-initiated read of scattered host rows reached on this box
+                # (LDG at any unroll/grid, .L2::256B, bulk L2 prefetch, TMA bulk) — 128-B PCIe reads
+                "sm_path_ceiling_GBps": SM_PCIE_CEILING,
+                "frac_of_sm_path_ceiling": round(ach / SM_PCIE_CEILING, 4),
+                "sm_path_ceiling_source": "profiles/r01_pcie_microbench.txt (tools/pcie_microbench.cu)"}
         phases["fill"]["pcie_h2d_GBps"] = round(ach, 2)
         phases["fill"]["frac_pcie"] = round(ach / pcie_peak, 4)
     if pull_ms > 0:
