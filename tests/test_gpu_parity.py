@@ -172,6 +172,60 @@ def test_oversized_set_buckets(policy, pvp):
     compare(hg, ho, f"big sets {policy}/pvp{pvp}")
 
 
+def test_bf16_rows():
+    """dtype only sets the row size (R = feat_dim x 2 for bf16/fp16): the gathered bytes and
+    the counters are those of the same rows moved as bytes."""
+    import torch
+    from paper_2407_15264_b200 import BF16, LsmGnn
+    from .harness import table_for
+    rng = np.random.default_rng(3)
+    N, D = 5000, 8  # 8 u32 words = 32 bytes = 16 bf16 values per row
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    tr = [[rng.integers(0, N, 200)] for _ in range(10)]
+    ho = run_oracle(tr, G=1, N=N, D=D, L=64, A=8, scores=sc, policy="hybrid", pvp=0, W=4)[:, 0, :]
+    c = LsmGnn(N, 2 * D, 64, 8, 0, sc, dtype=BF16, window=4, max_batch_ids=200)
+    c.attach_storage(table_for(N, D, pinned=True))
+    ids = [torch.from_numpy(x[0]).cuda() for x in tr] + [torch.zeros(0, dtype=torch.int64, device="cuda")] * 5
+    c.prefetch(ids[1:5], first_iter=1)
+    out = torch.empty((200, 4 * D), dtype=torch.uint8, device="cuda")
+    for t in range(10):
+        c.gather(ids[t], out)
+        c.prefetch([ids[t + 5]], first_iter=t + 5)
+        assert synth.check_rows(out.cpu().numpy().view(np.uint32).reshape(200, D), tr[t][0], D)[0] == 0
+    compare(c.history(0, 10), ho, "bf16")
+    c.close()
+
+
+def test_long_run_history_wrap():
+    """6,000 iterations (the on-device history keeps the last 4,096): the cumulative counters
+    and the last 4,096 per-iteration records still equal the oracle's (stamps, rings, wraps)."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    from .harness import table_for
+    from oracle import Oracle, run_trace
+    rng = np.random.default_rng(5)
+    N, D, K, W = 3000, 4, 6000, 3
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    tr = [[rng.integers(0, N, int(rng.integers(0, 60)))] for _ in range(K)]
+    ho = run_trace(Oracle(1, N, 16, 64, 4, sc, policy="hybrid", pvp=1, W=W, V=8 * W), tr)[:, 0, :]
+    c = LsmGnn(N, D, 64, 4, 8 * W, sc, policy="hybrid", pvp=1, window=W, max_batch_ids=60)
+    c.attach_storage(table_for(N, D, pinned=True))
+    ids = [torch.from_numpy(np.asarray(x[0], np.int64)).cuda() for x in tr]
+    ids += [torch.zeros(0, dtype=torch.int64, device="cuda")] * (W + 1)
+    c.prefetch(ids[1:W + 1], first_iter=1)
+    out = torch.empty((64, 4 * D), dtype=torch.uint8, device="cuda")
+    for t in range(K):
+        c.gather(ids[t], out)
+        c.prefetch([ids[t + 1 + W]], first_iter=t + 1 + W)
+    torch.cuda.synchronize()
+    compare(c.history(K - 4096, 4096), ho[K - 4096:], "history tail")
+    cum = c.stats(1)
+    from paper_2407_15264_b200 import STATS_FIELDS
+    for i, f in enumerate(STATS_FIELDS[1:], 1):
+        assert cum[f] == int(ho[:, i].sum()), f
+    c.close()
+
+
 def test_determinism_launch_geometry(cfg1_g1, monkeypatch):
     """I9: identical counters and bytes under a different launch geometry (one warp per CTA
     in k_set, one CTA per SM for every grid-stride kernel) — the batch-synchronous rules make
