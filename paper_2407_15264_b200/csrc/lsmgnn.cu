@@ -9,6 +9,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -253,12 +254,18 @@ cudaEvent_t take_event() {
   return e;
 }
 // Phase span on stream st: prof_begin records the start event, prof_end the end event.
+// NVTX ranges name the same phases for nsys / ncu timelines (no cost without a tool attached).
+const char* const kPhaseName[LSMGNN_NPHASES] = {"lsmgnn.route", "lsmgnn.dedup", "lsmgnn.probe_replace",
+                                                "lsmgnn.admit", "lsmgnn.fill", "lsmgnn.pull",
+                                                "lsmgnn.window", "lsmgnn.pvp"};
 void prof_begin(int ph, cudaStream_t st) {
+  nvtxRangePushA(kPhaseName[ph]);
   if (!g.prof) return;
   g.open_ev[ph] = take_event();
   cudaEventRecord(g.open_ev[ph], st);
 }
 void prof_end(int ph, cudaStream_t st) {
+  nvtxRangePop();
   if (!g.prof || !g.open_ev[ph]) return;
   cudaEvent_t b = take_event();
   cudaEventRecord(b, st);
