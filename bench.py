@@ -557,59 +557,82 @@ def epoch_storage(wl, g, scores, lines, dev, policies=("hybrid", "static", "lru"
     return res
 
 
-def gpu_sampler_pipeline(wl, g, scores, table, lines, args, dev, warm=5, steps=20):
-    """N3 measured: the window producer on the GPU inside the step. Each step samples batch
-    t+1+W with the UVA sampler (lsmgnn_sample), feeds it (lsmgnn_prefetch_dev) and gathers
-    batch t (sampled W steps earlier). Reports the sampler's own time and the whole step."""
+def gpu_sampler_pipeline(wl, g, scores, table, lines, args, dev, warm=5, steps=20, train_ms=10.0):
+    """N3 measured: the window producer on the GPU inside the step, and the PVP's overlap with a
+    fixed-cost "training" consumer. Each step samples batch t+1+W with the UVA sampler
+    (lsmgnn_sample), gathers batch t (sampled W steps earlier), feeds the new batch
+    (lsmgnn_prefetch_dev) and — with the PVP on — launches the side-stream copy of victim queue
+    t+1; then a GPU sleep kernel of train_ms stands in for training. GB/s counts requested rows
+    over the device time of sampler + gather + feed (training excluded)."""
     import torch
     import synth
     from paper_2407_15264_b200 import LsmGnn, Sampler, prefetch_dev
     W = wl.window
     st = torch.cuda.current_stream()
     bound = Sampler.bound(wl.batch, wl.fanout)
-    c = LsmGnn(wl.N, wl.D, lines, wl.ways, 0, scores, policy=args.policy, pvp=0, window=W, max_batch_ids=bound,
-               device=dev.index)
-    c.attach_storage(table)
-    s = Sampler(g.indptr, g.indices)
     perm = torch.from_numpy(synth.epoch_seeds(wl.N, 0)).to(dev)
-    total = warm + steps + W + 1
-    bufs = [(torch.empty(bound, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev))
-            for _ in range(W + 2)]
-    counts_host = {}
+    cycles = int(train_ms * 1e-3 * 1.9e9)
+    res = {"steps": steps, "warmup": warm, "train_stand_in_ms": train_ms,
+           "what": "GPU UVA GraphSAGE sampler (CSR pinned in host memory) feeds the window inside the step; "
+                   "hybrid, same workload; variants: no training gap, and a training stand-in with PVP off/on"}
+    samp = None
+    for name, pvp, train in (("pvp0_no_training", 0, False), ("pvp0_training", 0, True), ("pvp1_training", 1, True)):
+        c = LsmGnn(wl.N, wl.D, lines, wl.ways, wl.victim_lines if pvp else 0, scores, policy=args.policy, pvp=pvp,
+                   window=W, max_batch_ids=bound, device=dev.index)
+        c.attach_storage(table)
+        if samp is None:
+            samp = Sampler(g.indptr, g.indices)
+        else:
+            samp.reattach()
+        bufs = [(torch.empty(bound, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev))
+                for _ in range(W + 2)]
 
-    def sample(k):
-        o, cn = bufs[k % (W + 2)]
-        s.sample(perm[k * wl.batch:(k + 1) * wl.batch], wl.fanout, wl.seeds["s"], k, 0, out=o, count=cn)
-        return o, cn
+        def sample(k):
+            o, cn = bufs[k % (W + 2)]
+            samp.sample(perm[k * wl.batch:(k + 1) * wl.batch], wl.fanout, wl.seeds["s"], k, 0, out=o, count=cn)
+            return o, cn
 
-    for k in range(1, W + 1):
-        prefetch_dev(*sample(k), first_iter=k)
-    o0, c0 = sample(0)
-    out = torch.empty((bound, wl.R), dtype=torch.uint8, device=dev)
-    samp_ms, step_ms, nbytes, nids = 0.0, 0.0, 0, 0
-    for t in range(warm + steps):
-        o, cn = bufs[t % (W + 2)] if t else (o0, c0)
-        n = int(cn.item())  # sampled W steps ago: long complete
-        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        e0.record(st)
-        ok, ck = sample(t + 1 + W)
-        e1.record(st)
-        c.gather(o[:n], out)
-        prefetch_dev(ok, ck, first_iter=t + 1 + W)
-        e2.record(st)
-        if t >= warm:
-            e2.synchronize()
-            samp_ms += e0.elapsed_time(e1)
-            step_ms += e0.elapsed_time(e2)
-            nbytes += n * wl.R
-            nids += int(ck.item())
-    c.close()
-    return {"steps": steps, "sampler_ms_per_batch": round(samp_ms / steps, 4),
-            "sampled_ids_per_s": round(nids / (samp_ms / 1e3), 1),
-            "step_ms_with_sampler": round(step_ms / steps, 4),
-            "gather_GBps_incl_sampler": round(nbytes / (step_ms / 1e3) / 1e9, 3),
-            "what": "GPU UVA GraphSAGE sampler (CSR pinned in host memory) feeding the window inside the step; "
-                    "hybrid, pvp 0, same workload"}
+        for k in range(W + 1):
+            o, cn = sample(k)
+            if k:
+                prefetch_dev(o, cn, first_iter=k)
+        out = torch.empty((bound, wl.R), dtype=torch.uint8, device=dev)
+        samp_ms, step_ms, nbytes, nids = 0.0, 0.0, 0, 0
+        s0 = None
+        for t in range(warm + steps):
+            if t == warm:
+                torch.cuda.synchronize()
+                s0 = c.stats(1)
+            o, cn = bufs[t % (W + 2)]
+            n = int(cn.item())  # sampled W steps ago: long complete
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(st)
+            ok, ck = sample(t + 1 + W)
+            e1.record(st)
+            c.gather(o[:n], out)
+            prefetch_dev(ok, ck, first_iter=t + 1 + W)
+            if pvp:
+                c.prefetch([], first_iter=0)  # PVP copy of queue t+1 on the side stream
+            e2.record(st)
+            if train:
+                torch.cuda._sleep(cycles)
+            if t >= warm:
+                e2.synchronize()
+                samp_ms += e0.elapsed_time(e1)
+                step_ms += e0.elapsed_time(e2)
+                nbytes += n * wl.R
+                nids += int(ck.item())
+        torch.cuda.synchronize()
+        s1 = c.stats(1)
+        c.close()
+        u = max(s1["unique"] - s0["unique"], 1)
+        res[name] = {"sampler_ms_per_batch": round(samp_ms / steps, 4),
+                     "sampled_ids_per_s": round(nids / (samp_ms / 1e3), 1),
+                     "step_ms_excl_training": round(step_ms / steps, 4),
+                     "gather_GBps_incl_sampler": round(nbytes / (step_ms / 1e3) / 1e9, 3),
+                     "hit_ratio": round((s1["hits"] - s0["hits"]) / u, 4),
+                     "victim_hit_ratio": round((s1["victim_hits"] - s0["victim_hits"]) / u, 4)}
+    return res
 
 
 def measure_h2d(dev) -> float:
