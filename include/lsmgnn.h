@@ -207,6 +207,13 @@ int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope);
  * ring of the last 4096 iterations). Synchronous. */
 int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count);
 
+/* Debug/inspection (tests): copy a piece of this home's cache state to host memory after
+ * synchronising. what = 0: tags u32[lines_per_gpu] (node ID per line, set-major, way-minor;
+ * 0xFFFFFFFF = empty); 1: last use u32[lines_per_gpu]; 2: victim-queue lengths u32[W];
+ * 3: victim-queue nodes u32[W * C] (queue k at [k*C, k*C + len_k)). `count` = elements the
+ * caller's buffer holds; returns EINVAL if it is smaller than the piece. */
+int lsmgnn_debug_state(int32_t what, void* out_host, int64_t count);
+
 /* Number of kernels the library has launched since init (launch accounting). */
 int64_t lsmgnn_kernel_launches(void);
 

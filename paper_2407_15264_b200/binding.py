@@ -24,7 +24,7 @@ EXPORTS = ["lsmgnn_bind", "lsmgnn_set_options", "lsmgnn_init", "lsmgnn_attach_st
            "lsmgnn_export_handle", "lsmgnn_connect", "lsmgnn_gather", "lsmgnn_gather_host", "lsmgnn_prefetch",
            "lsmgnn_stats", "lsmgnn_stats_history", "lsmgnn_kernel_launches", "lsmgnn_finalize",
            "lsmgnn_last_error", "lsmgnn_profile", "lsmgnn_profile_read", "lsmgnn_sampler_attach", "lsmgnn_sample",
-           "lsmgnn_prefetch_dev", "lsmgnn_graph_capture", "lsmgnn_graph_replay"]
+           "lsmgnn_prefetch_dev", "lsmgnn_graph_capture", "lsmgnn_graph_replay", "lsmgnn_debug_state"]
 PHASES = ["route", "dedup", "probe_replace", "admit", "fill", "pull", "window", "pvp"]
 
 
@@ -80,6 +80,7 @@ def load_library(path: str = SO_PATH) -> ctypes.CDLL:
         "lsmgnn_prefetch_dev": ([vp, vp, i64, vp], i32),
         "lsmgnn_graph_capture": ([vp, vp, i32, vp, vp], i32),
         "lsmgnn_graph_replay": ([vp], i32),
+        "lsmgnn_debug_state": ([i32, vp, i64], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -220,6 +221,12 @@ class LsmGnn:
         _check(_LIB.lsmgnn_graph_capture(ctypes.c_void_p(self._ring_ptrs.data_ptr()),
                                          ctypes.c_void_p(self._ring_n.data_ptr()), len(batches),
                                          ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))))
+
+    def debug_state(self, what: int, count: int) -> np.ndarray:
+        """Cache state for tests: 0 tags, 1 last use, 2 victim-queue lengths, 3 queue nodes."""
+        buf = np.zeros(max(count, 1), np.uint32)
+        _check(_LIB.lsmgnn_debug_state(int(what), buf.ctypes.data, buf.size))
+        return buf[:count]
 
     def graph_replay(self, stream=None) -> None:
         _check(_LIB.lsmgnn_graph_replay(ctypes.c_void_p(_stream_ptr(stream))))

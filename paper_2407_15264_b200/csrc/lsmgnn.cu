@@ -1133,6 +1133,24 @@ int lsmgnn_graph_replay(void* stream) {
   return 0;
 }
 
+int lsmgnn_debug_state(int32_t what, void* out_host, int64_t count) {
+  if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
+  const void* src = nullptr;
+  int64_t n = 0;
+  switch (what) {
+    case 0: src = g.tags; n = (int64_t)g.L; break;
+    case 1: src = g.last_use; n = (int64_t)g.L; break;
+    case 2: src = g.qlen; n = g.C ? (int64_t)g.W : 0; break;
+    case 3: src = g.qnode; n = (int64_t)(g.W * g.C); break;
+    default: return set_err(LSMGNN_EINVAL, "bad debug_state selector %d", what);
+  }
+  if (!out_host || count < n) return set_err(LSMGNN_EINVAL, "debug_state buffer holds %lld < %lld", (long long)count,
+                                             (long long)n);
+  CK(cudaDeviceSynchronize());
+  if (n) CK(cudaMemcpy(out_host, src, (size_t)n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 int lsmgnn_profile(int32_t enable) {
   g.prof = enable != 0;
   return 0;

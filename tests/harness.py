@@ -28,7 +28,8 @@ def table_for(N: int, D: int, seed_f: int = 5, pinned: bool = False, home: int =
 
 
 def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1, table=None,
-            check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False, P=1):
+            check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False, P=1,
+            state_cb=None):
     """Run trace[t][rank] through the library. Returns (history [K, 24] uint64, outs or None, bad_rows).
 
     check_rows: "full" compares every row with the closed form F(v); "none" skips it."""
@@ -62,6 +63,8 @@ def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0,
                 outs.append(host)
     torch.cuda.synchronize()
     hist = c.history(0, K)
+    if state_cb is not None:  # inspect the final cache state before the home is freed
+        state_cb(c)
     c.close()
     return hist, (outs if keep_outs else None), bad
 

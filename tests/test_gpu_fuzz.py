@@ -36,8 +36,19 @@ def random_case(seed):
 
 @pytest.mark.parametrize("seed", range(int(os.environ.get("LSMGNN_FUZZ", "40"))))
 def test_fuzz_parity(seed):
+    from oracle import Oracle, run_trace
     cfg, tr, sc = random_case(seed)
-    hg, _, bad = run_gpu(tr, scores=sc, max_batch_ids=max(1, max(len(x[0]) for x in tr)), **cfg)
-    ho = run_oracle(tr, G=1, scores=sc, **cfg)[:, 0, :]
+    state = {}
+    hg, _, bad = run_gpu(tr, scores=sc, max_batch_ids=max(1, max(len(x[0]) for x in tr)),
+                         state_cb=lambda c: state.update(tags=c.debug_state(0, cfg["L"]),
+                                                         lu=c.debug_state(1, cfg["L"])), **cfg)
+    o = Oracle(1, cfg["N"], 4 * cfg["D"], cfg["L"], cfg["A"], sc, policy=cfg["policy"], pvp=cfg["pvp"], W=cfg["W"],
+               T=cfg["T"], V=cfg["V"], reinsert=cfg["reinsert"], P=cfg["P"])
+    ho = run_trace(o, tr)[:, 0, :]
     assert bad == 0
     compare(hg, ho, f"fuzz {seed}: {cfg}")
+    # the final cache state, way by way
+    ot, olu = o.tags(0)
+    gt = state["tags"].astype(np.int64)
+    gt[gt == 0xFFFFFFFF] = -1
+    assert np.array_equal(gt, ot.reshape(-1)) and np.array_equal(state["lu"].astype(np.int64), olu.reshape(-1))

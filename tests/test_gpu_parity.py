@@ -172,6 +172,51 @@ def test_oversized_set_buckets(policy, pvp):
     compare(hg, ho, f"big sets {policy}/pvp{pvp}")
 
 
+@pytest.mark.parametrize("policy,pvp,P", [("hybrid", 1, 1), ("lru", 0, 1), ("rr", 1, 1), ("dynamic", 1, 2)])
+def test_cache_state_parity(cfg1_g1, policy, pvp, P):
+    """Stronger than equal counters: after every iteration the GPU's cache state equals the
+    oracle's — the tag and last-use of every way of every set (way placement included) and
+    the content of every victim queue (as a set: slot order within a batch's admissions is
+    the atomic arrival order on the GPU)."""
+    import torch
+    from oracle import Oracle
+    from paper_2407_15264_b200 import LsmGnn
+    from .harness import table_for
+    g, tr, sc = cfg1_g1
+    N, D, L, A, W, V = 16384, 128, 1024, 8, 8, 512
+    K = len(tr)
+    o = Oracle(1, N, 4 * D, L, A, sc, policy=policy, pvp=pvp, W=W, V=V, P=P)
+    mb = max(len(x[0]) for x in tr)
+    c = LsmGnn(N, D, L, A, V, sc, policy=policy, pvp=pvp, window=W, max_batch_ids=mb, period=P)
+    c.attach_storage(table_for(N, D, pinned=True))
+    ids = [torch.from_numpy(np.asarray(x[0], np.int64)).cuda() for x in tr]
+    ids += [torch.zeros(0, dtype=torch.int64, device="cuda")] * (W + 1)
+    empty = [np.zeros(0, np.int64)]
+    for k in range(1, W + 1):
+        o.feed(k, tr[k] if k < K else empty)
+    c.prefetch(ids[1:W + 1], first_iter=1)
+    out = torch.empty((mb, 4 * D), dtype=torch.uint8, device="cuda")
+    C = V // W
+    for t in range(K):
+        o.gather(t, tr[t])
+        o.pvp_prefetch(t)
+        o.feed(t + 1 + W, tr[t + 1 + W] if t + 1 + W < K else empty)
+        c.gather(ids[t], out)
+        c.prefetch([ids[t + 1 + W]], first_iter=t + 1 + W)
+        ot, olu = o.tags(0)
+        gt = c.debug_state(0, L).astype(np.int64)
+        gt[gt == 0xFFFFFFFF] = -1
+        assert np.array_equal(gt.reshape(ot.shape), ot), t
+        assert np.array_equal(c.debug_state(1, L).astype(np.int64).reshape(olu.shape), olu), t
+        if pvp:
+            qlen = c.debug_state(2, W)
+            qn = c.debug_state(3, W * C)
+            for k in range(W):
+                onodes, _ = o.queue(0, k)
+                assert sorted(qn[k * C:k * C + qlen[k]].tolist()) == sorted(onodes.tolist()), (t, k)
+    c.close()
+
+
 def test_bf16_rows():
     """dtype only sets the row size (R = feat_dim x 2 for bf16/fp16): the gathered bytes and
     the counters are those of the same rows moved as bytes."""
