@@ -10,7 +10,7 @@
 //   k_snapshot     S4  period > 1: the paper's periodic window scan of every resident line
 //   k_set          S4+S5 home: warp per touched set — tag probe, staging probe, bypass selection,
 //                       way assignment by the policy key, eviction classes, victim candidates
-//   k_qhist/k_qscatter/k_admit  S5  victim admission per queue (PVP)
+//   k_qscatter/k_admit  S5  victim admission per queue (PVP); k_set builds the histogram
 //   k_serve        S6+S8 G = 1: fill (victim D2H, storage/staging row -> slot) fused with delivery
 //                       to every requester; 1 warp in 8 copies the hits
 //   k_fill         S6  G > 1: victim row D2H then new row -> slot / bypass staging
@@ -74,21 +74,29 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
 // mirrored to pinned host memory; a graph replay advances it->t_next.
 __global__ void k_end(IterState* it, unsigned long long* hist, unsigned long long* cum, Scratch* scr, uint32_t R,
                       volatile uint32_t* bad_mirror, uint32_t advance) {
-  if (threadIdx.x != 0) return;
+  __shared__ unsigned long long s_rec[F_NFIELDS];
+  const int f = threadIdx.x;  // one field per thread (blockDim = 32 >= F_NFIELDS)
   const uint64_t t = it->t;
   unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
-  rec[F_UNIQUE] = scr->nuniq;
-  rec[F_REQ] = scr->nreq;
-  rec[F_BOUT] = rec[F_REQ] * R;
-  rec[F_BNVL] = rec[F_PEER] * R;
-  rec[F_BH2D] = rec[F_STOR] * R;
-  rec[F_BPVP] = rec[F_PREF] * R;
-  rec[F_BD2H] = rec[F_VADM] * R;
-  for (int f = 1; f < F_NFIELDS; ++f) cum[f] += rec[f];
-  cum[F_ITER] = t;
-  scr->staged[(t + 1) & 1] = 0;
-  *bad_mirror = scr->bad_ids;
-  it->t_next = t + 1;  // direct calls and graph replays may be mixed
+  if (f == 0) {
+    rec[F_UNIQUE] = scr->nuniq;
+    rec[F_REQ] = scr->nreq;
+    rec[F_BOUT] = (unsigned long long)scr->nreq * R;
+    rec[F_BNVL] = rec[F_PEER] * R;
+    rec[F_BH2D] = rec[F_STOR] * R;
+    rec[F_BPVP] = rec[F_PREF] * R;
+    rec[F_BD2H] = rec[F_VADM] * R;
+  }
+  __syncthreads();
+  if (f < F_NFIELDS) s_rec[f] = rec[f];
+  __syncthreads();
+  if (f > 0 && f < F_NFIELDS) cum[f] += s_rec[f];
+  if (f == 0) {
+    cum[F_ITER] = t;
+    scr->staged[(t + 1) & 1] = 0;
+    *bad_mirror = scr->bad_ids;
+    it->t_next = t + 1;  // direct calls and graph replays may be mixed
+  }
   (void)advance;
 }
 
@@ -358,6 +366,7 @@ struct SetParams {
   const uint32_t* vst_idx;
   FillEnt* fills;
   Cand* cands;
+  uint32_t* qcnt;        // per-queue candidate counts (pvp = 1), zero on entry
   Scratch* scr;
   const IterState* it;       // t, stamp, p0, staging parity, record of this iteration
   unsigned long long* hist;
@@ -661,6 +670,7 @@ __global__ void k_set(SetParams p) {
           c.fill = fidx;
           c.pad = 0;
           p.cands[cidx] = c;
+          atomicAdd(&p.qcnt[reuse % p.W], 1u);  // per-queue histogram for the admission scan
         }
       }
     }
@@ -705,13 +715,8 @@ __global__ void k_set(SetParams p) {
 }
 
 // ------------------------------------------------------------------------------ S5: admission
-// Histogram of victim candidates per queue k = reuse mod W ("fourth victim buffer").
-__global__ void k_qhist(const Cand* __restrict__ cands, const Scratch* scr, uint32_t W,
-                        uint32_t* __restrict__ qcnt) {
-  const uint32_t n = scr->ncand;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicAdd(&qcnt[cands[i].reuse % W], 1u);
-}
+// Candidates grouped by queue k = reuse mod W ("fourth victim buffer"): qcnt (built by
+// k_set) is scanned into qoff, then counted back down to zero here.
 __global__ void k_qscatter(const Cand* __restrict__ cands, const Scratch* scr, uint32_t W,
                            const uint32_t* __restrict__ qoff, uint32_t* __restrict__ qcnt,
                            uint32_t* __restrict__ qb) {

@@ -400,6 +400,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   sp.vst_idx = g.vst_idx;
   sp.fills = g.fills;
   sp.cands = g.cands;
+  sp.qcnt = g.qcnt;
   sp.scr = g.scr;
   sp.it = g.it;
   sp.hist = g.hist;
@@ -439,8 +440,6 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   if (g.C) {
     prof_begin(3, st);
     const int qg = grid_for(g.ucap, 256, 2);
-    k_qhist<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qcnt);
-    LAUNCHED();
     k_scan<<<1, 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr, nullptr, 0);
     LAUNCHED();
     k_qscatter<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
