@@ -573,8 +573,9 @@ def gpu_sampler_pipeline(wl, g, scores, table, lines, args, dev, warm=5, steps=2
     perm = torch.from_numpy(synth.epoch_seeds(wl.N, 0)).to(dev)
     cycles = int(train_ms * 1e-3 * 1.9e9)
     res = {"steps": steps, "warmup": warm, "train_stand_in_ms": train_ms,
-           "what": "GPU UVA GraphSAGE sampler (CSR pinned in host memory) feeds the window inside the step; "
-                   "hybrid, same workload; variants: no training gap, and a training stand-in with PVP off/on"}
+           "what": "GPU GraphSAGE sampler (CSR copied to HBM; the paper's host-UVA placement is the library's "
+                   "default) feeds the window inside the step; hybrid, same workload; variants: no training gap, "
+                   "and a training stand-in with PVP off/on", "csr_placement": "hbm"}
     samp = None
     for name, pvp, train in (("pvp0_no_training", 0, False), ("pvp0_training", 0, True), ("pvp1_training", 1, True)):
         c = LsmGnn(wl.N, wl.D, lines, wl.ways, wl.victim_lines if pvp else 0, scores, policy=args.policy, pvp=pvp,
@@ -584,6 +585,7 @@ def gpu_sampler_pipeline(wl, g, scores, table, lines, args, dev, warm=5, steps=2
             samp = Sampler(g.indptr, g.indices)
         else:
             samp.reattach()
+        samp.place(True)  # the 1M-node CSR (0.1 GB) lives in HBM; the paper's UVA placement is place(False)
         bufs = [(torch.empty(bound, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev))
                 for _ in range(W + 2)]
 

@@ -183,6 +183,10 @@ int lsmgnn_sampler_attach(const int64_t* indptr, const int32_t* indices, int64_t
 int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, int32_t nlayers, uint64_t seed,
                   int64_t t, int32_t r, int64_t* out, int64_t cap, int64_t* count_dev, void* stream);
 int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t first_iter, void* stream);
+/* Where lsmgnn_sample reads the CSR: in_hbm = 0 (default) — the pinned host copy over PCIe
+ * (UVA, the paper's placement P:251); 1 — a copy the library makes in HBM (B200's 180 GB
+ * holds a 100M-node CSR); same lists either way. */
+int lsmgnn_sampler_place(int32_t in_hbm);
 
 /* ---- CUDA-graph step (G = 1): one captured launch per iteration.
  * lsmgnn_graph_capture records ONE step — gather(t) of batch ids_ring[t mod ring_len]

@@ -24,7 +24,8 @@ EXPORTS = ["lsmgnn_bind", "lsmgnn_set_options", "lsmgnn_init", "lsmgnn_attach_st
            "lsmgnn_export_handle", "lsmgnn_connect", "lsmgnn_gather", "lsmgnn_gather_host", "lsmgnn_prefetch",
            "lsmgnn_stats", "lsmgnn_stats_history", "lsmgnn_kernel_launches", "lsmgnn_finalize",
            "lsmgnn_last_error", "lsmgnn_profile", "lsmgnn_profile_read", "lsmgnn_sampler_attach", "lsmgnn_sample",
-           "lsmgnn_prefetch_dev", "lsmgnn_graph_capture", "lsmgnn_graph_replay", "lsmgnn_debug_state"]
+           "lsmgnn_prefetch_dev", "lsmgnn_graph_capture", "lsmgnn_graph_replay", "lsmgnn_debug_state",
+           "lsmgnn_sampler_place"]
 PHASES = ["route", "dedup", "probe_replace", "admit", "fill", "pull", "window", "pvp"]
 
 
@@ -81,6 +82,7 @@ def load_library(path: str = SO_PATH) -> ctypes.CDLL:
         "lsmgnn_graph_capture": ([vp, vp, i32, vp, vp], i32),
         "lsmgnn_graph_replay": ([vp], i32),
         "lsmgnn_debug_state": ([i32, vp, i64], i32),
+        "lsmgnn_sampler_place": ([i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -276,6 +278,10 @@ class Sampler:
         _check(load_library().lsmgnn_sampler_attach(ctypes.c_void_p(self.indptr.data_ptr()),
                                                     ctypes.c_void_p(self.indices.data_ptr()),
                                                     self.indptr.numel() - 1, self.indices.numel()))
+
+    def place(self, in_hbm: bool) -> None:
+        """Read the CSR from HBM (a library-owned copy) or from pinned host memory (UVA)."""
+        _check(_LIB.lsmgnn_sampler_place(1 if in_hbm else 0))
 
     @staticmethod
     def bound(nseeds: int, fanout) -> int:

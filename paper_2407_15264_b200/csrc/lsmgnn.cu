@@ -120,6 +120,11 @@ struct Ctx {
   uint32_t *s_keep = nullptr, *s_pos = nullptr, *s_bsum = nullptr;
   SampCounts* s_counts = nullptr;
   uint32_t s_hi = 0xFFFFFFFFu;
+  const int64_t* s_map_indptr = nullptr;  // device mappings of the host CSR (UVA)
+  const int32_t* s_map_indices = nullptr;
+  int64_t* s_hbm_indptr = nullptr;        // HBM-resident copy (lsmgnn_sampler_place)
+  int32_t* s_hbm_indices = nullptr;
+  int64_t s_nnz = 0;
 
   // phase profiling
   bool prof = false;
@@ -282,7 +287,8 @@ int free_all() {
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  void* sp[] = {g.s_tab, g.s_raw, g.s_layer, g.s_front, g.s_cnt, g.s_off, g.s_keep, g.s_pos, g.s_bsum, g.s_counts};
+  void* sp[] = {g.s_tab,  g.s_raw,    g.s_layer,  g.s_front,        g.s_cnt,          g.s_off,
+                g.s_keep, g.s_pos,    g.s_bsum,   g.s_counts, g.s_hbm_indptr, g.s_hbm_indices};
   for (void* p : sp)
     if (p) cudaFree(p);
   if (g.s_reg_indptr) cudaHostUnregister(const_cast<void*>(g.s_host_indptr));
@@ -955,7 +961,16 @@ int lsmgnn_sampler_attach(const int64_t* indptr, const int32_t* indices, int64_t
     return rc;
   g.s_host_indptr = indptr;
   g.s_host_indices = indices;
+  g.s_map_indptr = g.s_indptr;
+  g.s_map_indices = g.s_indices;
+  g.s_nnz = nnz;
   g.s_N = (uint64_t)num_nodes;
+  if (g.s_hbm_indptr) {
+    cudaFree(g.s_hbm_indptr);
+    cudaFree(g.s_hbm_indices);
+    g.s_hbm_indptr = nullptr;
+    g.s_hbm_indices = nullptr;
+  }
   if (g.s_tab) cudaFree(g.s_tab);
   CK(cudaMalloc(&g.s_tab, g.s_N * sizeof(unsigned long long)));
   CK(cudaMemset(g.s_tab, 0xFF, g.s_N * sizeof(unsigned long long)));
@@ -1032,8 +1047,8 @@ int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, i
     if (int rc = xscan(g.s_cnt, &c->nf, g.s_off, fmax)) return rc;
     k_xscan_total<<<1, 1, 0, st>>>(g.s_off, g.s_cnt, &c->nf, 0, &c->layer_n);
     LAUNCHED();
-    k_samp_draw<<<gr, 256, 0, st>>>(g.s_front, c, g.s_indptr, g.s_indices, f, g.s_off, g.s_layer, seed, (uint64_t)t,
-                                    (uint64_t)r, (uint64_t)l);
+    k_samp_draw<<<grid_for((int64_t)std::max<uint64_t>(fmax, 1) * 32, 256, 8), 256, 0, st>>>(
+        g.s_front, c, g.s_indptr, g.s_indices, f, g.s_off, g.s_layer, seed, (uint64_t)t, (uint64_t)r, (uint64_t)l);
     LAUNCHED();
     k_samp_append<<<grid_for((int64_t)std::max<uint64_t>(lmax, 1), 256, 4), 256, 0, st>>>(g.s_layer, c, g.s_raw);
     LAUNCHED();
@@ -1046,6 +1061,27 @@ int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, i
   if (int rc = unique_first(g.s_raw, &c->nraw, bound, out, &c->nout)) return rc;
   k_samp_out_count<<<1, 1, 0, st>>>(c, count_dev);
   LAUNCHED();
+  return 0;
+}
+
+// Where the sampler reads the CSR: in_hbm = 0 — pinned host memory over PCIe (UVA, the
+// paper's placement); 1 — a copy in HBM (B200's 180 GB holds a 100M-node CSR).
+int lsmgnn_sampler_place(int32_t in_hbm) {
+  if (!g.s_tab) return set_err(LSMGNN_ESTATE, "sampler_attach first");
+  if (in_hbm) {
+    if (!g.s_hbm_indptr) {
+      CK(cudaMalloc(&g.s_hbm_indptr, (g.s_N + 1) * sizeof(int64_t)));
+      CK(cudaMalloc(&g.s_hbm_indices, std::max<int64_t>(g.s_nnz, 1) * sizeof(int32_t)));
+      CK(cudaMemcpy(g.s_hbm_indptr, g.s_host_indptr, (g.s_N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(g.s_hbm_indices, g.s_host_indices, std::max<int64_t>(g.s_nnz, 1) * sizeof(int32_t),
+                    cudaMemcpyHostToDevice));
+    }
+    g.s_indptr = g.s_hbm_indptr;
+    g.s_indices = g.s_hbm_indices;
+  } else {
+    g.s_indptr = g.s_map_indptr;
+    g.s_indices = g.s_map_indices;
+  }
   return 0;
 }
 

@@ -53,19 +53,23 @@ __global__ void k_samp_count(const uint32_t* __restrict__ frontier, const SampCo
 __global__ void k_samp_draw(const uint32_t* __restrict__ frontier, const SampCounts* c, const int64_t* indptr,
                             const int32_t* indices, uint32_t f, const uint32_t* __restrict__ off,
                             uint32_t* __restrict__ layer, uint64_t seed, uint64_t t, uint64_t r, uint64_t l) {
+  // warp per frontier node, lane per draw: every neighbour read of a node is in flight at once
+  // (the reads are latency-bound when the CSR is in host memory)
   const uint32_t nf = c->nf;
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nf; p += gridDim.x * blockDim.x) {
+  const uint32_t lane = lane_id();
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < nf; p += nw) {
     const uint32_t x = frontier[p];
     const int64_t b = indptr[x], deg = indptr[x + 1] - b;
     uint32_t* dst = layer + off[p];
     if (deg <= (int64_t)f) {
-      for (int64_t j = 0; j < deg; ++j) dst[j] = (uint32_t)indices[b + j];
+      for (int64_t j = lane; j < deg; j += 32) dst[j] = (uint32_t)indices[b + j];
     } else {
       uint64_t hp = splitmix64_dev(t ^ seed);
       hp = splitmix64_dev(r ^ hp);
       hp = splitmix64_dev(l ^ hp);
       hp = splitmix64_dev((uint64_t)p ^ hp);
-      for (uint32_t j = 0; j < f; ++j) {
+      for (uint32_t j = lane; j < f; j += 32) {
         const uint64_t h = splitmix64_dev((uint64_t)j ^ hp);
         const double u = __dmul_rn((double)(h >> 11), 1.0 / 9007199254740992.0);
         const int64_t pos = (int64_t)__dmul_rn(u, (double)deg);

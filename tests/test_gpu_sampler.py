@@ -18,12 +18,14 @@ def graph1m():
     return synth.plcite(1_000_000, 12)
 
 
-@pytest.mark.parametrize("fanout", [(10, 5, 5), (5, 2, 2, 2), (25, 10), ()])
-def test_sampler_parity(graph1m, fanout):
+@pytest.mark.parametrize("in_hbm", [False, True])
+@pytest.mark.parametrize("fanout", [(10, 5, 5), (5, 2, 2, 2), (25, 10), (40,), ()])
+def test_sampler_parity(graph1m, fanout, in_hbm):
     import torch
     from paper_2407_15264_b200 import Sampler
     g = graph1m
     s = Sampler(g.indptr, g.indices)
+    s.place(in_hbm)  # CSR read over PCIe (UVA) or from an HBM copy: same lists
     perm = synth.epoch_seeds(g.num_nodes, 0)
     for t in range(3):
         for r in range(2):
