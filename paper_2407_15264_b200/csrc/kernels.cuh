@@ -35,6 +35,8 @@ struct BeginArgs {
   uint32_t ring_len;
   uint32_t Wp1, period, L, C;
   uint32_t* inbox_cnt;             // zeroed (G = 1), may be null
+  int64_t cap;                     // max_batch_ids: a longer device-resident batch is clamped ...
+  volatile uint32_t* overflow;     // ... and flagged here (pinned host word, sticky EINVAL)
 };
 __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, BeginArgs a) {
   const uint64_t t = a.t_host >= 0 ? (uint64_t)a.t_host : it->t_next;
@@ -51,6 +53,10 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
       const uint32_t k = (uint32_t)(t % a.ring_len);
       it->ids = a.ids_ring[k];
       it->n = a.n_ring[k];
+      if (it->n > a.cap || it->n < 0) {
+        it->n = it->n < 0 ? 0 : a.cap;
+        *a.overflow = 1u;
+      }
     }
     it->stamp = (uint32_t)(t + 1);
     it->p0 = (uint32_t)((t + 1) % a.Wp1);
@@ -104,7 +110,7 @@ __global__ void k_end(IterState* it, unsigned long long* hist, unsigned long lon
 // replay) wk = it->wk_next with the batch from the ring.
 __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host,
                             const int64_t* n_dev, const int64_t* const* ids_ring, const int64_t* n_ring,
-                            uint32_t ring_len, uint32_t Wp1) {
+                            uint32_t ring_len, uint32_t Wp1, int64_t cap, volatile uint32_t* overflow) {
   if (threadIdx.x != 0) return;
   const uint64_t k = k_host >= 0 ? (uint64_t)k_host : it->wk_next;
   it->wk = k;
@@ -116,6 +122,10 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
     const uint32_t j = (uint32_t)(k % ring_len);
     it->wids = ids_ring[j];
     it->wn = n_ring[j];
+  }
+  if (it->wn > cap || it->wn < 0) {  // a device-resident length beyond max_batch_ids
+    it->wn = it->wn < 0 ? 0 : cap;
+    *overflow = 1u;
   }
   it->wk_next = k + 1;
 }

@@ -91,7 +91,8 @@ struct Ctx {
   const uint8_t* table_host = nullptr;
   const uint8_t* table_dev = nullptr;
   bool table_registered = false;
-  volatile uint32_t* bad_host = nullptr;  // pinned mirror of scr->bad_ids
+  volatile uint32_t* bad_host = nullptr;  // pinned mirror: [0] scr->bad_ids, [1] batch-length overflow
+  uint32_t* bad_dev_overflow = nullptr;   // device mapping of bad_host + 1
   uint32_t* bad_dev = nullptr;
 
   // streams / events
@@ -196,6 +197,10 @@ int grid_for(int64_t work, int threads, int per_sm = 8) {
 }
 
 int check_sticky() {
+  if (g.bad_host && g.bad_host[1]) {
+    g.sticky = LSMGNN_EINVAL;
+    return set_err(g.sticky, "a device-resident batch length exceeded max_batch_ids (sticky; clamped)");
+  }
   if (g.bad_host && *g.bad_host) g.sticky = LSMGNN_ERANGE;
   if (g.sticky) return set_err(g.sticky, "a node id >= num_nodes was passed (sticky)");
   return 0;
@@ -350,6 +355,8 @@ BeginArgs begin_args(int64_t t_host, const int64_t* ids, int64_t n, const int64_
   a.L = (uint32_t)g.stage_base0;
   a.C = (uint32_t)g.C;
   a.inbox_cnt = g.world == 1 ? g.local_inbox_cnt : nullptr;
+  a.cap = (int64_t)g.cap;
+  a.overflow = g.bad_dev_overflow;
   return a;
 }
 
@@ -517,7 +524,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
 int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* n_dev, const int64_t* const* ids_ring,
                   const int64_t* n_ring, uint32_t ring_len, int64_t n_bound, cudaStream_t st) {
   const int G = g.world;
-  k_win_begin<<<1, 32, 0, st>>>(g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1);
+  k_win_begin<<<1, 32, 0, st>>>(g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1,
+                                (int64_t)g.cap, g.bad_dev_overflow);
   LAUNCHED();
   const uint64_t stride = g.cap * G;
   // drop the bits of the iteration that last used this slot (k - (W+1)), then empty the slot
@@ -749,6 +757,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     std::memset(hb, 0, 64);
     g.bad_host = reinterpret_cast<volatile uint32_t*>(hb);
     CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&g.bad_dev), hb, 0));
+    g.bad_dev_overflow = g.bad_dev + 1;
   }
   CK(cudaStreamCreateWithFlags(&g.side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&g.ev_main, cudaEventDisableTiming));

@@ -112,6 +112,22 @@ def test_bad_ids_sticky_erange():
     c.close()
 
 
+def test_device_count_overflow_sticky():
+    """A device-resident batch length beyond max_batch_ids (lsmgnn_prefetch_dev / graph ring)
+    is clamped on the device — no out-of-bounds write — and reported as a sticky EINVAL."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn, LsmGnnError, prefetch_dev
+    from .harness import table_for
+    c = LsmGnn(100, 4, 16, 4, 0, None, window=2, max_batch_ids=8)
+    c.attach_storage(table_for(100, 4, pinned=True))
+    ids = torch.arange(20, dtype=torch.int64, device="cuda")
+    prefetch_dev(ids, torch.tensor([20], dtype=torch.int64, device="cuda"), first_iter=1)
+    torch.cuda.synchronize()
+    with pytest.raises(LsmGnnError):
+        c.stats()
+    c.close()
+
+
 def test_abi_errors():
     from paper_2407_15264_b200 import LsmGnn, LsmGnnError
     with pytest.raises(LsmGnnError):
