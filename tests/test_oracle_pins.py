@@ -345,3 +345,41 @@ def test_update_period_never_reduces_to_static(seed):
     # all lines Fresh: nothing carries reuse information, so PVP admits nothing
     c = run_trace(Oracle(1, N, 16, S * A, A, sc, policy="hybrid", pvp=1, W=6, V=60, P=1000), trace)
     assert tot(c, "victim_admitted") == 0 and tot(c, "evict_fresh") == tot(c, "evictions")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_admission_order_on_overflow(seed):
+    """R14 (P:408-409 leaves the order to the atomic race): when more victims with the same
+    reuse iteration arrive than their queue has room for, the ones with the smallest node IDs
+    are admitted — checked by brute force from the eviction log of each batch."""
+    rng = np.random.default_rng(seed)
+    A, S, W = 4, 4, 6
+    N, C = 400, 2
+    o = Oracle(1, N, 16, S * A, A, rng.integers(0, 256, N).astype(np.uint8), policy="hybrid", pvp=1, W=W,
+               V=C * W)
+    trace = [[rng.integers(0, N, 40)] for _ in range(30)]
+    K = len(trace)
+    empty = [np.zeros(0, np.int64)]
+    for k in range(1, W + 1):
+        o.feed(k, trace[k] if k < K else empty)
+    overflowed = 0
+    for t in range(K):
+        before = {k: set(o.queue(0, k)[0].tolist()) for k in range(W)}
+        c, _ = o.gather(t, trace[t])
+        ev = o.events()
+        evicted = [int(r[3]) for r in ev if r[2] == 0]
+        # candidates: evicted lines that carried a reuse iteration (next use at decision time)
+        cands = {}
+        for x in evicted:
+            nx = o.next_use(x, t)
+            if nx >= 0:
+                cands.setdefault(nx % W, []).append(x)
+        for k, xs in cands.items():
+            room = C - len(before[k])
+            admitted = set(o.queue(0, k)[0].tolist()) - before[k]
+            want = set(sorted(xs)[:max(0, room)])
+            assert admitted == want, (t, k, sorted(xs), room, admitted)
+            overflowed += len(xs) > room
+        o.pvp_prefetch(t)
+        o.feed(t + 1 + W, trace[t + 1 + W] if t + 1 + W < K else empty)
+    assert overflowed > 0
