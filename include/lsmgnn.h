@@ -177,8 +177,10 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
  *   int64[cap] with cap >= nseeds * (1 + f0 + f0 f1 + ...) (the bound); the list length is
  *   written to count_dev (device int64) — nothing synchronises. Stream-ordered on `stream`.
  * lsmgnn_prefetch_dev: window feed of ONE batch (device int64 ids, device int64 count) for
- *   iteration first_iter — lsmgnn_prefetch semantics for G = 1 without reading the count on
- *   the host; issue the PVP copy with lsmgnn_prefetch(NULL, NULL, 0, 0, stream). */
+ *   iteration first_iter — lsmgnn_prefetch semantics (any G: with G > 1 every rank calls it
+ *   for the same first_iter, its own batch routed to the homes like lsmgnn_prefetch's)
+ *   without reading the count on the host; issue the PVP copy with
+ *   lsmgnn_prefetch(NULL, NULL, 0, 0, stream). */
 int lsmgnn_sampler_attach(const int64_t* indptr, const int32_t* indices, int64_t num_nodes, int64_t nnz);
 int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, int32_t nlayers, uint64_t seed,
                   int64_t t, int32_t r, int64_t* out, int64_t cap, int64_t* count_dev, void* stream);

@@ -307,6 +307,6 @@ class Sampler:
 
 
 def prefetch_dev(ids, count, first_iter: int, stream=None) -> None:
-    """Window feed of one device-resident batch (G = 1)."""
+    """Window feed of one device-resident batch (any G; with G > 1 every rank calls it for the same first_iter)."""
     _check(_LIB.lsmgnn_prefetch_dev(ctypes.c_void_p(ids.data_ptr()), ctypes.c_void_p(count.data_ptr()), int(first_iter),
                                     ctypes.c_void_p(_stream_ptr(stream))))

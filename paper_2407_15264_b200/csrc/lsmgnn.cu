@@ -1095,10 +1095,10 @@ int lsmgnn_sampler_place(int32_t in_hbm) {
 }
 
 // Window feed of one batch whose length lives on the device (e.g. straight from
-// lsmgnn_sample): same semantics as lsmgnn_prefetch with num_batches = 1 (G = 1).
+// lsmgnn_sample): same semantics as lsmgnn_prefetch with num_batches = 1. With G > 1 the
+// route kernel reads the length from IterState (k_win_begin), so no rank needs it on the host.
 int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t first_iter, void* stream) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
-  if (g.world != 1) return set_err(LSMGNN_EINVAL, "prefetch_dev is single-home only");
   if (!count_dev) return set_err(LSMGNN_EINVAL, "null count");
   if (first_iter != g.feed_next) return set_err(LSMGNN_ESTATE, "window iteration out of order");
   if (first_iter > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");

@@ -84,6 +84,50 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         return
+    if mode == "sampler":  # NEXT N3 at G > 1: each rank's GPU sampler feeds the shared window
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+        import synth
+        from paper_2407_15264_b200 import LsmGnn, Sampler, prefetch_dev
+        from tests.harness import table_for
+        pvp = int(sys.argv[3])
+        N, D, W, K, B, fan = 16384, 128, 8, 20, 256, (10, 5)
+        g = synth.plcite(N, 8)
+        perm = synth.epoch_seeds(N, 0)
+        bound = Sampler.bound(B, fan)
+        c = LsmGnn(N, D, 1024, 8, 512, synth.static_scores(g), policy="hybrid", pvp=pvp, window=W,
+                   max_batch_ids=bound, rank=rank, world=world, group=dist.group.WORLD)
+        c.attach_storage(table_for(N, D, pinned=True, home=rank, G=world))
+        s = Sampler(g.indptr, g.indices)
+        lists = {}
+
+        def sampled(k):  # batch k of this rank: seeds slot (k, rank) of the epoch permutation
+            if k not in lists:
+                if k < K:
+                    sd = torch.from_numpy(perm[(k * world + rank) * B:(k * world + rank + 1) * B]).cuda()
+                    lists[k] = s.sample(sd, fan, 4, k, rank)
+                else:
+                    lists[k] = (torch.zeros(1, dtype=torch.int64, device="cuda"),
+                                torch.zeros(1, dtype=torch.int64, device="cuda"))
+            return lists[k]
+
+        for k in range(1, W + 1):
+            prefetch_dev(*sampled(k), first_iter=k)
+        out = torch.empty((bound, 4 * D), dtype=torch.uint8, device="cuda")
+        bad = 0
+        for t in range(K):
+            ids, cnt = sampled(t)
+            n = int(cnt.item())
+            c.gather(ids[:n], out)
+            prefetch_dev(*sampled(t + 1 + W), first_iter=t + 1 + W)
+            c.prefetch([], first_iter=0)
+            rows = out[:n].cpu().numpy().view(np.uint32).reshape(n, D)
+            bad += synth.check_rows(rows, ids[:n].cpu().numpy(), D)[0]
+        torch.cuda.synchronize()
+        np.save(os.path.join(outdir, f"hist{rank}.npy"), c.history(0, K))
+        json.dump({"rank": rank, "bad": int(bad)}, open(os.path.join(outdir, f"r{rank}.json"), "w"))
+        c.close()
+        dist.destroy_process_group()
+        return
     policy = sys.argv[3] if len(sys.argv) > 3 else "hybrid"
     pvp = int(sys.argv[4]) if len(sys.argv) > 4 else 1
     ndev = torch.cuda.device_count()

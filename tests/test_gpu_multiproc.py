@@ -125,3 +125,24 @@ def test_multiprocess_parity(tmp_path, G, policy, pvp):
         for f in range(hg.shape[1]):
             if f not in skip:
                 assert np.array_equal(hg[:, f], h1[:, f].astype(np.int64)), f
+
+
+@pytest.mark.parametrize("G,pvp", [(2, 1), (3, 0)])
+def test_multiprocess_gpu_sampler_window(tmp_path, G, pvp):
+    """NEXT N3 at G > 1: every rank samples its own batches on the GPU and feeds the shared
+    window with lsmgnn_prefetch_dev (the length never leaves the device); per-home counters
+    equal the oracle's G-home run over the sampler oracle's lists, rows equal F(v)."""
+    import oracle
+    launch(G, tmp_path, "sampler", str(tmp_path), str(pvp))
+    N, D, W, K, B, fan = 16384, 128, 8, 20, 256, (10, 5)
+    g = synth.plcite(N, 8)
+    perm = synth.epoch_seeds(N, 0)
+    tr = [[oracle.sample_batch(g.indptr, g.indices, perm[(t * G + r) * B:(t * G + r + 1) * B], fan, 4, t, r)
+           for r in range(G)] for t in range(K)]
+    ho = run_oracle(tr, G=G, N=N, D=D, L=1024, A=8, scores=synth.static_scores(g), policy="hybrid", pvp=pvp, W=W,
+                    V=512)
+    for r in range(G):
+        assert json.load(open(tmp_path / f"r{r}.json"))["bad"] == 0
+        hg = np.load(tmp_path / f"hist{r}.npy")
+        assert np.array_equal(hg, ho[:, r, :]), (r, np.argwhere(hg != ho[:, r, :])[:3])
+    assert ho[:, :, 2].sum() > 0
