@@ -137,6 +137,7 @@ struct Ctx {
   // driver entry points (stream memory operations)
   PFN_cuStreamWaitValue32_v2 waitv = nullptr;
   PFN_cuStreamWriteValue32_v2 writev = nullptr;
+  PFN_cuStreamBatchMemOp_v2 batchv = nullptr;  // optional: G flag operations per submission
 };
 
 Ctx g;
@@ -217,6 +218,48 @@ int flag_wait(cudaStream_t st, uint32_t* addr, uint32_t value) {
   if (r != CUDA_SUCCESS) return set_err(LSMGNN_ECOMM, "cuStreamWaitValue32 failed (%d)", (int)r);
   return 0;
 }
+// The G flag operations of one protocol step in ONE stream memory-op batch (one front-end
+// submission instead of G; executed in array order, each write fenced like a single
+// cuStreamWriteValue32): wait until base[h] >= value for every home h (local words), or write
+// `value` into word `word` of every rank's flag block (peer-mapped).
+int flags_wait_all(cudaStream_t st, uint32_t* base, uint32_t value) {
+  const int G = g.world;
+  if (!g.batchv) {
+    for (int h = 0; h < G; ++h)
+      if (int rc = flag_wait(st, base + h, value)) return rc;
+    return 0;
+  }
+  CUstreamBatchMemOpParams ops[kMaxG];
+  std::memset(ops, 0, sizeof(ops));
+  for (int h = 0; h < G; ++h) {
+    ops[h].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+    ops[h].waitValue.address = (CUdeviceptr)(base + h);
+    ops[h].waitValue.value = value;
+    ops[h].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+  }
+  CUresult r = g.batchv(st, (unsigned)G, ops, 0);
+  if (r != CUDA_SUCCESS) return set_err(LSMGNN_ECOMM, "cuStreamBatchMemOp(wait) failed (%d)", (int)r);
+  return 0;
+}
+int flags_write_all(cudaStream_t st, uint32_t word, uint32_t value) {
+  const int G = g.world;
+  if (!g.batchv) {
+    for (int r = 0; r < G; ++r)
+      if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[word], value)) return rc;
+    return 0;
+  }
+  CUstreamBatchMemOpParams ops[kMaxG];
+  std::memset(ops, 0, sizeof(ops));
+  for (int r = 0; r < G; ++r) {
+    ops[r].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    ops[r].writeValue.address = (CUdeviceptr)&flags_of(g.peer_arena[r])[word];
+    ops[r].writeValue.value = value;
+    ops[r].writeValue.flags = 0;  // default: fenced after the stream's prior work
+  }
+  CUresult r = g.batchv(st, (unsigned)G, ops, 0);
+  if (r != CUDA_SUCCESS) return set_err(LSMGNN_ECOMM, "cuStreamBatchMemOp(write) failed (%d)", (int)r);
+  return 0;
+}
 
 // Route `n` int64 IDs of this requester to the homes' inboxes (gather: win=false) and run the
 // flag exchange so that, on return (stream order), every home's inbox for this round is full.
@@ -224,8 +267,7 @@ int exchange_ids(int64_t n_bound, bool win, uint32_t seq, cudaStream_t st) {
   const int G = g.world;
   uint32_t* myflags = flags_of(g.arena);
   if (win) {  // the homes must have consumed the previous window round
-    for (int h = 0; h < G; ++h)
-      if (int rc = flag_wait(st, &myflags[3 * G + h], seq - 1)) return rc;
+    if (int rc = flags_wait_all(st, &myflags[3 * G], seq - 1)) return rc;
   }
   CK(cudaMemsetAsync(g.route_cnt, 0, sizeof(uint32_t) * G, st));
   RouteArgs ra{};
@@ -246,10 +288,8 @@ int exchange_ids(int64_t n_bound, bool win, uint32_t seq, cudaStream_t st) {
   k_route_publish<<<1, 32, 0, st>>>(g.route_cnt, pa);
   LAUNCHED();
   const int slot = win ? 2 : 0;
-  for (int h = 0; h < G; ++h)
-    if (int rc = flag_write(st, &flags_of(g.peer_arena[h])[slot * G + g.rank], seq)) return rc;
-  for (int r = 0; r < G; ++r)
-    if (int rc = flag_wait(st, &myflags[slot * G + r], seq)) return rc;
+  if (int rc = flags_write_all(st, (uint32_t)(slot * G + g.rank), seq)) return rc;
+  if (int rc = flags_wait_all(st, &myflags[slot * G], seq)) return rc;
   return 0;
 }
 
@@ -494,10 +534,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     prof_end(4, st);
     // homes signal "served", requesters wait for every home, then pull
     prof_begin(5, st);
-    for (int r = 0; r < G; ++r)
-      if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[G + g.rank], stamp_host)) return rc;
-    for (int h = 0; h < G; ++h)
-      if (int rc = flag_wait(st, &flags_of(g.arena)[G + h], stamp_host)) return rc;
+    if (int rc = flags_write_all(st, (uint32_t)(G + g.rank), stamp_host)) return rc;
+    if (int rc = flags_wait_all(st, &flags_of(g.arena)[G], stamp_host)) return rc;
     if (n_bound > 0) {
       PullArgs pa{};
       for (int h = 0; h < G; ++h) {
@@ -543,8 +581,8 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
     k_win_gather<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(win_of(g.arena), wcnt_of(g.arena), (uint32_t)G,
                                                                     (uint32_t)g.cap, g.ring, stride, g.ring_len, g.it);
     LAUNCHED();
-    for (int r = 0; r < G; ++r)  // window inbox consumed
-      if (int rc = flag_write(st, &flags_of(g.peer_arena[r])[3 * G + g.rank], seq)) return rc;
+    // window inbox consumed
+    if (int rc = flags_write_all(st, (uint32_t)(3 * G + g.rank), seq)) return rc;
   }
   k_mask_set<<<grid_for((int64_t)stride, 256, 2), 256, 0, st>>>(g.ring, stride, g.ring_len, g.it, (uint32_t)G, g.MW,
                                                                  g.mask);
@@ -769,6 +807,14 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     CK(cudaGetDriverEntryPoint("cuStreamWriteValue32", reinterpret_cast<void**>(&g.writev), cudaEnableDefault, &q2));
     if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !g.waitv || !g.writev)
       return set_err(LSMGNN_ECOMM, "stream memory operations unavailable");
+    cudaDriverEntryPointQueryResult q3;
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", reinterpret_cast<void**>(&g.batchv), cudaEnableDefault, &q3) !=
+            cudaSuccess ||
+        q3 != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      g.batchv = nullptr;  // single operations instead
+    }
+    if (std::getenv("LSMGNN_NO_BATCH_MEMOP")) g.batchv = nullptr;
   }
   CK(cudaDeviceSynchronize());
   g.inited = true;
