@@ -387,7 +387,10 @@ def main():
                 "sm_path_ceiling_source": "profiles/r01_pcie_microbench.txt (tools/pcie_microbench.cu)"}
         phases["fill"]["pcie_h2d_GBps"] = round(ach, 2)
         phases["fill"]["frac_pcie"] = round(ach / pcie_peak, 4)
-    if pull_ms > 0:
+    if G == 1 and "pull" in phases:  # k_serve delivers every request inside the fill phase
+        phases["pull"]["note"] = ("G = 1: delivery to out is fused into k_serve (fill phase); this span is empty "
+                                  "(event overhead only), so no bandwidth is derived from it")
+    elif pull_ms > 0:
         ach = pull_bytes / (pull_ms / 1e3) / 1e9
         phases["pull"]["hbm_GBps"] = round(ach, 1)
         phases["pull"]["frac_hbm"] = round(ach / hbm_peak, 4)
