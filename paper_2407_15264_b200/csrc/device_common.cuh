@@ -50,7 +50,8 @@ struct Scratch {
   uint32_t nreq;       // requests routed to this home
   uint32_t staged[2];  // rows the PVP staged, by iteration parity
   uint32_t pvp_done;   // grid-completion counter of the PVP kernel
-  uint32_t pad[7];
+  uint32_t pull_next;  // k_serve: next request index handed to a delivering warp
+  uint32_t pad[6];
 };
 
 // Per-iteration values, resident on the device. k_begin / k_win_begin write them (from host

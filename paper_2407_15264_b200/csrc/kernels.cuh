@@ -71,6 +71,7 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
     scr->ncand = 0;
     scr->nbypass = 0;
     scr->nreq = 0;
+    scr->pull_next = 0;
     if (a.inbox_cnt) *a.inbox_cnt = 0;
   }
 }
@@ -860,14 +861,18 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
 // table (PCIe) or PVP staging into registers once and store it to its cache slot / bypass
 // row AND to every requester position of that node (the request list built by k_dedup) —
 // the storage read and the delivery overlap, and the row is never re-read from HBM. The
-// remaining warps (1 in 8) copy rows not delivered by a fill (hits, staged rows served in
-// place) from HBM into `out`, concurrently with the PCIe-bound fills.
+// remaining warps (1 in 8) start copying the rows not delivered by a fill (hits, staged rows
+// served in place) from HBM into `out`, concurrently with the PCIe-bound fills; fill warps
+// join them once the fills are handed out. Delivery work is taken in chunks of requests from
+// a shared counter, so a hit-dominated batch gets the whole grid and a miss-dominated one
+// keeps 7/8 of it on the fills.
 template <int UNROLL, int OUT>
-__global__ void k_serve(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
+__global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* __restrict__ pool,
                         const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
                         const unsigned long long* __restrict__ head, const uint32_t* __restrict__ nxt,
                         const uint32_t* __restrict__ inbox_i, const IterState* it, uint64_t N,
                         const uint32_t* __restrict__ node_loc, uint4* __restrict__ out) {
+  constexpr uint32_t kChunk = 16;
   const uint32_t stamp = it->stamp;
   const int64_t* __restrict__ ids = it->ids;
   const int64_t n = it->n;
@@ -875,8 +880,47 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, const Scratch* scr, u
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t npull = nw >= 8 ? nw / 8 : 1;
   const int lane = (int)lane_id();
-  if (gw < npull) {  // ---- pull warps: rows not delivered by a fill
-    for (int64_t i = gw; i < n; i += npull) {
+  if (gw >= npull) {  // ---- fill warps
+    const uint32_t nf = scr->nfill;
+    for (uint32_t e = gw - npull; e < nf; e += nw - npull) {
+      const FillEnt f = fills[e];
+      uint4* slot = pool + (size_t)f.dst * nvec;
+      if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, slot, nvec);
+      const bool from_host = (f.src & kHostBit) != 0;
+      const uint4* src = from_host ? table + (size_t)(f.src & ~kHostBit) * nvec : pool + (size_t)f.src * nvec;
+      const unsigned long long h = head[f.node];
+      const uint32_t first = (uint32_t)(h >> 32) == stamp ? (uint32_t)h : kInvalid;
+      for (uint32_t base = 0; base < nvec; base += 32 * UNROLL) {
+        uint4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const uint32_t k = base + lane + 32 * u;
+          if (k < nvec) v[u] = from_host ? ld16<kHost>(src + k) : ld16<kDev>(src + k);
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const uint32_t k = base + lane + 32 * u;
+          if (k < nvec) st16<kDev>(slot + k, v[u]);
+        }
+        for (uint32_t pos = first; pos != kInvalid; pos = nxt[pos]) {
+          uint4* dst = out + (size_t)inbox_i[pos] * nvec;
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            const uint32_t k = base + lane + 32 * u;
+            if (k < nvec) st16<OUT>(dst + k, v[u]);
+          }
+        }
+      }
+    }
+  }
+  // ---- delivery of the rows no fill delivers, in chunks from the shared counter
+  for (;;) {
+    uint32_t c0 = 0;
+    if (lane == 0) c0 = atomicAdd(&scr->pull_next, kChunk);
+    c0 = __shfl_sync(0xffffffffu, c0, 0);
+    if ((int64_t)c0 >= n) break;
+    const int64_t c1 = min((int64_t)c0 + kChunk, n);
+    for (int64_t i = c0; i < c1; ++i) {
       const int64_t x = ids[i];
       uint4* dst = out + (size_t)i * nvec;
       if (x < 0 || (uint64_t)x >= N) {
@@ -886,38 +930,6 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, const Scratch* scr, u
       const uint32_t loc = node_loc[(uint32_t)x];
       if (loc & kDelivered) continue;
       warp_copy_row<UNROLL, kDev, OUT>(dst, pool + (size_t)loc * nvec, nvec);
-    }
-    return;
-  }
-  const uint32_t nf = scr->nfill;
-  for (uint32_t e = gw - npull; e < nf; e += nw - npull) {
-    const FillEnt f = fills[e];
-    uint4* slot = pool + (size_t)f.dst * nvec;
-    if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, slot, nvec);
-    const bool from_host = (f.src & kHostBit) != 0;
-    const uint4* src = from_host ? table + (size_t)(f.src & ~kHostBit) * nvec : pool + (size_t)f.src * nvec;
-    const unsigned long long h = head[f.node];
-    const uint32_t first = (uint32_t)(h >> 32) == stamp ? (uint32_t)h : kInvalid;
-    for (uint32_t base = 0; base < nvec; base += 32 * UNROLL) {
-      uint4 v[UNROLL];
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const uint32_t k = base + lane + 32 * u;
-        if (k < nvec) v[u] = from_host ? ld16<kHost>(src + k) : ld16<kDev>(src + k);
-      }
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const uint32_t k = base + lane + 32 * u;
-        if (k < nvec) st16<kDev>(slot + k, v[u]);
-      }
-      for (uint32_t pos = first; pos != kInvalid; pos = nxt[pos]) {
-        uint4* dst = out + (size_t)inbox_i[pos] * nvec;
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          const uint32_t k = base + lane + 32 * u;
-          if (k < nvec) st16<OUT>(dst + k, v[u]);
-        }
-      }
     }
   }
 }
