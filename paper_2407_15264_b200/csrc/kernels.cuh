@@ -15,7 +15,7 @@
 //                       to every requester; 1 warp in 8 copies the hits
 //   k_fill         S6  G > 1: victim row D2H then new row -> slot / bypass staging
 //   k_pull         S7+S8 G > 1: location lookup at the home + row copy (local or peer HBM)
-//   k_win_begin, k_mask_clear, k_mask_set, k_win_gather  S10  window feed (reuse bitmask)
+//   k_win_begin, k_mask_clear, k_win_gather (+ k_route_local)  S10  window feed (reuse bitmask)
 //   k_pvp          S11 PVP copy of victim queue (t+1) mod W into home staging (side stream)
 #pragma once
 #include "device_common.cuh"
@@ -134,9 +134,10 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
 // ------------------------------------------------------------------------------ S1 (G = 1)
 // Validate the caller's int64 IDs and write them (u32) into this home's inbox (gather) or a
 // window ring slot (prefetch): ids/n = it->ids/n or it->wids/wn; output slot = *slot_ptr.
+// With `mask` (window feed), each stored node also sets its reuse bit of the slot (S10).
 __global__ void k_route_local(const IterState* it, uint32_t window, uint64_t N, uint32_t* __restrict__ out_base,
                               uint64_t out_stride, uint32_t* __restrict__ cnt_base, Scratch* scr,
-                              uint32_t* __restrict__ inbox_i) {
+                              uint32_t* __restrict__ inbox_i, uint32_t* __restrict__ mask, uint32_t MW) {
   const int64_t* __restrict__ ids = window ? it->wids : it->ids;
   const int64_t n = window ? it->wn : it->n;
   const uint32_t slot = window ? it->wslot : 0u;
@@ -157,6 +158,7 @@ __global__ void k_route_local(const IterState* it, uint32_t window, uint64_t N, 
     if (ok) {
       inbox[pos] = v;
       if (inbox_i) inbox_i[pos] = (uint32_t)i;
+      if (mask) atomicOr(&mask[(size_t)v * MW + (slot >> 5)], 1u << (slot & 31));  // G = 1: q = v
     }
   }
 }
@@ -288,36 +290,55 @@ __device__ __forceinline__ uint32_t pow2_at_least_32(uint32_t m) {
 // Exclusive scan of set_cnt[0..S) into set_off[0..S] by one CTA (1024 threads). With poff,
 // also the offsets of the global scratch of the sets too large for k_set's shared memory
 // (bucket > big_P): each gets a power-of-two region. The same CTA counts staged PVP rows
-// that this batch did not request (pvp_unused).
+// that this batch did not request (pvp_unused). Tiles of 4096 counts move through shared
+// memory (coalesced loads and stores; each thread scans 4 contiguous counts, skewed against
+// bank conflicts), one block-wide scan per tile carries the running total.
+constexpr uint32_t kScanTile = 4096;
+__device__ __forceinline__ uint32_t scan_skew(uint32_t j) { return j + (j >> 5); }
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off,
                                                uint32_t n, const uint32_t* __restrict__ stg_base, uint32_t C,
                                                const Scratch* scr, const uint32_t* __restrict__ mark,
                                                const IterState* it, uint32_t G, unsigned long long* hist,
                                                uint32_t* __restrict__ poff, uint32_t big_P) {
   __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_c[kScanTile + kScanTile / 32];
+  __shared__ uint32_t s_p[kScanTile + kScanTile / 32];
   const uint32_t tid = threadIdx.x;
-  const uint32_t per = (n + 1023) / 1024;
-  const uint32_t lo = tid * per, hi = min(n, lo + per);
-  uint32_t sum = 0, psum = 0;
-  for (uint32_t i = lo; i < hi; ++i) {
-    const uint32_t m = cnt[i];
-    sum += m;
-    if (m > big_P) psum += pow2_at_least_32(m);
-  }
-  uint32_t run = block_exclusive_1024(sum, s_warp);
-  for (uint32_t i = lo; i < hi; ++i) {
-    off[i] = run;
-    run += cnt[i];
-  }
-  if (tid == 1023) off[n] = run;
-  if (poff) {
-    uint32_t prun = block_exclusive_1024(psum, s_warp);
-    for (uint32_t i = lo; i < hi; ++i) {
-      const uint32_t m = cnt[i];
-      poff[i] = prun;
-      if (m > big_P) prun += pow2_at_least_32(m);
+  uint32_t carry = 0, pcarry = 0;
+  for (uint32_t base = 0; base < n; base += kScanTile) {
+    for (uint32_t j = tid; j < kScanTile; j += 1024) s_c[scan_skew(j)] = base + j < n ? cnt[base + j] : 0u;
+    __syncthreads();
+    uint32_t v[4], sum = 0, psum = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = s_c[scan_skew(tid * 4 + k)];
+      sum += v[k];
+      if (v[k] > big_P) psum += pow2_at_least_32(v[k]);
     }
+    uint32_t run = block_exclusive_1024(sum, s_warp) + carry;
+    carry += s_warp[31];
+    if (poff) {
+      uint32_t prun = block_exclusive_1024(psum, s_warp) + pcarry;
+      pcarry += s_warp[31];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        s_p[scan_skew(tid * 4 + k)] = prun;
+        if (v[k] > big_P) prun += pow2_at_least_32(v[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      s_c[scan_skew(tid * 4 + k)] = run;
+      run += v[k];
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < kScanTile && base + j < n; j += 1024) {
+      off[base + j] = s_c[scan_skew(j)];
+      if (poff) poff[base + j] = s_p[scan_skew(j)];
+    }
+    __syncthreads();
   }
+  if (tid == 0) off[n] = carry;
   // pvp_unused: staged rows whose node this batch did not request
   if (stg_base) {
     const uint32_t par = it->par, stamp = it->stamp;
@@ -490,17 +511,6 @@ __global__ void k_set(SetParams p) {
       lu = p.last_use[s * A + lane];
     }
     stag[lane] = tg;
-    int d = 0, cls = kNoReuse;  // next reuse distance (0 = none) and class of the resident line
-    if (tg != kInvalid) {
-      if (p.period <= 1) {  // exact, from the window bitmask (P = 1)
-        d = next_reuse_d(p.mask + (size_t)(tg / G) * p.MW, p0_, p.W);
-        cls = class_of(d, p.T);
-      } else {              // the last window scan's snapshot
-        cls = class_of_info(p.line_info[s * A + lane], t_, p.T, &d);
-      }
-    }
-    sd[lane] = d;
-    scls[lane] = cls;
     __syncwarp();
     warp_bitonic_sort(sv, (int)Pm);  // nodes ascending (R10: misses installed in node order)
 
@@ -604,6 +614,19 @@ __global__ void k_set(SetParams p) {
     const uint32_t nF = __popc(freem);
     const uint32_t e = nI > nF ? nI - nF : 0;
     if (e) {
+      // next reuse distance (0 = none) and class of each resident line: needed only when
+      // lines are evicted (victim keys, eviction classes, victim candidates)
+      int d = 0, cls = kNoReuse;
+      if (tg != kInvalid) {
+        if (p.period <= 1) {  // exact, from the window bitmask (P = 1)
+          d = next_reuse_d(p.mask + (size_t)(tg / G) * p.MW, p0_, p.W);
+          cls = class_of(d, p.T);
+        } else {              // the last window scan's snapshot
+          cls = class_of_info(p.line_info[s * A + lane], t_, p.T, &d);
+        }
+      }
+      sd[lane] = d;
+      scls[lane] = cls;
       uint32_t rank;
       if (p.policy == 3) {  // RR: candidates in cyclic order from the cursor
         const uint32_t c0 = p.rr[s];
@@ -938,7 +961,7 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
 // Window feed. Bit (k mod (W+1)) of mask[q] is set when node q*G+me is in B_k. The ring slot
 // and bit of the batch being fed is it->wslot. k_mask_clear drops the bits of the iteration
 // that last used the slot (its stored list) and then — last CTA out — empties the slot;
-// k_route_local / k_win_gather store the new batch; k_mask_set sets its bits.
+// k_route_local / k_win_gather store the new batch and set its bits.
 __global__ void k_mask_clear(const uint32_t* __restrict__ ring, uint64_t stride, uint32_t* ring_len, IterState* it,
                              uint32_t G, uint32_t MW, uint32_t* __restrict__ mask) {
   const uint32_t bit = it->wslot;
@@ -956,26 +979,23 @@ __global__ void k_mask_clear(const uint32_t* __restrict__ ring, uint64_t stride,
     }
   }
 }
-__global__ void k_mask_set(const uint32_t* __restrict__ ring, uint64_t stride, const uint32_t* ring_len,
-                           const IterState* it, uint32_t G, uint32_t MW, uint32_t* __restrict__ mask) {
-  const uint32_t bit = it->wslot;
-  const uint32_t* __restrict__ list = ring + (size_t)bit * stride;
-  const uint32_t n = ring_len[bit];
-  const uint32_t m = 1u << (bit & 31);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicOr(&mask[(size_t)(list[i] / G) * MW + (bit >> 5)], m);
-}
-// Copy the inboxes of all sources (window IDs routed to this home) into the ring slot.
+// Copy the inboxes of all sources (window IDs routed to this home) into the ring slot and
+// set each node's reuse bit of the slot.
 __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
                              uint32_t nsrc, uint32_t cap, uint32_t* __restrict__ ring, uint64_t stride,
-                             uint32_t* ring_len, const IterState* it) {
+                             uint32_t* ring_len, const IterState* it, uint32_t G, uint32_t MW,
+                             uint32_t* __restrict__ mask) {
   const uint32_t slot_i = it->wslot;
   uint32_t* __restrict__ slot = ring + (size_t)slot_i * stride;
+  const uint32_t m = 1u << (slot_i & 31);
   uint32_t base = 0;
   for (uint32_t r = 0; r < nsrc; ++r) {
     const uint32_t n = inbox_cnt[r];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-      slot[base + i] = inbox[(size_t)r * cap + i];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const uint32_t v = inbox[(size_t)r * cap + i];
+      slot[base + i] = v;
+      atomicOr(&mask[(size_t)(v / G) * MW + (slot_i >> 5)], m);
+    }
     base += n;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) ring_len[slot_i] = base;

@@ -414,7 +414,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   if (G == 1) {
     if (n_bound > 0) {
       k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, 0u, g.N, inbox_of(g.arena), 0, g.local_inbox_cnt,
-                                                            g.scr, g.inbox_i);
+                                                            g.scr, g.inbox_i, nullptr, 0u);
       LAUNCHED();
     }
     inbox_cnt = g.local_inbox_cnt;
@@ -572,21 +572,20 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
   LAUNCHED();
   if (G == 1) {
     if (n_bound > 0) {
-      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, 1u, g.N, g.ring, stride, g.ring_len, g.scr, nullptr);
+      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, 1u, g.N, g.ring, stride, g.ring_len, g.scr, nullptr,
+                                                            g.mask, g.MW);
       LAUNCHED();
     }
   } else {
     const uint32_t seq = ++g.win_seq;
     if (int rc = exchange_ids(n_bound, true, seq, st)) return rc;
     k_win_gather<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(win_of(g.arena), wcnt_of(g.arena), (uint32_t)G,
-                                                                    (uint32_t)g.cap, g.ring, stride, g.ring_len, g.it);
+                                                                    (uint32_t)g.cap, g.ring, stride, g.ring_len, g.it,
+                                                                    (uint32_t)G, g.MW, g.mask);
     LAUNCHED();
     // window inbox consumed
     if (int rc = flags_write_all(st, (uint32_t)(3 * G + g.rank), seq)) return rc;
   }
-  k_mask_set<<<grid_for((int64_t)stride, 256, 2), 256, 0, st>>>(g.ring, stride, g.ring_len, g.it, (uint32_t)G, g.MW,
-                                                                 g.mask);
-  LAUNCHED();
   return 0;
 }
 
