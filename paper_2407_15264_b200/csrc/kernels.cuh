@@ -512,6 +512,25 @@ __global__ void k_set(SetParams p) {
     }
     stag[lane] = tg;
     __syncwarp();
+    if (m <= 32) {  // fast path: every node of the bucket is resident (no miss, no replacement)
+      const uint32_t v = lane < m ? sv[lane] : kInvalid;
+      int way = -1;
+      if (lane < m)
+        for (uint32_t w = 0; w < A; ++w)
+          if (stag[w] == v) way = (int)w;
+      if (__all_sync(0xffffffffu, lane >= m || way >= 0)) {
+        uint32_t pm = 0;
+        if (lane < m) {
+          p.node_loc[v / G] = s * A + (uint32_t)way;
+          ++ctr[C_HIT];
+          pm = 1u << way;
+        }
+        pm = __reduce_or_sync(0xffffffffu, pm);
+        if ((pm >> lane) & 1u) p.last_use[s * A + lane] = t_;
+        __syncwarp();
+        continue;
+      }
+    }
     warp_bitonic_sort(sv, (int)Pm);  // nodes ascending (R10: misses installed in node order)
 
     // ---- probe (S4): tag compare, then the PVP staging directory
