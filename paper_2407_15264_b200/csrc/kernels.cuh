@@ -287,65 +287,102 @@ __device__ __forceinline__ uint32_t pow2_at_least_32(uint32_t m) {
   return p;
 }
 
-// Exclusive scan of set_cnt[0..S) into set_off[0..S] by one CTA (1024 threads). With poff,
-// also the offsets of the global scratch of the sets too large for k_set's shared memory
-// (bucket > big_P): each gets a power-of-two region. The same CTA counts staged PVP rows
-// that this batch did not request (pvp_unused). Tiles of 4096 counts move through shared
-// memory (coalesced loads and stores; each thread scans 4 contiguous counts, skewed against
-// bank conflicts), one block-wide scan per tile carries the running total.
+// Exclusive scan of cnt[0..n) into off[0..n], one CTA (1024 threads) per tile of 4096 counts.
+// Each CTA scans its tile in shared memory (coalesced loads and stores; each thread owns 4
+// contiguous counts, skewed against bank conflicts), publishes the tile total, and takes
+// its carry from the totals of the tiles before it (look-back on per-tile flags stamped
+// with `seq`, unique per launch site and iteration). With poff, also the offsets of the
+// global scratch of the sets too large for k_set's shared memory (bucket > big_P): each
+// gets a power-of-two region. The CTAs also count staged PVP rows that this batch did not
+// request (pvp_unused).
 constexpr uint32_t kScanTile = 4096;
+struct ScanSync {
+  uint32_t* flag;  // [tiles] seq once agg/pagg of the tile are published
+  uint32_t* agg;   // [tiles] tile totals
+  uint32_t* pagg;  // [tiles] tile totals of the oversized-set regions
+};
 __device__ __forceinline__ uint32_t scan_skew(uint32_t j) { return j + (j >> 5); }
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off,
                                                uint32_t n, const uint32_t* __restrict__ stg_base, uint32_t C,
                                                const Scratch* scr, const uint32_t* __restrict__ mark,
                                                const IterState* it, uint32_t G, unsigned long long* hist,
-                                               uint32_t* __restrict__ poff, uint32_t big_P) {
+                                               uint32_t* __restrict__ poff, uint32_t big_P, ScanSync sy,
+                                               uint32_t seq_add) {
   __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_carry[2];
   __shared__ uint32_t s_c[kScanTile + kScanTile / 32];
   __shared__ uint32_t s_p[kScanTile + kScanTile / 32];
-  const uint32_t tid = threadIdx.x;
-  uint32_t carry = 0, pcarry = 0;
-  for (uint32_t base = 0; base < n; base += kScanTile) {
-    for (uint32_t j = tid; j < kScanTile; j += 1024) s_c[scan_skew(j)] = base + j < n ? cnt[base + j] : 0u;
-    __syncthreads();
-    uint32_t v[4], sum = 0, psum = 0;
+  const uint32_t tid = threadIdx.x, b = blockIdx.x;
+  const uint32_t base = b * kScanTile;
+  const uint32_t seq = 2u * it->stamp + seq_add;
+  for (uint32_t j = tid; j < kScanTile; j += 1024) s_c[scan_skew(j)] = base + j < n ? cnt[base + j] : 0u;
+  __syncthreads();
+  uint32_t v[4], sum = 0, psum = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[k] = s_c[scan_skew(tid * 4 + k)];
-      sum += v[k];
-      if (v[k] > big_P) psum += pow2_at_least_32(v[k]);
+  for (int k = 0; k < 4; ++k) {
+    v[k] = s_c[scan_skew(tid * 4 + k)];
+    sum += v[k];
+    if (v[k] > big_P) psum += pow2_at_least_32(v[k]);
+  }
+  uint32_t run = block_exclusive_1024(sum, s_warp);
+  const uint32_t total = s_warp[31];
+  uint32_t prun = 0, ptotal = 0;
+  if (poff) {
+    prun = block_exclusive_1024(psum, s_warp);
+    ptotal = s_warp[31];
+  }
+  if (gridDim.x > 1) {
+    if (tid == 0) {  // publish this tile's totals
+      sy.agg[b] = total;
+      sy.pagg[b] = ptotal;
+      __threadfence();
+      *(volatile uint32_t*)&sy.flag[b] = seq;
     }
-    uint32_t run = block_exclusive_1024(sum, s_warp) + carry;
-    carry += s_warp[31];
-    if (poff) {
-      uint32_t prun = block_exclusive_1024(psum, s_warp) + pcarry;
-      pcarry += s_warp[31];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        s_p[scan_skew(tid * 4 + k)] = prun;
-        if (v[k] > big_P) prun += pow2_at_least_32(v[k]);
+    if (tid < 32) {  // carry = totals of the tiles before this one
+      uint32_t c = 0, pc = 0;
+      for (uint32_t j = tid; j < b; j += 32) {
+        while (*(volatile const uint32_t*)&sy.flag[j] != seq) {
+        }
+        __threadfence();
+        c += *(volatile const uint32_t*)&sy.agg[j];
+        pc += *(volatile const uint32_t*)&sy.pagg[j];
+      }
+      c = __reduce_add_sync(0xffffffffu, c);
+      pc = __reduce_add_sync(0xffffffffu, pc);
+      if (tid == 0) {
+        s_carry[0] = c;
+        s_carry[1] = pc;
       }
     }
+    __syncthreads();
+    run += s_carry[0];
+    prun += s_carry[1];
+  }
+  if (poff) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      s_c[scan_skew(tid * 4 + k)] = run;
-      run += v[k];
+      s_p[scan_skew(tid * 4 + k)] = prun;
+      if (v[k] > big_P) prun += pow2_at_least_32(v[k]);
     }
-    __syncthreads();
-    for (uint32_t j = tid; j < kScanTile && base + j < n; j += 1024) {
-      off[base + j] = s_c[scan_skew(j)];
-      if (poff) poff[base + j] = s_p[scan_skew(j)];
-    }
-    __syncthreads();
   }
-  if (tid == 0) off[n] = carry;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    s_c[scan_skew(tid * 4 + k)] = run;
+    run += v[k];
+  }
+  __syncthreads();
+  for (uint32_t j = tid; j < kScanTile && base + j < n; j += 1024) {
+    off[base + j] = s_c[scan_skew(j)];
+    if (poff) poff[base + j] = s_p[scan_skew(j)];
+  }
+  if (b == gridDim.x - 1 && tid == 1023) off[n] = run;  // the grand total
   // pvp_unused: staged rows whose node this batch did not request
   if (stg_base) {
     const uint32_t par = it->par, stamp = it->stamp;
     const uint32_t* stg_nodes = stg_base + (size_t)par * C;
     const uint32_t ns = scr->staged[par];
     uint32_t unused = 0;
-    for (uint32_t j = tid; j < ns; j += 1024) unused += mark[stg_nodes[j] / G] != stamp;
+    for (uint32_t j = b * 1024 + tid; j < ns; j += gridDim.x * 1024) unused += mark[stg_nodes[j] / G] != stamp;
     unused = __reduce_add_sync(0xffffffffu, unused);
     if ((tid & 31) == 0 && unused)
       atomicAdd(&hist[(size_t)it->rec_idx * F_NFIELDS + F_UNUSED], (unsigned long long)unused);

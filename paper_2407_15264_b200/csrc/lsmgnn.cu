@@ -66,6 +66,7 @@ struct Ctx {
   // global scratch for cache sets whose bucket exceeds k_set's shared-memory capacity
   uint32_t *poff = nullptr, *g_sv = nullptr, *g_sk = nullptr, *g_sidx = nullptr;
   unsigned long long* g_skey = nullptr;
+  uint32_t *scan_set = nullptr, *scan_q = nullptr;  // k_scan look-back words (3 x tiles each)
   uint32_t *qcnt = nullptr, *qoff = nullptr, *qb = nullptr, *qlen = nullptr, *qnode = nullptr;
   uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr, *local_inbox_cnt = nullptr;
   unsigned long long* head = nullptr;            // G = 1 fused delivery: per-node request list heads
@@ -177,6 +178,13 @@ int dalloc(T** p, size_t count) {
   CK(cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
   CK(cudaMemset(*p, 0, count * sizeof(T)));
   return 0;
+}
+
+// k_scan grid (one CTA per tile of counts) and its look-back words
+int scan_tiles(uint64_t n) { return (int)std::max<uint64_t>(1, (n + kScanTile - 1) / kScanTile); }
+ScanSync scan_sync(uint32_t* words, uint64_t n) {
+  const size_t k = (size_t)scan_tiles(n);
+  return ScanSync{words, words + k, words + 2 * k};
 }
 
 // arena views (local or peer)
@@ -325,7 +333,7 @@ void prof_end(int ph, cudaStream_t st) {
 
 int free_all() {
   cudaDeviceSynchronize();
-  void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off,
+  void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off, g.scan_set, g.scan_q,
                   g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
                   g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.head, g.nxt, g.inbox_i, g.line_info, g.score, g.fills, g.cands,
                   g.scr, g.it, g.hist, g.poff, g.g_sv, g.g_sk, g.g_sidx, g.g_skey,
@@ -430,8 +438,9 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, g.it, g.mark,
       g.uniq, g.set_cnt, g.scr, g.hist, G == 1 ? g.head : nullptr, g.nxt);
   LAUNCHED();
-  k_scan<<<1, 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr, (uint32_t)g.C, g.scr,
-                             g.mark, g.it, (uint32_t)G, g.hist, g.poff, g.P);
+  k_scan<<<scan_tiles(g.S), 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr,
+                                           (uint32_t)g.C, g.scr, g.mark, g.it, (uint32_t)G, g.hist, g.poff, g.P,
+                                           scan_sync(g.scan_set, g.S), 0u);
   LAUNCHED();
   k_bucket<<<grid_for(std::max<int64_t>(n_bound, 1) * G, 256, 4), 256, 0, st>>>(g.uniq, g.scr, (uint32_t)G,
                                                                                  (uint32_t)g.S, g.set_off, g.set_cnt,
@@ -493,7 +502,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   if (g.C) {
     prof_begin(3, st);
     const int qg = grid_for(g.ucap, 256, 2);
-    k_scan<<<1, 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr, nullptr, 0);
+    k_scan<<<scan_tiles(g.W), 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr,
+                                             nullptr, 0, scan_sync(g.scan_q, g.W), 1u);
     LAUNCHED();
     k_qscatter<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
     LAUNCHED();
@@ -738,6 +748,8 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.vst_idx, g.Q);
   DA(g.set_cnt, g.S);
   DA(g.set_off, g.S + 1);
+  DA(g.scan_set, 3 * (size_t)scan_tiles(g.S));
+  DA(g.scan_q, 3 * (size_t)scan_tiles(g.W));
   if (big_sets) {  // power-of-two regions per oversized set: at most 2x the unique count
     DA(g.poff, g.S);
     DA(g.g_sv, 2 * g.ucap + 64);

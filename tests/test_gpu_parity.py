@@ -188,6 +188,26 @@ def test_oversized_set_buckets(policy, pvp):
     compare(hg, ho, f"big sets {policy}/pvp{pvp}")
 
 
+@pytest.mark.parametrize("policy,pvp", [("hybrid", 1), ("lru", 0)])
+def test_multi_tile_set_scan(policy, pvp):
+    """S = 12,000 sets: the set-offset scan spans three 4096-count tiles (k_scan's look-back
+    carries), and two sets in later tiles receive > 1024 distinct nodes per batch, so their
+    global-scratch regions are placed by the carried oversized-set offsets — bit-exact."""
+    rng = np.random.default_rng(23)
+    S, A = 12_000, 4
+    N = 1_120 * S
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    tr = []
+    for _ in range(10):
+        big = [s + S * rng.choice(1_120, 1_100, replace=False) for s in (5_000, 9_000)]
+        tr.append([rng.permutation(np.concatenate(big + [rng.integers(0, N, 20_000)])).astype(np.int64)])
+    kw = dict(N=N, D=4, L=S * A, A=A, scores=sc, policy=policy, pvp=pvp, W=4, V=4_000)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"multi-tile scan {policy}/pvp{pvp}")
+
+
 @pytest.mark.parametrize("policy,pvp,P", [("hybrid", 1, 1), ("lru", 0, 1), ("rr", 1, 1), ("dynamic", 1, 2)])
 def test_cache_state_parity(cfg1_g1, policy, pvp, P):
     """Stronger than equal counters: after every iteration the GPU's cache state equals the
