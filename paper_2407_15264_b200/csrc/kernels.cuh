@@ -2,9 +2,9 @@
 //
 // Step names follow SURVEY.md §8(a) (S1..S11) and DESIGN.md §"Kernels":
 //   k_begin/k_end  S9  per-iteration state (IterState: t, stamps, batch pointer) and counters
-//   k_route_local  S1  G = 1: validate IDs, write the home inbox (or a window ring slot)
 //   k_route_peer   S1  G > 1: bucket by home (v mod G), store into the homes' inboxes (P2P)
-//   k_dedup        S3  home: unique nodes (node-indexed stamp table) + per-set counts (+ request lists)
+//   k_dedup        S1+S3 home: unique nodes (node-indexed stamp table) + per-set counts; at G = 1 it
+//                       reads the caller's IDs directly and threads the request lists
 //   k_scan         S3  home: exclusive scan of per-set counts; oversized-set scratch; PVP "unused"
 //   k_bucket       S3  home: scatter unique nodes into set buckets
 //   k_snapshot     S4  period > 1: the paper's periodic window scan of every resident line
@@ -23,8 +23,8 @@
 namespace lsm {
 
 // ------------------------------------------------------------------------------ S9
-// Start gather t: publish the iteration's values (IterState), zero its record, the per-batch
-// scratch counters and the local inbox count. t_host >= 0: t and the batch come from the
+// Start gather t: publish the iteration's values (IterState), zero its record and the per-batch
+// scratch counters. t_host >= 0: t and the batch come from the
 // host; t_host < 0 (graph replay): t = it->t_next, batch = ids_ring[t mod ring_len].
 struct BeginArgs {
   int64_t t_host;
@@ -34,7 +34,6 @@ struct BeginArgs {
   const int64_t* n_ring;           // and their lengths
   uint32_t ring_len;
   uint32_t Wp1, period, L, C;
-  uint32_t* inbox_cnt;             // zeroed (G = 1), may be null
   int64_t cap;                     // max_batch_ids: a longer device-resident batch is clamped ...
   volatile uint32_t* overflow;     // ... and flagged here (pinned host word, sticky EINVAL)
 };
@@ -72,7 +71,6 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
     scr->nbypass = 0;
     scr->nreq = 0;
     scr->pull_next = 0;
-    if (a.inbox_cnt) *a.inbox_cnt = 0;
   }
 }
 
@@ -131,20 +129,20 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
   it->wk_next = k + 1;
 }
 
-// ------------------------------------------------------------------------------ S1 (G = 1)
-// Validate the caller's int64 IDs and write them (u32) into this home's inbox (gather) or a
-// window ring slot (prefetch): ids/n = it->ids/n or it->wids/wn; output slot = *slot_ptr.
-// With `mask` (window feed), each stored node also sets its reuse bit of the slot (S10).
-__global__ void k_route_local(const IterState* it, uint32_t window, uint64_t N, uint32_t* __restrict__ out_base,
-                              uint64_t out_stride, uint32_t* __restrict__ cnt_base, Scratch* scr,
-                              uint32_t* __restrict__ inbox_i, uint32_t* __restrict__ mask, uint32_t MW) {
-  const int64_t* __restrict__ ids = window ? it->wids : it->ids;
-  const int64_t n = window ? it->wn : it->n;
-  const uint32_t slot = window ? it->wslot : 0u;
-  uint32_t* __restrict__ inbox = out_base + (size_t)slot * out_stride;
-  uint32_t* inbox_cnt = cnt_base + slot;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+// ------------------------------------------------------------------------------ S10 (G = 1)
+// Window feed at one home: validate the caller's int64 IDs (it->wids/wn), write them (u32)
+// into ring slot it->wslot, and set each node's reuse bit of the slot. (The gather side of
+// S1 at G = 1 is fused into k_dedup.)
+__global__ void k_route_local(const IterState* it, uint64_t N, uint32_t* __restrict__ ring, uint64_t stride,
+                              uint32_t* __restrict__ ring_len, Scratch* scr, uint32_t* __restrict__ mask,
+                              uint32_t MW) {
+  const int64_t* __restrict__ ids = it->wids;
+  const int64_t n = it->wn;
+  const uint32_t slot = it->wslot;
+  uint32_t* __restrict__ list = ring + (size_t)slot * stride;
+  uint32_t* cnt = ring_len + slot;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += gstride) {
     const int64_t i = base + threadIdx.x;
     bool ok = false;
     uint32_t v = 0;
@@ -154,11 +152,10 @@ __global__ void k_route_local(const IterState* it, uint32_t window, uint64_t N, 
       v = (uint32_t)x;
       if (!ok) atomicAdd(&scr->bad_ids, 1u);
     }
-    const uint32_t pos = warp_reserve(inbox_cnt, ok ? 1u : 0u);
+    const uint32_t pos = warp_reserve(cnt, ok ? 1u : 0u);
     if (ok) {
-      inbox[pos] = v;
-      if (inbox_i) inbox_i[pos] = (uint32_t)i;
-      if (mask) atomicOr(&mask[(size_t)v * MW + (slot >> 5)], 1u << (slot & 31));  // G = 1: q = v
+      list[pos] = v;
+      atomicOr(&mask[(size_t)v * MW + (slot >> 5)], 1u << (slot & 31));  // G = 1: q = v
     }
   }
 }
@@ -215,38 +212,70 @@ __global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
 // Home: one representative per distinct node (stamp table indexed by q = v / G),
 // appended to uniq[]; per-set counts for the bucket pass. Requests and peer requests
 // are counted here (every count but `requests` is over unique nodes, R11).
-// With `head` != null (G = 1, fused delivery) it also threads every request position onto
-// its node's list: head[q] = stamp<<32 | last position, nxt[pos] = previous (kInvalid = end).
+// G = 1 (direct): the caller's int64 IDs are read straight from it->ids and validated here
+// (S1 fused away; an ID >= N counts toward ERANGE and is skipped), and every request
+// position i is threaded onto its node's list for the fused delivery of k_serve:
+// head[q] = stamp<<32 | last position, nxt[i] = previous (kInvalid = end).
+// G > 1: the IDs come from the inbox segments of the nsrc requesters.
+__device__ __forceinline__ void dedup_one(uint32_t v, uint32_t pos, uint32_t G, uint32_t S, uint32_t stamp,
+                                          uint32_t* __restrict__ mark, uint32_t* __restrict__ set_cnt,
+                                          unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt,
+                                          bool* first) {
+  const uint32_t q = v / G;
+  *first = atomicExch(&mark[q], stamp) != stamp;
+  if (*first) atomicAdd(&set_cnt[q % S], 1u);
+  if (head) {
+    const unsigned long long old = atomicExch(&head[q], ((unsigned long long)stamp << 32) | pos);
+    nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
+  }
+}
 __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
                         uint32_t nsrc, uint32_t cap, uint32_t me, uint32_t G, uint32_t S,
                         const IterState* it, uint32_t* __restrict__ mark, uint32_t* __restrict__ uniq,
                         uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* hist,
-                        unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt) {
+                        unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt, uint32_t direct,
+                        uint64_t N) {
   const uint32_t stamp = it->stamp;
   unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
   uint32_t nreq = 0, npeer = 0;
-  for (uint32_t r = 0; r < nsrc; ++r) {
-    const uint32_t n = inbox_cnt[r];
-    const uint32_t* in = inbox + (size_t)r * cap;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
-      const uint32_t i = base + threadIdx.x;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  if (direct) {
+    const int64_t* __restrict__ ids = it->ids;
+    const int64_t n = it->n;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+      const int64_t i = base + threadIdx.x;
       bool first = false;
       uint32_t v = 0;
       if (i < n) {
-        v = in[i];
-        const uint32_t q = v / G;
-        first = atomicExch(&mark[q], stamp) != stamp;
-        if (first) atomicAdd(&set_cnt[q % S], 1u);
-        if (head) {
-          const unsigned long long old = atomicExch(&head[q], ((unsigned long long)stamp << 32) | i);
-          nxt[i] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
+        const int64_t x = ids[i];
+        if (x >= 0 && (uint64_t)x < N) {
+          v = (uint32_t)x;
+          dedup_one(v, (uint32_t)i, G, S, stamp, mark, set_cnt, head, nxt, &first);
+          ++nreq;
+        } else {
+          atomicAdd(&scr->bad_ids, 1u);
         }
-        ++nreq;
-        if (r != me) ++npeer;
       }
       const uint32_t pos = warp_reserve(&scr->nuniq, first ? 1u : 0u);
       if (first) uniq[pos] = v;
+    }
+  } else {
+    for (uint32_t r = 0; r < nsrc; ++r) {
+      const uint32_t n = inbox_cnt[r];
+      const uint32_t* in = inbox + (size_t)r * cap;
+      for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+        const uint32_t i = base + threadIdx.x;
+        bool first = false;
+        uint32_t v = 0;
+        if (i < n) {
+          v = in[i];
+          dedup_one(v, i, G, S, stamp, mark, set_cnt, head, nxt, &first);
+          ++nreq;
+          if (r != me) ++npeer;
+        }
+        const uint32_t pos = warp_reserve(&scr->nuniq, first ? 1u : 0u);
+        if (first) uniq[pos] = v;
+      }
     }
   }
   nreq = __reduce_add_sync(0xffffffffu, nreq);
@@ -949,7 +978,7 @@ template <int UNROLL, int OUT>
 __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* __restrict__ pool,
                         const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
                         const unsigned long long* __restrict__ head, const uint32_t* __restrict__ nxt,
-                        const uint32_t* __restrict__ inbox_i, const IterState* it, uint64_t N,
+                        const IterState* it, uint64_t N,
                         const uint32_t* __restrict__ node_loc, uint4* __restrict__ out) {
   constexpr uint32_t kChunk = 16;
   const uint32_t stamp = it->stamp;
@@ -982,7 +1011,7 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
           if (k < nvec) st16<kDev>(slot + k, v[u]);
         }
         for (uint32_t pos = first; pos != kInvalid; pos = nxt[pos]) {
-          uint4* dst = out + (size_t)inbox_i[pos] * nvec;
+          uint4* dst = out + (size_t)pos * nvec;  // list positions are request indices
 #pragma unroll
           for (int u = 0; u < UNROLL; ++u) {
             const uint32_t k = base + lane + 32 * u;

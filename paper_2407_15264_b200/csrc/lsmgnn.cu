@@ -68,10 +68,10 @@ struct Ctx {
   unsigned long long* g_skey = nullptr;
   uint32_t *scan_set = nullptr, *scan_q = nullptr;  // k_scan look-back words (3 x tiles each)
   uint32_t *qcnt = nullptr, *qoff = nullptr, *qb = nullptr, *qlen = nullptr, *qnode = nullptr;
-  uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr, *local_inbox_cnt = nullptr;
+  uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr;
   unsigned long long* head = nullptr;            // G = 1 fused delivery: per-node request list heads
   uint32_t* line_info = nullptr;                 // update period > 1: per-line dynamic information
-  uint32_t *nxt = nullptr, *inbox_i = nullptr;   // next position / original request index
+  uint32_t* nxt = nullptr;   // next request position of the same node
   uint8_t* score = nullptr;
   FillEnt* fills = nullptr;
   Cand* cands = nullptr;
@@ -335,7 +335,7 @@ int free_all() {
   cudaDeviceSynchronize();
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off, g.scan_set, g.scan_q,
                   g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
-                  g.stg_nodes, g.route_cnt, g.local_inbox_cnt, g.head, g.nxt, g.inbox_i, g.line_info, g.score, g.fills, g.cands,
+                  g.stg_nodes, g.route_cnt, g.head, g.nxt, g.line_info, g.score, g.fills, g.cands,
                   g.scr, g.it, g.hist, g.poff, g.g_sv, g.g_sk, g.g_sidx, g.g_skey,
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
@@ -402,7 +402,6 @@ BeginArgs begin_args(int64_t t_host, const int64_t* ids, int64_t n, const int64_
   a.period = (uint32_t)std::max(1, g.opt.update_period);
   a.L = (uint32_t)g.stage_base0;
   a.C = (uint32_t)g.C;
-  a.inbox_cnt = g.world == 1 ? g.local_inbox_cnt : nullptr;
   a.cap = (int64_t)g.cap;
   a.overflow = g.bad_dev_overflow;
   return a;
@@ -420,12 +419,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   const uint32_t* inbox = inbox_of(g.arena);
   const uint32_t* inbox_cnt;
   if (G == 1) {
-    if (n_bound > 0) {
-      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, 0u, g.N, inbox_of(g.arena), 0, g.local_inbox_cnt,
-                                                            g.scr, g.inbox_i, nullptr, 0u);
-      LAUNCHED();
-    }
-    inbox_cnt = g.local_inbox_cnt;
+    inbox_cnt = nullptr;  // k_dedup reads the caller's IDs directly
   } else {
     if (int rc = exchange_ids(n_bound, false, stamp_host, st)) return rc;
     inbox_cnt = icnt_of(g.arena);
@@ -436,7 +430,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   const int64_t maxreq = (int64_t)g.cap * G;
   k_dedup<<<grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st>>>(
       inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, g.it, g.mark,
-      g.uniq, g.set_cnt, g.scr, g.hist, G == 1 ? g.head : nullptr, g.nxt);
+      g.uniq, g.set_cnt, g.scr, g.hist, G == 1 ? g.head : nullptr, g.nxt, G == 1 ? 1u : 0u, g.N);
   LAUNCHED();
   k_scan<<<scan_tiles(g.S), 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr,
                                            (uint32_t)g.C, g.scr, g.mark, g.it, (uint32_t)G, g.hist, g.poff, g.P,
@@ -523,7 +517,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     prof_begin(4, st);
     const int blocks = g.sms * std::min(4, g.geom_per_sm);
 #define SERVE(U, O)                                                                                                  \
-  k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.inbox_i, g.it, g.N, \
+  k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.it, g.N, \
                                         loc_of(g.arena), o4)
     if (wide && !out_host) SERVE(8, kDev);
     else if (wide) SERVE(8, kHost);
@@ -582,8 +576,8 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
   LAUNCHED();
   if (G == 1) {
     if (n_bound > 0) {
-      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, 1u, g.N, g.ring, stride, g.ring_len, g.scr, nullptr,
-                                                            g.mask, g.MW);
+      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, g.N, g.ring, stride, g.ring_len, g.scr, g.mask,
+                                                            g.MW);
       LAUNCHED();
     }
   } else {
@@ -769,7 +763,6 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.qreuse, std::max<uint64_t>(1, g.W * g.C));
   DA(g.stg_nodes, std::max<uint64_t>(1, 2 * g.C));
   DA(g.route_cnt, G);
-  DA(g.local_inbox_cnt, 1);
   if (g.opt.update_period > 1) {
     DA(g.line_info, g.L);
     CK(cudaMemset(g.line_info, 0xFF, g.L * sizeof(uint32_t)));
@@ -777,7 +770,6 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (G == 1) {
     DA(g.head, g.Q);
     DA(g.nxt, g.cap);
-    DA(g.inbox_i, g.cap);
   }
   DA(g.score, g.Q);
   DA(g.fills, g.ucap);
