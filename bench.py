@@ -148,11 +148,24 @@ def run_reference(args, wl, G, rank):
                        "N": wl.N, "row_bytes": wl.R, "batch_per_rank": wl.batch, "fanout": list(wl.fanout),
                        "lines_per_gpu": args.lines or wl.lines_per_gpu, "ways": wl.ways, "window": wl.window,
                        "policy": args.policy, "pvp": pvp},
-            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
                              "sample": f"full {wl.name} iterations {Wu}..{Wu + K - 1} after {Wu} untimed, rows "
                                        f"materialised by memcpy from the host table, single thread"},
             "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def host_cpu() -> dict:
+    """CPU model and logical CPU count of this host (the oracle uses one thread of it)."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count(), "threads_used": 1}
 
 
 def cpu_baseline(wl, G, trace, scores, table_np, args, lines):
@@ -172,7 +185,7 @@ def cpu_baseline(wl, G, trace, scores, table_np, args, lines):
         tsum += time.perf_counter() - t0
         byts += sum(len(x) for x in trace[t]) * wl.R
         t += 1
-    return {"value": round(byts / tsum / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+    return {"value": round(byts / tsum / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
             "sample": f"{wl.name} iterations 0..{t - 1} from a cold cache ({tsum:.1f}s), rows materialised by "
                       f"memcpy from the host table, single thread (C oracle, gcc -O2)"}
 
