@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true")
     p.add_argument("--no-ablation", action="store_true", help="skip the PVP on/off ablation")
+    p.add_argument("--no-file-tier", action="store_true", help="skip the file-tier (N2) measurement")
+    p.add_argument("--file-dir", default="/tmp", help="directory for the file tier's backing file")
     p.add_argument("--lines", type=int, default=None, help="override lines per GPU")
     p.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph (G = 1)")
     p.add_argument("--graph-steps", type=int, default=20, help="extra steps timed as CUDA-graph replays (G = 1)")
@@ -448,10 +450,71 @@ def main():
         line["gpu_sampler_pipeline"] = gpu_sampler_pipeline(wl, g_, scores, table, lines, args, dev)
         line["storage_per_epoch"] = epoch_storage(wl, g_, scores, lines, dev)
         line["hbm_regime"] = hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src)
+        if not args.no_file_tier:
+            line["file_tier"] = file_tier(wl, scores, ids_d, lines, args, max_ids, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if G > 1:
         torch.distributed.destroy_process_group()
+
+
+def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=3, steps=8):
+    """NEXT N2 measured: the same workload with the backing rows in a FILE on this box's disk
+    (the GPU pool has no NVMe; the root disk is a virtio block device). Each gather reads
+    the rows its fills need with parallel pread into a pinned bounce buffer; variants:
+    O_DIRECT (every storage row is a device read) and buffered after the file was just
+    written (page-cache hits: the tier's software overhead without the device)."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    from tests.harness import write_table_file
+    W = wl.window
+    st = torch.cuda.current_stream()
+    path = os.path.join(args.file_dir, f"lsmgnn_{wl.name}_home0.bin")
+    t0 = time.time()
+    write_table_file(path, wl.N, wl.D, wl.seeds["f"])
+    res = {"file": path, "file_GB": round(os.path.getsize(path) / 1e9, 3), "write_s": round(time.time() - t0, 1),
+           "steps": steps, "warmup": warm, "what": "backing rows in a file; fills read with pread (64 threads) into a "
+           "pinned bounce buffer, then the fill kernel as usual; gather GB/s = requested bytes / step time"}
+    out = torch.empty((max(x.numel() for x in ids_d), wl.R), dtype=torch.uint8, device=dev)
+    for name, env in (("o_direct", None), ("buffered_page_cache", "1")):
+        if env:
+            os.environ["LSMGNN_STORAGE_BUFFERED"] = env
+        try:
+            c = LsmGnn(wl.N, wl.D, lines, wl.ways, 0, scores, policy=args.policy, pvp=0, window=W,
+                       max_batch_ids=max_ids, device=dev.index)
+            c.attach_storage_file(path)
+            c.prefetch(ids_d[1:W + 1], first_iter=1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0, prof = None, {}
+            for t in range(warm + steps):
+                if t == warm:
+                    torch.cuda.synchronize()
+                    s0 = c.stats(1)
+                    c.profile(True)
+                    c.profile_read()
+                    e0.record(st)
+                c.gather(ids_d[t], out)
+                c.prefetch([ids_d[t + 1 + W]], first_iter=t + 1 + W)
+            e1.record(st)
+            torch.cuda.synchronize()
+            prof = c.profile_read()
+            c.profile(False)
+            s1 = c.stats(1)
+            c.close()
+        finally:
+            os.environ.pop("LSMGNN_STORAGE_BUFFERED", None)
+        T = e0.elapsed_time(e1) / 1e3
+        d = {k: s1[k] - s0[k] for k in s1 if k != "iter"}
+        fill_s = prof.get("fill", (0.0, 0))[0] / 1e3
+        res[name] = {"gather_GBps": round(d["requests"] * wl.R / T / 1e9, 3), "ms_per_step": round(T / steps * 1e3, 2),
+                     "storage_GB_per_step": round(d["bytes_h2d_storage"] / steps / 1e9, 4),
+                     "storage_read_GBps": round(d["bytes_h2d_storage"] / fill_s / 1e9, 3) if fill_s else None,
+                     "fill_share_of_step": round(fill_s / T, 4)}
+    try:
+        os.remove(path)
+    except OSError:
+        pass
+    return res
 
 
 def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, warm=60, steps=30):

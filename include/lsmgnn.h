@@ -46,6 +46,7 @@ extern "C" {
 #define LSMGNN_ECUDA (-4)   /* a CUDA runtime/driver call failed                            */
 #define LSMGNN_ESTATE (-5)  /* call order (not initialised, iterations out of order, ...)   */
 #define LSMGNN_ECOMM (-6)   /* peer mapping / exchange failure                              */
+#define LSMGNN_EIO (-7)     /* storage file open/read failure (file tier)                    */
 
 typedef enum { LSMGNN_F32 = 0, LSMGNN_F16 = 1, LSMGNN_BF16 = 2 } lsmgnn_dtype;
 
@@ -126,7 +127,17 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
  * rank + k*G), ceil((N - rank)/G) rows of R bytes. The library page-locks it with
  * cudaHostRegister unless it is already pinned, and reads it with zero-copy loads from
  * its fill kernel (features "directly fetched by GPU threads").
- * nvme_path must be NULL (an NVMe tier is not implemented). */
+ *
+ * File tier (NEXT N2, "storage"): host_rows_for_my_home = NULL and
+ * nvme_path = a file holding the same rows in the same order (row k at byte offset k*R;
+ * at least ceil((N - rank)/G) * R bytes, else LSMGNN_EINVAL). Opened read-only with
+ * O_DIRECT when R is a multiple of 512 (the page cache is bypassed: every storage read is
+ * a device read), buffered otherwise; LSMGNN_STORAGE_BUFFERED=1 forces buffered. Each
+ * gather then reads the rows its fills need (known once replacement has run) with
+ * parallel pread into a pinned bounce buffer that the fill kernel reads over PCIe — a host
+ * step in the middle of the gather (it synchronises `stream` once); graph capture is
+ * refused in this mode. Open/read failures return LSMGNN_EIO. Exactly one of the two
+ * arguments must be non-NULL. */
 int lsmgnn_attach_storage(const void* host_rows_for_my_home, const char* nvme_path);
 
 /* G > 1 bootstrap. lsmgnn_export_handle writes this rank's shareable handle blob

@@ -170,6 +170,11 @@ class LsmGnn:
         self._keep.append(host_rows)
         _check(_LIB.lsmgnn_attach_storage(ctypes.c_void_p(ptr), None))
 
+    def attach_storage_file(self, path: str) -> None:
+        """File tier (N2): this home's rows in a file, row k at byte offset k*R (same order as
+        attach_storage). Read with O_DIRECT when R % 512 == 0, into a pinned bounce buffer."""
+        _check(_LIB.lsmgnn_attach_storage(None, os.fsencode(path)))
+
     def gather(self, ids, out, stream=None) -> None:
         """out[i] = table[ids[i]]; ids: int64 CUDA tensor, out: CUDA tensor of n*R bytes."""
         assert ids.is_cuda and ids.dtype.itemsize == 8 and ids.is_contiguous()

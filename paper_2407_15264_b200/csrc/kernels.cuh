@@ -921,7 +921,8 @@ __global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, c
 // P:249 "directly fetched by GPU threads") or from PVP staging into the slot.
 template <int UNROLL>
 __global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
-                       const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec) {
+                       const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
+                       uint32_t bounce) {
   const uint32_t n = scr->nfill;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -930,7 +931,7 @@ __global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, ui
     uint4* dst = pool + (size_t)f.dst * nvec;
     if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, dst, nvec);
     if (f.src & kHostBit)
-      warp_copy_row<UNROLL, kHost, kDev>(dst, table + (size_t)(f.src & ~kHostBit) * nvec, nvec);
+      warp_copy_row<UNROLL, kHost, kDev>(dst, table + (size_t)(bounce ? e : (f.src & ~kHostBit)) * nvec, nvec);
     else
       warp_copy_row<UNROLL, kDev, kDev>(dst, pool + (size_t)f.src * nvec, nvec);
   }
@@ -979,7 +980,7 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
                         const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
                         const unsigned long long* __restrict__ head, const uint32_t* __restrict__ nxt,
                         const IterState* it, uint64_t N,
-                        const uint32_t* __restrict__ node_loc, uint4* __restrict__ out) {
+                        const uint32_t* __restrict__ node_loc, uint4* __restrict__ out, uint32_t bounce) {
   constexpr uint32_t kChunk = 16;
   const uint32_t stamp = it->stamp;
   const int64_t* __restrict__ ids = it->ids;
@@ -995,7 +996,9 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
       uint4* slot = pool + (size_t)f.dst * nvec;
       if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, slot, nvec);
       const bool from_host = (f.src & kHostBit) != 0;
-      const uint4* src = from_host ? table + (size_t)(f.src & ~kHostBit) * nvec : pool + (size_t)f.src * nvec;
+      // host row: the backing table's row q, or (file tier) bounce-buffer row e
+      const uint4* src = from_host ? table + (size_t)(bounce ? e : (f.src & ~kHostBit)) * nvec
+                                   : pool + (size_t)f.src * nvec;
       const unsigned long long h = head[f.node];
       const uint32_t first = (uint32_t)(h >> 32) == stamp ? (uint32_t)h : kInvalid;
       for (uint32_t base = 0; base < nvec; base += 32 * UNROLL) {

@@ -11,7 +11,15 @@
 #include <cudaTypedefs.h>
 #include <nvtx3/nvToolsExt.h>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
+#include <cstdlib>
+#include <thread>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -92,6 +100,13 @@ struct Ctx {
   const uint8_t* table_host = nullptr;
   const uint8_t* table_dev = nullptr;
   bool table_registered = false;
+  // file tier (N2): rows read with pread into a pinned bounce buffer, row e = fill entry e
+  int file_fd = -1;
+  bool file_direct = false;
+  uint8_t* bounce_host = nullptr;
+  FillEnt* fills_host = nullptr;  // pinned copy of the fill list
+  uint32_t* nfill_host = nullptr;
+  int io_threads = 64;  // pread workers per batch (LSMGNN_IO_THREADS); deeper queues help NVMe
   volatile uint32_t* bad_host = nullptr;  // pinned mirror: [0] scr->bad_ids, [1] batch-length overflow
   uint32_t* bad_dev_overflow = nullptr;   // device mapping of bad_host + 1
   uint32_t* bad_dev = nullptr;
@@ -351,6 +366,10 @@ int free_all() {
   if (g.qrows_host) cudaFreeHost(g.qrows_host);
   if (g.bad_host) cudaFreeHost((void*)g.bad_host);
   if (g.table_registered) cudaHostUnregister((void*)g.table_host);
+  if (g.file_fd >= 0) close(g.file_fd);
+  if (g.bounce_host) cudaFreeHost(g.bounce_host);
+  if (g.fills_host) cudaFreeHost(g.fills_host);
+  if (g.nfill_host) cudaFreeHost(g.nfill_host);
   if (g.graph_exec) cudaGraphExecDestroy(g.graph_exec);
   if (g.graph) cudaGraphDestroy(g.graph);
   if (g.cap_stream) cudaStreamDestroy(g.cap_stream);
@@ -406,6 +425,8 @@ BeginArgs begin_args(int64_t t_host, const int64_t* ids, int64_t n, const int64_
   a.overflow = g.bad_dev_overflow;
   return a;
 }
+
+int read_storage_rows(cudaStream_t st);  // file tier (below)
 
 // gather kernels; n_bound = host bound of this rank's request count (grid sizing only);
 // stamp_host = t + 1 for the G > 1 flag protocol (direct calls only).
@@ -509,16 +530,19 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   // ---- S6 fill (victim D2H + storage/staging -> slot) and S7/S8 serve
   uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
   const uint4* tab = reinterpret_cast<const uint4*>(g.table_dev);
+  int rc_io = 0;
   uint4* hq = reinterpret_cast<uint4*>(g.qrows_dev);
   uint4* o4 = reinterpret_cast<uint4*>(out);
   const bool wide = g.nvec >= 256;
+  const uint32_t bounce = g.file_fd >= 0 ? 1u : 0u;  // file tier: storage rows staged per fill entry
   if (G == 1) {
     // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits
     prof_begin(4, st);
+    if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
     const int blocks = g.sms * std::min(4, g.geom_per_sm);
 #define SERVE(U, O)                                                                                                  \
   k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.it, g.N, \
-                                        loc_of(g.arena), o4)
+                                        loc_of(g.arena), o4, bounce)
     if (wide && !out_host) SERVE(8, kDev);
     else if (wide) SERVE(8, kHost);
     else if (!out_host) SERVE(2, kDev);
@@ -529,11 +553,12 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     prof_begin(5, st);
   } else {
     prof_begin(4, st);
+    if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
     const int blocks = g.sms * std::min(4, g.geom_per_sm);
     if (wide)
-      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
+      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce);
     else
-      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec);
+      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce);
     LAUNCHED();
     prof_end(4, st);
     // homes signal "served", requesters wait for every home, then pull
@@ -612,6 +637,88 @@ int launch_pvp(cudaStream_t st) {
   prof_end(7, g.side);
   CK(cudaEventRecord(g.ev_pvp, g.side));
   g.pvp_pending = true;
+  return 0;
+}
+
+// ---- file tier (N2)
+void detach_file() {
+  if (g.file_fd >= 0) close(g.file_fd);
+  g.file_fd = -1;
+  if (g.bounce_host) cudaFreeHost(g.bounce_host);
+  if (g.fills_host) cudaFreeHost(g.fills_host);
+  if (g.nfill_host) cudaFreeHost(g.nfill_host);
+  g.bounce_host = nullptr;
+  g.fills_host = nullptr;
+  g.nfill_host = nullptr;
+  g.table_dev = nullptr;
+}
+int attach_file(const char* path, uint64_t rows) {
+  const bool want_direct = g.R % 512 == 0 && !std::getenv("LSMGNN_STORAGE_BUFFERED");
+  int fd = open(path, O_RDONLY | (want_direct ? O_DIRECT : 0));
+  if (fd < 0 && want_direct) fd = open(path, O_RDONLY);  // a filesystem without O_DIRECT
+  if (fd < 0) return set_err(LSMGNN_EIO, "open(%s): %s", path, std::strerror(errno));
+  struct stat sb {};
+  if (fstat(fd, &sb) != 0 || (uint64_t)sb.st_size < rows * g.R) {
+    close(fd);
+    return set_err(LSMGNN_EINVAL, "%s holds %lld bytes, this home needs %llu", path, (long long)sb.st_size,
+                   (unsigned long long)(rows * g.R));
+  }
+  g.file_fd = fd;
+  g.file_direct = want_direct && (fcntl(fd, F_GETFL) & O_DIRECT);
+  // fills per batch <= unique nodes per batch at this home (installs + bypassed misses)
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&g.bounce_host), std::max<uint64_t>(1, g.ucap) * g.R,
+                   cudaHostAllocMapped | cudaHostAllocPortable));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&g.fills_host), std::max<uint64_t>(1, g.ucap) * sizeof(FillEnt),
+                   cudaHostAllocDefault));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&g.nfill_host), sizeof(uint32_t), cudaHostAllocDefault));
+  void* dp = nullptr;
+  CK(cudaHostGetDevicePointer(&dp, g.bounce_host, 0));
+  g.table_dev = reinterpret_cast<const uint8_t*>(dp);
+  g.table_host = nullptr;
+  if (const char* nt = std::getenv("LSMGNN_IO_THREADS")) g.io_threads = std::max(1, std::atoi(nt));
+  return 0;
+}
+// Read the storage rows of this batch's fills into the bounce buffer (row e = fill e).
+// Synchronises `st` (the fill list is decided on the device by k_set).
+int read_storage_rows(cudaStream_t st) {
+  CK(cudaMemcpyAsync(g.nfill_host, &g.scr->nfill, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const uint32_t n = *g.nfill_host;
+  if (n == 0) return 0;
+  CK(cudaMemcpyAsync(g.fills_host, g.fills, (size_t)n * sizeof(FillEnt), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::atomic<uint32_t> next{0};
+  std::atomic<int> err{0};
+  const uint64_t R = g.R;
+  auto work = [&]() {
+    for (;;) {
+      const uint32_t e0 = next.fetch_add(64);
+      if (e0 >= n || err.load()) return;
+      const uint32_t e1 = std::min(n, e0 + 64);
+      for (uint32_t e = e0; e < e1; ++e) {
+        const FillEnt f = g.fills_host[e];
+        if (!(f.src & kHostBit)) continue;  // PVP staging row: already in HBM
+        uint8_t* dst = g.bounce_host + (size_t)e * R;
+        const off_t off = (off_t)(f.src & ~kHostBit) * (off_t)R;
+        size_t done = 0;
+        while (done < R) {
+          const ssize_t r = pread(g.file_fd, dst + done, R - done, off + (off_t)done);
+          if (r <= 0) {
+            if (r < 0 && errno == EINTR) continue;
+            err.store(r < 0 ? errno : EIO);
+            return;
+          }
+          done += (size_t)r;
+        }
+      }
+    }
+  };
+  const int nt = (int)std::min<uint32_t>((uint32_t)g.io_threads, (n + 63) / 64);
+  std::vector<std::thread> pool;
+  for (int i = 1; i < nt; ++i) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  if (err.load()) return set_err(LSMGNN_EIO, "storage read failed: %s", std::strerror(err.load()));
   return 0;
 }
 
@@ -829,13 +936,14 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
 
 int lsmgnn_attach_storage(const void* host_rows, const char* nvme_path) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "attach_storage before init");
-  if (nvme_path) return set_err(LSMGNN_EINVAL, "NVMe tier not implemented (DESIGN.md: out of scope this round)");
-  if (!host_rows) return set_err(LSMGNN_EINVAL, "null storage");
+  if (!host_rows == !nvme_path) return set_err(LSMGNN_EINVAL, "exactly one of host_rows / nvme_path");
   if (g.table_registered) {
     cudaHostUnregister((void*)g.table_host);
     g.table_registered = false;
   }
+  detach_file();
   const uint64_t rows = (g.N > (uint64_t)g.rank) ? (g.N - g.rank + g.world - 1) / g.world : 0;
+  if (nvme_path) return attach_file(nvme_path, rows);
   cudaPointerAttributes at{};
   cudaError_t e = cudaPointerGetAttributes(&at, host_rows);
   if (e != cudaSuccess) cudaGetLastError();
@@ -1166,6 +1274,7 @@ int lsmgnn_graph_capture(const int64_t* const* ids_ring, const int64_t* n_ring, 
                          void* stream) {
   if (!g.inited || !g.table_dev) return set_err(LSMGNN_ESTATE, "graph_capture before init/attach_storage");
   if (g.world != 1) return set_err(LSMGNN_EINVAL, "graph mode is single-home (G = 1) only");
+  if (g.file_fd >= 0) return set_err(LSMGNN_EINVAL, "graph mode needs host-memory storage (the file tier reads on the host)");
   if (!ids_ring || !n_ring || !out || ring_len < (int32_t)g.W + 2)
     return set_err(LSMGNN_EINVAL, "graph_capture needs a ring of >= W+2 batches and an out buffer");
   if (g.feed_next != g.t_next + (int64_t)g.W + 1)

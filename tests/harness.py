@@ -29,7 +29,7 @@ def table_for(N: int, D: int, seed_f: int = 5, pinned: bool = False, home: int =
 
 def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1, table=None,
             check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False, P=1,
-            state_cb=None):
+            state_cb=None, storage_file=None):
     """Run trace[t][rank] through the library. Returns (history [K, 24] uint64, outs or None, bad_rows).
 
     check_rows: "full" compares every row with the closed form F(v); "none" skips it."""
@@ -41,9 +41,12 @@ def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0,
     mb = max_batch_ids or max(1, max(x.size for x in mine))
     c = LsmGnn(N, D, L, A, V, scores, policy=policy, pvp=pvp, window=W, threshold=T, reinsert=reinsert,
                max_batch_ids=mb, rank=rank, world=world, group=group, period=P)
-    if table is None:
-        table = table_for(N, D, seed_f, pinned=True, home=rank, G=world)
-    c.attach_storage(table)
+    if storage_file is not None:  # file tier: the same rows, read from a file per batch
+        c.attach_storage_file(storage_file)
+    else:
+        if table is None:
+            table = table_for(N, D, seed_f, pinned=True, home=rank, G=world)
+        c.attach_storage(table)
     dev = torch.device("cuda", torch.cuda.current_device())
     ids_d = [torch.from_numpy(x).to(dev) for x in mine]
     empty = torch.zeros(0, dtype=torch.int64, device=dev)
@@ -79,3 +82,17 @@ def small_workload(N=16384, m=8, G=1, batch=256, fanout=(10, 5), iters=20, dedup
     g = synth.plcite(N, m)
     tr = synth.make_trace(g, G, batch, fanout, iters, dedup=dedup, seed_s=seed_s)
     return g, tr, synth.static_scores(g)
+
+
+def write_table_file(path, N: int, D: int, seed_f: int = 5, home: int = 0, G: int = 1, chunk: int = 1 << 16):
+    """The file-tier layout of home `home`: its rows (node home + k*G at row k) back to back."""
+    import torch
+    rows = (N - home + G - 1) // G
+    with open(path, "wb") as f:
+        for r0 in range(0, rows, chunk):
+            n = min(chunk, rows - r0)
+            t = torch.empty((n, 4 * D), dtype=torch.uint8)
+            ids = np.arange(home + r0 * G, home + (r0 + n) * G, G, dtype=np.int64)
+            synth._lib().synth_fill_f32_ids(t.data_ptr(), ids.ctypes.data, ids.size, D, seed_f)
+            f.write(t.numpy().tobytes())
+    return str(path)

@@ -61,6 +61,10 @@ def main():
         K = len([k for k in z.files if k.endswith("_r0")])
         tr = [[z[f"t{t}_r{r}"] for r in range(world)] for t in range(K)]
         cfg = json.load(open(os.path.join(outdir, "cfg.json")))
+        if cfg.pop("file", 0):  # file tier: this home's rows in its own file
+            from tests.harness import write_table_file
+            cfg["storage_file"] = write_table_file(os.path.join(outdir, f"home{rank}.bin"), cfg["N"], cfg["D"],
+                                                   home=rank, G=world)
         hist, _, bad = run_gpu(tr, scores=z["scores"], rank=rank, world=world, group=dist.group.WORLD,
                                max_batch_ids=max(1, max(len(x) for row in tr for x in row)), **cfg)
         np.save(os.path.join(outdir, f"hist{rank}.npy"), hist)
