@@ -458,7 +458,7 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=3, steps=8):
+def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=10, steps=8):
     """NEXT N2 measured: the same workload with the backing rows in a FILE on this box's disk
     (the GPU pool has no NVMe; the root disk is a virtio block device). Each gather reads
     the rows its fills need with parallel pread into a pinned bounce buffer; variants:
@@ -476,12 +476,12 @@ def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=3, steps=8):
            "steps": steps, "warmup": warm, "what": "backing rows in a file; fills read with pread (64 threads) into a "
            "pinned bounce buffer, then the fill kernel as usual; gather GB/s = requested bytes / step time"}
     out = torch.empty((max(x.numel() for x in ids_d), wl.R), dtype=torch.uint8, device=dev)
-    for name, env in (("o_direct", None), ("buffered_page_cache", "1")):
+    for name, env, pvp in (("o_direct", None, 0), ("o_direct_pvp", None, 1), ("buffered_page_cache", "1", 0)):
         if env:
             os.environ["LSMGNN_STORAGE_BUFFERED"] = env
         try:
-            c = LsmGnn(wl.N, wl.D, lines, wl.ways, 0, scores, policy=args.policy, pvp=0, window=W,
-                       max_batch_ids=max_ids, device=dev.index)
+            c = LsmGnn(wl.N, wl.D, lines, wl.ways, wl.victim_lines if pvp else 0, scores, policy=args.policy, pvp=pvp,
+                       window=W, max_batch_ids=max_ids, device=dev.index)
             c.attach_storage_file(path)
             c.prefetch(ids_d[1:W + 1], first_iter=1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -496,7 +496,7 @@ def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=3, steps=8):
                 c.gather(ids_d[t], out)
                 c.prefetch([ids_d[t + 1 + W]], first_iter=t + 1 + W)
             e1.record(st)
-            torch.cuda.synchronize()
+            torch.cuda.synchronize()  # (the PVP side-stream copy overlaps the next gather's storage reads)
             prof = c.profile_read()
             c.profile(False)
             s1 = c.stats(1)
@@ -509,7 +509,8 @@ def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=3, steps=8):
         res[name] = {"gather_GBps": round(d["requests"] * wl.R / T / 1e9, 3), "ms_per_step": round(T / steps * 1e3, 2),
                      "storage_GB_per_step": round(d["bytes_h2d_storage"] / steps / 1e9, 4),
                      "storage_read_GBps": round(d["bytes_h2d_storage"] / fill_s / 1e9, 3) if fill_s else None,
-                     "fill_share_of_step": round(fill_s / T, 4)}
+                     "fill_share_of_step": round(fill_s / T, 4),
+                     "victim_hit_ratio": round(d["victim_hits"] / max(d["unique"], 1), 4)}
     try:
         os.remove(path)
     except OSError:
