@@ -385,7 +385,7 @@ def main():
             if hit and wl.name == "cfg2":
                 traffic = {"dram_bytes": int(hit[0]["dram_bytes"]), "pcie_read_bytes": int(hit[0]["pcie_read_bytes"]),
                            "pcie_write_bytes": int(hit[0]["pcie_write_bytes"])}
-                tsrc = "profiles/" + hit[0]["report"] + " (ncu --set full, one launch, cfg2)"
+                tsrc = "profiles/ncu/" + hit[0]["report"] + " (ncu --set full, one launch, cfg2)"
         except Exception:
             pass
         roof = {"bound": "pcie", "kernel": kname, "achieved": round(ach, 2), "peak": round(pcie_peak, 2),
