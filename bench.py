@@ -518,7 +518,7 @@ def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=10, steps=8):
     return res
 
 
-def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, warm=60, steps=30):
+def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, warm=50, steps=30, gsteps=20):
     """The same workload with a cache that holds the whole table (lines_per_gpu = N): after
     warm-up nearly every request hits, the storage tier drops out, and the step is bound by
     HBM — k_serve reads each requested row from its slot and writes it to `out`. Reports the
@@ -552,6 +552,21 @@ def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, 
     prof = c.profile_read()
     c.profile(False)
     s1 = c.stats(1)
+    # the same step as CUDA-graph replays (launch gaps removed)
+    gsteps = max(0, min(gsteps, len(ids_d) - W - 1 - (warm + steps)))
+    graph = None
+    if gsteps:
+        c.graph_capture(ids_d, out)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        g0.record(st)
+        for _ in range(gsteps):
+            c.graph_replay()
+        g1.record(st)
+        torch.cuda.synchronize()
+        tg = g0.elapsed_time(g1) / 1e3
+        gb = sum(ids_d[warm + steps + i].numel() for i in range(gsteps)) * wl.R
+        graph = {"steps": gsteps, "value": round(gb / tg / 1e9, 2), "ms_per_step": round(tg / gsteps * 1e3, 4)}
     c.close()
     T = e0.elapsed_time(e1) / 1e3
     d = {k: s1[k] - s0[k] for k in s1 if k != "iter"}
@@ -561,7 +576,7 @@ def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, 
     ach = alg / (serve_ms / 1e3) / 1e9 if serve_ms > 0 else 0.0
     return {"lines_per_gpu": lines, "warmup": warm, "steps": steps,
             "value": round(d["requests"] * R / T / 1e9, 2), "unit": "GB/s", "ms_per_step": round(T / steps * 1e3, 4),
-            "hit_ratio": round(d["hits"] / max(d["unique"], 1), 4),
+            "hit_ratio": round(d["hits"] / max(d["unique"], 1), 4), "graph_replay": graph,
             "phases_ms_per_step": {k: round(v[0] / steps, 4) for k, v in prof.items()},
             "roofline": {"bound": "hbm", "kernel": "k_serve", "achieved": round(ach, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "peak_source": hbm_src,
