@@ -136,7 +136,8 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
  * gather then reads the rows its fills need (known once replacement has run) with
  * parallel pread into a pinned bounce buffer that the fill kernel reads over PCIe — a host
  * step in the middle of the gather (it synchronises `stream` once); graph capture is
- * refused in this mode. Open/read failures return LSMGNN_EIO. Exactly one of the two
+ * refused in this mode. Open/read failures return LSMGNN_EIO (a read failure is sticky:
+ * the cache already recorded the rows). Exactly one of the two
  * arguments must be non-NULL. */
 int lsmgnn_attach_storage(const void* host_rows_for_my_home, const char* nvme_path);
 

@@ -76,9 +76,9 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
 
 // Close the record: algorithmic bytes per tier, cumulative sums; the staging count of
 // the next parity is reset so that a missing PVP call stages nothing. The ERANGE counter is
-// mirrored to pinned host memory; a graph replay advances it->t_next.
+// mirrored to pinned host memory; it->t_next = t + 1 (the next graph replay's iteration).
 __global__ void k_end(IterState* it, unsigned long long* hist, unsigned long long* cum, Scratch* scr, uint32_t R,
-                      volatile uint32_t* bad_mirror, uint32_t advance) {
+                      volatile uint32_t* bad_mirror) {
   __shared__ unsigned long long s_rec[F_NFIELDS];
   const int f = threadIdx.x;  // one field per thread (blockDim = 32 >= F_NFIELDS)
   const uint64_t t = it->t;
@@ -102,7 +102,6 @@ __global__ void k_end(IterState* it, unsigned long long* hist, unsigned long lon
     *bad_mirror = scr->bad_ids;
     it->t_next = t + 1;  // direct calls and graph replays may be mixed
   }
-  (void)advance;
 }
 
 // Start the window feed of one batch (iteration wk): k_host >= 0 from the host, else (graph

@@ -226,6 +226,7 @@ int check_sticky() {
     return set_err(g.sticky, "a device-resident batch length exceeded max_batch_ids (sticky; clamped)");
   }
   if (g.bad_host && *g.bad_host) g.sticky = LSMGNN_ERANGE;
+  if (g.sticky == LSMGNN_EIO) return set_err(g.sticky, "an earlier storage read failed (sticky)");
   if (g.sticky) return set_err(g.sticky, "a node id >= num_nodes was passed (sticky)");
   return 0;
 }
@@ -581,7 +582,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     }
   }
   prof_end(5, st);
-  k_end<<<1, 32, 0, st>>>(g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev, graph ? 1u : 0u);
+  k_end<<<1, 32, 0, st>>>(g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev);
   LAUNCHED();
   return 0;
 }
@@ -718,7 +719,10 @@ int read_storage_rows(cudaStream_t st) {
   for (int i = 1; i < nt; ++i) pool.emplace_back(work);
   work();
   for (auto& th : pool) th.join();
-  if (err.load()) return set_err(LSMGNN_EIO, "storage read failed: %s", std::strerror(err.load()));
+  if (err.load()) {  // the cache already holds tags for rows that never arrived: sticky
+    g.sticky = LSMGNN_EIO;
+    return set_err(LSMGNN_EIO, "storage read failed: %s", std::strerror(err.load()));
+  }
   return 0;
 }
 
