@@ -419,7 +419,9 @@ def main():
                    else wl.name, "N": wl.N, "row_bytes": R, "payload": "fp32 rows (1024-dim), copied bytewise",
                    "batch_per_rank": wl.batch, "fanout": list(wl.fanout), "lines_per_gpu": lines, "ways": wl.ways,
                    "window": W, "threshold": max(1, W // 8), "policy": args.policy, "pvp": pvp,
-                   "victim_lines": wl.victim_lines if pvp else 0, "parallelism": f"shared cache over {G} GPU",
+                   "victim_lines": wl.victim_lines if pvp else 0, "parallelism": f"shared cache over {G} GPU" if ndev >= G else
+                   f"shared cache over {G} homes on {ndev} GPU (ranks share a device: protocol test, not a "
+                   f"multi-GPU throughput)",
                    "l2": "inputs larger than L2: cache 400 MB, out ~550 MB/step, host table 4 GB",
                    "seeds": wl.seeds},
         "gpu_launches": int(launches),
