@@ -99,7 +99,8 @@ def test_multiprocess_edge_cases(tmp_path, G, case):
         assert np.array_equal(hg, ho[:, r, :]), (case, r, np.argwhere(hg != ho[:, r, :])[:3])
 
 
-@pytest.mark.parametrize("G,policy,pvp", [(2, "hybrid", 1), (2, "lru", 0), (3, "hybrid", 0), (4, "static", 1)])
+@pytest.mark.parametrize("G,policy,pvp", [(2, "hybrid", 1), (2, "lru", 0), (3, "hybrid", 0), (4, "static", 1),
+                                         (8, "hybrid", 1), (8, "hybrid", 0)])
 def test_multiprocess_parity(tmp_path, G, policy, pvp):
     launch(G, tmp_path, "gather", str(tmp_path), policy, str(pvp))
     N, D = 16384, 128
