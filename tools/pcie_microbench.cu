@@ -291,6 +291,29 @@ int main(int argc, char** argv) {
         printf("duplex: SM H2D reads %.2f GB/s (%.3f ms) || SM D2H stores %.2f GB/s (%.3f ms)\n",
                (double)n * R / ma / 1e6, ma, (double)n * R / mb / 1e6, mb);
     }
+    // same direction: SM zero-copy H2D reads of scattered rows || copy-engine H2D of a
+    // contiguous block — is 51.5 GB/s a limit of the SM read path or of the link?
+    uint8_t* dce;
+    CK(cudaMalloc(&dce, (size_t)n * R));
+    for (int it = 0; it < 3; ++it) {
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(a0, 0);
+      cudaStreamWaitEvent(sa, a0, 0);
+      cudaStreamWaitEvent(sb, a0, 0);
+      k_ldg<8, 0><<<4 * sms, 256, 0, sa>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16);
+      cudaEventRecord(a1, sa);
+      cudaMemcpyAsync(dce, host + (size_t)n * R, (size_t)n * R, cudaMemcpyHostToDevice, sb);
+      cudaEventRecord(b1, sb);
+      CK(cudaDeviceSynchronize());
+      float ma, mb;
+      cudaEventElapsedTime(&ma, a0, a1);
+      cudaEventElapsedTime(&mb, a0, b1);
+      if (it == 2)
+        printf("same direction: SM H2D reads %.2f GB/s (%.3f ms) || CE H2D %.2f GB/s (%.3f ms); both done in %.3f ms "
+               "= %.2f GB/s total\n", (double)n * R / ma / 1e6, ma, (double)n * R / mb / 1e6, mb, std::max(ma, mb),
+               2.0 * n * R / std::max(ma, mb) / 1e6);
+    }
+    cudaFree(dce);
   }
   CK(cudaGetLastError());
   // correctness of one row
