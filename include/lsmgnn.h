@@ -7,7 +7,7 @@
  * (§4.2), a victim buffer in pinned host memory and its Preemptive
  * Victim-buffer Prefetcher (§4.3), and a host-resident backing table that
  * stands in for the SSD tier. DESIGN.md states every reading taken where the
- * paper is silent (R1..R25) and the data layout.
+ * paper is silent (R1..R27) and the data layout.
  *
  * Process model: one process per GPU ("DDP leverages multi-processing");
  * rank r of G is the home of every node v with v mod G == r (R1).
