@@ -19,6 +19,9 @@
 #include <atomic>
 #include <cerrno>
 #include <cstdlib>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <cstdarg>
 #include <cstdio>
@@ -41,6 +44,82 @@ struct Handle {  // exported per rank for lsmgnn_connect
   uint64_t arena_bytes;
   uint64_t layout_sig;
   int32_t rank, world;
+};
+
+// Persistent worker threads of the file tier (N2): started when a storage file is attached,
+// parked on a condition variable between batches. run(n, fn) hands entries 0..n-1 out in
+// chunks of 64 through an atomic cursor to the workers and the calling thread; it returns
+// the first nonzero fn result (an errno), after which the remaining entries are skipped.
+class IoPool {
+ public:
+  void start(int nthreads) {
+    for (int i = 0; i < nthreads; ++i) th_.emplace_back([this] { worker(); });
+  }
+  void stop() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      quit_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+    th_.clear();
+  }
+  int run(uint32_t n, const std::function<int(uint32_t)>& fn) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      n_ = n;
+      fn_ = &fn;
+      next_.store(0);
+      err_.store(0);
+      active_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return active_ == 0; });
+    fn_ = nullptr;
+    return err_.load();
+  }
+
+ private:
+  void drain() {
+    for (;;) {
+      const uint32_t e0 = next_.fetch_add(64);
+      if (e0 >= n_ || err_.load()) return;
+      const uint32_t e1 = std::min(n_, e0 + 64);
+      for (uint32_t e = e0; e < e1; ++e)
+        if (int rc = (*fn_)(e)) {
+          int zero = 0;
+          err_.compare_exchange_strong(zero, rc);
+          return;
+        }
+    }
+  }
+  void worker() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return quit_ || gen_ != seen; });
+        if (quit_) return;
+        seen = gen_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--active_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  bool quit_ = false;
+  int active_ = 0;
+  uint32_t n_ = 0;
+  const std::function<int(uint32_t)>* fn_ = nullptr;
+  std::atomic<uint32_t> next_{0};
+  std::atomic<int> err_{0};
 };
 
 struct Ctx {
@@ -106,6 +185,7 @@ struct Ctx {
   uint8_t* bounce_host = nullptr;
   FillEnt* fills_host = nullptr;  // pinned copy of the fill list
   uint32_t* nfill_host = nullptr;
+  IoPool* io = nullptr;  // persistent pread workers (io_threads - 1; the caller is one more)
   int io_threads = 64;  // pread workers per batch (LSMGNN_IO_THREADS); deeper queues help NVMe
   volatile uint32_t* bad_host = nullptr;  // pinned mirror: [0] scr->bad_ids, [1] batch-length overflow
   uint32_t* bad_dev_overflow = nullptr;   // device mapping of bad_host + 1
@@ -347,6 +427,7 @@ void prof_end(int ph, cudaStream_t st) {
   g.open_ev[ph] = nullptr;
 }
 
+void detach_file();  // file tier (below)
 int free_all() {
   cudaDeviceSynchronize();
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off, g.scan_set, g.scan_q,
@@ -367,10 +448,7 @@ int free_all() {
   if (g.qrows_host) cudaFreeHost(g.qrows_host);
   if (g.bad_host) cudaFreeHost((void*)g.bad_host);
   if (g.table_registered) cudaHostUnregister((void*)g.table_host);
-  if (g.file_fd >= 0) close(g.file_fd);
-  if (g.bounce_host) cudaFreeHost(g.bounce_host);
-  if (g.fills_host) cudaFreeHost(g.fills_host);
-  if (g.nfill_host) cudaFreeHost(g.nfill_host);
+  detach_file();
   if (g.graph_exec) cudaGraphExecDestroy(g.graph_exec);
   if (g.graph) cudaGraphDestroy(g.graph);
   if (g.cap_stream) cudaStreamDestroy(g.cap_stream);
@@ -643,6 +721,11 @@ int launch_pvp(cudaStream_t st) {
 
 // ---- file tier (N2)
 void detach_file() {
+  if (g.io) {
+    g.io->stop();
+    delete g.io;
+    g.io = nullptr;
+  }
   if (g.file_fd >= 0) close(g.file_fd);
   g.file_fd = -1;
   if (g.bounce_host) cudaFreeHost(g.bounce_host);
@@ -677,6 +760,8 @@ int attach_file(const char* path, uint64_t rows) {
   g.table_dev = reinterpret_cast<const uint8_t*>(dp);
   g.table_host = nullptr;
   if (const char* nt = std::getenv("LSMGNN_IO_THREADS")) g.io_threads = std::max(1, std::atoi(nt));
+  g.io = new IoPool();
+  g.io->start(g.io_threads - 1);
   return 0;
 }
 // Read the storage rows of this batch's fills into the bounce buffer (row e = fill e).
@@ -688,40 +773,25 @@ int read_storage_rows(cudaStream_t st) {
   if (n == 0) return 0;
   CK(cudaMemcpyAsync(g.fills_host, g.fills, (size_t)n * sizeof(FillEnt), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  std::atomic<uint32_t> next{0};
-  std::atomic<int> err{0};
   const uint64_t R = g.R;
-  auto work = [&]() {
-    for (;;) {
-      const uint32_t e0 = next.fetch_add(64);
-      if (e0 >= n || err.load()) return;
-      const uint32_t e1 = std::min(n, e0 + 64);
-      for (uint32_t e = e0; e < e1; ++e) {
-        const FillEnt f = g.fills_host[e];
-        if (!(f.src & kHostBit)) continue;  // PVP staging row: already in HBM
-        uint8_t* dst = g.bounce_host + (size_t)e * R;
-        const off_t off = (off_t)(f.src & ~kHostBit) * (off_t)R;
-        size_t done = 0;
-        while (done < R) {
-          const ssize_t r = pread(g.file_fd, dst + done, R - done, off + (off_t)done);
-          if (r <= 0) {
-            if (r < 0 && errno == EINTR) continue;
-            err.store(r < 0 ? errno : EIO);
-            return;
-          }
-          done += (size_t)r;
-        }
-      }
+  const std::function<int(uint32_t)> read_one = [R](uint32_t e) -> int {
+    const FillEnt f = g.fills_host[e];
+    if (!(f.src & kHostBit)) return 0;  // PVP staging row: already in HBM
+    uint8_t* dst = g.bounce_host + (size_t)e * R;
+    const off_t off = (off_t)(f.src & ~kHostBit) * (off_t)R;
+    size_t done = 0;
+    while (done < R) {
+      const ssize_t r = pread(g.file_fd, dst + done, R - done, off + (off_t)done);
+      if (r < 0 && errno == EINTR) continue;
+      if (r <= 0) return r < 0 ? errno : EIO;
+      done += (size_t)r;
     }
+    return 0;
   };
-  const int nt = (int)std::min<uint32_t>((uint32_t)g.io_threads, (n + 63) / 64);
-  std::vector<std::thread> pool;
-  for (int i = 1; i < nt; ++i) pool.emplace_back(work);
-  work();
-  for (auto& th : pool) th.join();
-  if (err.load()) {  // the cache already holds tags for rows that never arrived: sticky
+  const int err = g.io->run(n, read_one);
+  if (err) {  // the cache already holds tags for rows that never arrived: sticky
     g.sticky = LSMGNN_EIO;
-    return set_err(LSMGNN_EIO, "storage read failed: %s", std::strerror(err.load()));
+    return set_err(LSMGNN_EIO, "storage read failed: %s", std::strerror(err));
   }
   return 0;
 }
