@@ -122,6 +122,8 @@ def run_reference(args, wl, G, rank):
         return
     import oracle
     from tests.harness import table_for
+    core = gpu_local_cpu(0)
+    os.sched_setaffinity(0, {core})  # one core, NUMA-local to GPU 0 when sysfs says which
     K, Wu = args.steps, args.warmup
     pvp = wl.pvp if args.pvp is None else args.pvp
     iters = Wu + K + wl.window + 1
@@ -150,7 +152,8 @@ def run_reference(args, wl, G, rank):
                        "N": wl.N, "row_bytes": wl.R, "batch_per_rank": wl.batch, "fanout": list(wl.fanout),
                        "lines_per_gpu": args.lines or wl.lines_per_gpu, "ways": wl.ways, "window": wl.window,
                        "policy": args.policy, "pvp": pvp},
-            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "host": host_cpu(),
+            "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "host": dict(host_cpu(), pinned_cpu=core),
                              "sample": f"full {wl.name} iterations {Wu}..{Wu + K - 1} after {Wu} untimed, rows "
                                        f"materialised by memcpy from the host table, single thread"},
             "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -170,9 +173,37 @@ def host_cpu() -> dict:
     return {"model": model, "nproc": os.cpu_count(), "threads_used": 1}
 
 
+def gpu_local_cpu(dev_index: int = 0):
+    """First CPU of the NUMA node local to the GPU (sysfs local_cpulist), else the first CPU
+    this process may run on."""
+    try:
+        import torch
+        bus = torch.cuda.get_device_properties(dev_index).pci_bus_id.lower()  # e.g. 0000:1b:00.0
+        txt = open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+        first = int(txt.split(",")[0].split("-")[0])
+        if first in os.sched_getaffinity(0):
+            return first
+    except Exception:
+        pass
+    return min(os.sched_getaffinity(0))
+
+
 def cpu_baseline(wl, G, trace, scores, table_np, args, lines):
-    """The oracle as it stands, timed on this host: a bounded sample (about args.cpu_seconds)."""
+    """The oracle as it stands, timed on this host: a bounded sample (about args.cpu_seconds),
+    pinned to one core NUMA-local to GPU 0."""
     import oracle
+    core = gpu_local_cpu(0)
+    saved = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, {core})
+    try:
+        res = _cpu_baseline(wl, G, trace, scores, table_np, args, lines, oracle)
+    finally:
+        os.sched_setaffinity(0, saved)
+    res["host"]["pinned_cpu"] = core
+    return res
+
+
+def _cpu_baseline(wl, G, trace, scores, table_np, args, lines, oracle):
     pvp = wl.pvp if args.pvp is None else args.pvp
     o = oracle.Oracle(G, wl.N, wl.R, lines, wl.ways, scores, policy=args.policy, pvp=pvp, W=wl.window,
                       V=wl.victim_lines)
