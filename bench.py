@@ -479,16 +479,29 @@ def main():
         line["cpu_baseline"] = cpu_baseline(wl, G, trace, scores, table.numpy(), args, lines)
     c.close()
     if not args.no_ablation and G == 1:
-        line["pvp_ablation"] = pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev)
-        line["gpu_sampler_pipeline"] = gpu_sampler_pipeline(wl, g_, scores, table, lines, args, dev)
-        line["storage_per_epoch"] = epoch_storage(wl, g_, scores, lines, dev)
-        line["hbm_regime"] = hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src)
+        line["pvp_ablation"] = optional(pvp_ablation, wl, scores, table, ids_d, lines, args, max_ids, dev)
+        line["gpu_sampler_pipeline"] = optional(gpu_sampler_pipeline, wl, g_, scores, table, lines, args, dev)
+        line["storage_per_epoch"] = optional(epoch_storage, wl, g_, scores, lines, dev)
+        line["hbm_regime"] = optional(hbm_regime, wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src)
         if not args.no_file_tier:
-            line["file_tier"] = file_tier(wl, scores, ids_d, lines, args, max_ids, dev)
+            line["file_tier"] = optional(file_tier, wl, scores, ids_d, lines, args, max_ids, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if G > 1:
         torch.distributed.destroy_process_group()
+
+
+def optional(fn, *a):
+    """Run one of the extra measurements; a failure (e.g. no room for the file tier's file)
+    is recorded in its place instead of losing the bench line, and the library is reset."""
+    try:
+        return fn(*a)
+    except Exception as e:  # noqa: BLE001 — reported, not swallowed
+        log(f"[bench] {fn.__name__} failed: {e!r}")
+        from paper_2407_15264_b200 import binding
+        if binding._LIB is not None:
+            binding._LIB.lsmgnn_finalize()
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
 
 
 def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=10, steps=8):
@@ -497,14 +510,22 @@ def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=10, steps=8):
     the rows its fills need with parallel pread into a pinned bounce buffer; variants:
     O_DIRECT (every storage row is a device read) and buffered after the file was just
     written (page-cache hits: the tier's software overhead without the device)."""
-    import torch
-    from paper_2407_15264_b200 import LsmGnn
     from tests.harness import write_table_file
-    W = wl.window
-    st = torch.cuda.current_stream()
     path = os.path.join(args.file_dir, f"lsmgnn_{wl.name}_home0.bin")
     t0 = time.time()
-    write_table_file(path, wl.N, wl.D, wl.seeds["f"])
+    try:
+        write_table_file(path, wl.N, wl.D, wl.seeds["f"])
+        return _file_tier_runs(wl, scores, ids_d, lines, args, max_ids, dev, warm, steps, path, t0)
+    finally:
+        if os.path.exists(path):
+            os.remove(path)
+
+
+def _file_tier_runs(wl, scores, ids_d, lines, args, max_ids, dev, warm, steps, path, t0):
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    W = wl.window
+    st = torch.cuda.current_stream()
     res = {"file": path, "file_GB": round(os.path.getsize(path) / 1e9, 3), "write_s": round(time.time() - t0, 1),
            "steps": steps, "warmup": warm, "what": "backing rows in a file; fills read with pread (64 threads) into a "
            "pinned bounce buffer, then the fill kernel as usual; gather GB/s = requested bytes / step time"}
@@ -544,10 +565,6 @@ def file_tier(wl, scores, ids_d, lines, args, max_ids, dev, warm=10, steps=8):
                      "storage_read_GBps": round(d["bytes_h2d_storage"] / fill_s / 1e9, 3) if fill_s else None,
                      "fill_share_of_step": round(fill_s / T, 4),
                      "victim_hit_ratio": round(d["victim_hits"] / max(d["unique"], 1), 4)}
-    try:
-        os.remove(path)
-    except OSError:
-        pass
     return res
 
 
