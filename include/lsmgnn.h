@@ -112,7 +112,7 @@ int lsmgnn_set_options(const lsmgnn_options* opt);
  * set(v) = floor(v / G) mod S, R2), the window reuse mask, staging areas and, when
  * pvp = 1, W victim queues of floor(victim_lines / W) rows in pinned host memory
  * ("data ... victim buffers", "16K cache-lines" each; R13).
- *   num_nodes      N; node IDs are 0 .. N-1
+ *   num_nodes      N; node IDs are 0 .. N-1; N < 2^32 - 16 and ceil(N / G) < 2^31
  *   feat_dim, dtype  row bytes R = feat_dim * sizeof(dtype); R % 16 must be 0
  *   lines_per_gpu  L (> 0, multiple of ways), ways A in 1..32
  *   victim_lines   V (ignored when pvp = 0)

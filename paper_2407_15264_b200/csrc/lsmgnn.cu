@@ -868,6 +868,8 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   g.L = (uint64_t)lines_per_gpu;
   g.S = g.L / g.A;
   g.Q = (g.N + G - 1) / G;
+  if (g.Q >= (uint64_t)kHostBit)  // FillEnt::src keeps a home row index in 31 bits
+    return set_err(LSMGNN_EINVAL, "ceil(num_nodes / world) must be < 2^31 (use more homes)");
   g.W = (uint32_t)g.opt.window;
   g.Wp1 = g.W + 1;
   g.T = g.opt.threshold ? (uint32_t)g.opt.threshold : std::max<uint32_t>(1, g.W / 8);

@@ -134,6 +134,8 @@ def test_abi_errors():
         LsmGnn(100, 3, 16, 4)  # R = 12 bytes: not a multiple of 16
     with pytest.raises(LsmGnnError):
         LsmGnn(100, 4, 18, 4)  # lines not a multiple of ways
+    with pytest.raises(LsmGnnError, match="2\\^31"):
+        LsmGnn(2**31 + 8, 4, 64, 8, max_batch_ids=8)  # one home cannot index 2^31 rows in a fill record
     c = LsmGnn(100, 4, 16, 4, max_batch_ids=8)
     import torch
     ids = torch.zeros(9, dtype=torch.int64, device="cuda")
