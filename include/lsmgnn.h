@@ -171,7 +171,11 @@ int lsmgnn_gather_host(const int64_t* host_ids, int64_t n, void* host_out, void*
  *  - Each later call, after gather(t), feeds the single batch t + 1 + W (an empty
  *    batch past the end of the trace) and launches the PVP copy of victim queue
  *    (t+1) mod W into home staging on a side stream (R17); gather(t+1)
- *    waits for it with an event. */
+ *    waits for it with an event.
+ *  - `stream` may differ from the gather stream: the library orders the two with events
+ *    (the feed of t+1+W waits only for gather(t-1), the last gather that reads its mask
+ *    bit; gather(t+1) waits for the feed; the PVP copy waits for gather(t)), so a feed on
+ *    its own stream overlaps gather(t). The ids must be ready on `stream`. */
 int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batches,
                     int64_t first_iter, void* stream);
 

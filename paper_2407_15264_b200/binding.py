@@ -194,12 +194,15 @@ class LsmGnn:
 
     def prefetch(self, batches, first_iter: int, stream=None) -> None:
         """Feed window batches (list of int64 CUDA tensors) for iterations first_iter.. ."""
+        import contextlib
         import torch
-        if len(batches):
-            flat = torch.cat([b.reshape(-1) for b in batches]) if len(batches) > 1 else batches[0].reshape(-1)
-            flat = flat.contiguous()
-        else:
-            flat = torch.zeros(1, dtype=torch.int64, device=self.device)
+        # the concatenation (a device copy) is ordered on the stream the library will read it on
+        with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+            if len(batches):
+                flat = torch.cat([b.reshape(-1) for b in batches]) if len(batches) > 1 else batches[0].reshape(-1)
+                flat = flat.contiguous()
+            else:
+                flat = torch.zeros(1, dtype=torch.int64, device=self.device)
         offs = np.zeros(len(batches) + 1, np.int64)
         offs[1:] = np.cumsum([b.numel() for b in batches])
         self._last_flat = flat  # keep alive until the stream consumes it

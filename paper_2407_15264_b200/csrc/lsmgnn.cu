@@ -170,6 +170,8 @@ struct Ctx {
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t cap_stream2 = nullptr;  // the window-feed branch of the captured step
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t graph_launches = 0;  // kernels per replay
   bool graph_out_host = false;
 
@@ -195,6 +197,12 @@ struct Ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
+  // cross-stream order (callers may gather and prefetch on different streams): the end of
+  // gather t is ev_gend[t & 7] (gend_t says which t it holds); the last window feed is ev_feed
+  cudaEvent_t ev_gend[8] = {};
+  int64_t gend_t[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  cudaEvent_t ev_feed = nullptr;
+  bool feed_recorded = false, feed_since_gather = false;
   cudaStream_t last_stream = nullptr;
   int64_t* tmp_ids = nullptr;  // for lsmgnn_gather_host
   void* tmp_out = nullptr;
@@ -452,8 +460,14 @@ int free_all() {
   if (g.graph_exec) cudaGraphExecDestroy(g.graph_exec);
   if (g.graph) cudaGraphDestroy(g.graph);
   if (g.cap_stream) cudaStreamDestroy(g.cap_stream);
+  if (g.cap_stream2) cudaStreamDestroy(g.cap_stream2);
+  if (g.ev_fork) cudaEventDestroy(g.ev_fork);
+  if (g.ev_join) cudaEventDestroy(g.ev_join);
   if (g.side) cudaStreamDestroy(g.side);
   if (g.ev_main) cudaEventDestroy(g.ev_main);
+  for (auto e : g.ev_gend)
+    if (e) cudaEventDestroy(e);
+  if (g.ev_feed) cudaEventDestroy(g.ev_feed);
   if (g.ev_pvp) cudaEventDestroy(g.ev_pvp);
   for (auto& sp : g.spans) {
     cudaEventDestroy(sp.a);
@@ -697,10 +711,52 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
   return 0;
 }
 
-// S11: PVP copy of victim queue (t+1) mod W on the side stream, after gather(t) (R17).
+// ---- cross-stream order of gathers, window feeds and the PVP copy
+int note_gather_end(int64_t t, cudaStream_t st) {
+  const int i = (int)(t & 7);
+  if (!g.ev_gend[i]) CK(cudaEventCreateWithFlags(&g.ev_gend[i], cudaEventDisableTiming));
+  CK(cudaEventRecord(g.ev_gend[i], st));
+  g.gend_t[i] = t;
+  return 0;
+}
+// `st` waits for the end of gather t (t < 0: nothing to wait for). If that record was
+// overwritten, wait for every recorded gather (conservative, still correct).
+int wait_gather_end(int64_t t, cudaStream_t st) {
+  if (t < 0) return 0;
+  const int i = (int)(t & 7);
+  if (g.gend_t[i] == t) {
+    CK(cudaStreamWaitEvent(st, g.ev_gend[i], 0));
+    return 0;
+  }
+  for (int j = 0; j < 8; ++j)
+    if (g.gend_t[j] >= 0) CK(cudaStreamWaitEvent(st, g.ev_gend[j], 0));
+  return 0;
+}
+// Before feeding iteration k: the previous feed (IterState window fields, ring order) and
+// gather(k - W - 2), the last gather that reads mask bit / ring slot k mod (W+1).
+int feed_begin(int64_t k, cudaStream_t st) {
+  if (g.feed_recorded) CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+  return wait_gather_end(k - (int64_t)g.W - 2, st);
+}
+int feed_end(cudaStream_t st) {
+  if (!g.ev_feed) CK(cudaEventCreateWithFlags(&g.ev_feed, cudaEventDisableTiming));
+  CK(cudaEventRecord(g.ev_feed, st));
+  g.feed_recorded = g.feed_since_gather = true;
+  return 0;
+}
+
+// S11: PVP copy of victim queue (t+1) mod W on the side stream, after gather(t) (R17): it
+// rewrites staging parity (t+1) & 1, last read by gather(t-1), and reads queue (t+1) mod W,
+// last appended to by gather(t).
 int launch_pvp(cudaStream_t st) {
-  CK(cudaEventRecord(g.ev_main, st));
-  CK(cudaStreamWaitEvent(g.side, g.ev_main, 0));
+  const int64_t t = g.t_next - 1;
+  if (g.gend_t[t & 7] == t) {
+    if (int rc = wait_gather_end(t, g.side)) return rc;
+    if (int rc = wait_gather_end(t - 1, g.side)) return rc;
+  } else {  // gather(t) was not noted (cannot happen through the C-ABI): order after st
+    CK(cudaEventRecord(g.ev_main, st));
+    CK(cudaStreamWaitEvent(g.side, g.ev_main, 0));
+  }
   uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
   const int blocks = g.sms * std::min(2, g.geom_per_sm);
   prof_begin(7, g.side);
@@ -1088,8 +1144,13 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     CK(cudaStreamWaitEvent(st, g.ev_pvp, 0));
     g.pvp_pending = false;
   }
+  if (g.feed_since_gather) {  // the window fed through t+W (possibly on another stream)
+    CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+    g.feed_since_gather = false;
+  }
   const BeginArgs ba = begin_args(t, node_ids, n, nullptr, nullptr, 0);
   if (int rc = launch_gather(ba, n, out, out_host, false, (uint32_t)(t + 1), st)) return rc;
+  if (int rc = note_gather_end(t, st)) return rc;
   g.t_next = t + 1;
   g.last_stream = st;
   return 0;
@@ -1110,8 +1171,10 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
     const int64_t n = offsets[b + 1] - offsets[b];
     if (n < 0 || (uint64_t)n > g.cap) return set_err(LSMGNN_EINVAL, "window batch of %lld ids", (long long)n);
     if (k > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
+    if (int rc = feed_begin(k, st)) return rc;
     if (int rc = launch_window(k, n > 0 ? ids + offsets[b] : nullptr, n, nullptr, nullptr, nullptr, 0, n, st))
       return rc;
+    if (int rc = feed_end(st)) return rc;
     g.feed_next = k + 1;
   }
   if (num_batches > 0) prof_end(6, st);
@@ -1337,7 +1400,9 @@ int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t fi
   if (first_iter > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   prof_begin(6, st);
+  if (int rc = feed_begin(first_iter, st)) return rc;
   if (int rc = launch_window(first_iter, ids, 0, count_dev, nullptr, nullptr, 0, (int64_t)g.cap, st)) return rc;
+  if (int rc = feed_end(st)) return rc;
   prof_end(6, st);
   g.feed_next = first_iter + 1;
   // the PVP copy for t+1 is issued by lsmgnn_prefetch; call it with num_batches = 0 when needed
@@ -1369,13 +1434,28 @@ int lsmgnn_graph_capture(const int64_t* const* ids_ring, const int64_t* n_ring, 
     g.graph = nullptr;
   }
   if (!g.cap_stream) CK(cudaStreamCreateWithFlags(&g.cap_stream, cudaStreamNonBlocking));
+  if (!g.cap_stream2) CK(cudaStreamCreateWithFlags(&g.cap_stream2, cudaStreamNonBlocking));
+  if (!g.ev_fork) CK(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+  if (!g.ev_join) CK(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
   const bool prof = g.prof;
   g.prof = false;  // no host-side event spans inside a graph
   const int64_t l0 = g.launches;
+  // Two branches: gather(t) and the window feed of t+1+W. They touch disjoint data — the
+  // feed rewrites ring slot / mask bit t mod (W+1), which gather(t) never reads (it looks
+  // at t+1..t+W) — so they run concurrently; the feed only has to follow gather(t-1),
+  // which the previous replay on the same stream guarantees.
   CK(cudaStreamBeginCapture(g.cap_stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t fe = cudaEventRecord(g.ev_fork, g.cap_stream);
+  if (fe == cudaSuccess) fe = cudaStreamWaitEvent(g.cap_stream2, g.ev_fork, 0);
   const BeginArgs ba = begin_args(-1, nullptr, 0, ids_ring, n_ring, (uint32_t)ring_len);
-  int rc = launch_gather(ba, (int64_t)g.cap, out, out_host, true, 0, g.cap_stream);
-  if (!rc) rc = launch_window(-1, nullptr, 0, nullptr, ids_ring, n_ring, (uint32_t)ring_len, (int64_t)g.cap, g.cap_stream);
+  int rc = fe == cudaSuccess ? launch_gather(ba, (int64_t)g.cap, out, out_host, true, 0, g.cap_stream)
+                             : set_err(LSMGNN_ECUDA, "graph fork: %s", cudaGetErrorString(fe));
+  if (!rc) rc = launch_window(-1, nullptr, 0, nullptr, ids_ring, n_ring, (uint32_t)ring_len, (int64_t)g.cap, g.cap_stream2);
+  if (!rc) {
+    fe = cudaEventRecord(g.ev_join, g.cap_stream2);
+    if (fe == cudaSuccess) fe = cudaStreamWaitEvent(g.cap_stream, g.ev_join, 0);
+    if (fe != cudaSuccess) rc = set_err(LSMGNN_ECUDA, "graph join: %s", cudaGetErrorString(fe));
+  }
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(g.cap_stream, &graph);
   g.prof = prof;
@@ -1401,7 +1481,14 @@ int lsmgnn_graph_replay(void* stream) {
     CK(cudaStreamWaitEvent(st, g.ev_pvp, 0));
     g.pvp_pending = false;
   }
+  if (g.feed_since_gather) {
+    CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+    g.feed_since_gather = false;
+  }
+  if (int rc = wait_gather_end(g.t_next - 1, st)) return rc;  // the replay's feed follows gather(t-1)
   CK(cudaGraphLaunch(g.graph_exec, st));
+  if (int rc = note_gather_end(g.t_next, st)) return rc;
+  if (int rc = feed_end(st)) return rc;  // the replay fed t+1+W itself
   g.launches += g.graph_launches;
   g.t_next += 1;
   g.feed_next += 1;
