@@ -381,7 +381,9 @@ int exchange_ids(int64_t n_bound, bool win, uint32_t seq, cudaStream_t st) {
   if (win) {  // the homes must have consumed the previous window round
     if (int rc = flags_wait_all(st, &myflags[3 * G], seq - 1)) return rc;
   }
-  CK(cudaMemsetAsync(g.route_cnt, 0, sizeof(uint32_t) * G, st));
+  // gather and window exchanges keep separate counters: they may run on different streams
+  uint32_t* rcnt = g.route_cnt + (win ? G : 0);
+  CK(cudaMemsetAsync(rcnt, 0, sizeof(uint32_t) * G, st));
   RouteArgs ra{};
   PublishArgs pa{};
   for (int h = 0; h < G; ++h) {
@@ -389,7 +391,7 @@ int exchange_ids(int64_t n_bound, bool win, uint32_t seq, cudaStream_t st) {
     ra.inbox[h] = (win ? win_of(base) : inbox_of(base)) + (size_t)g.rank * g.cap;
     pa.peer_cnt[h] = win ? wcnt_of(base) : icnt_of(base);
   }
-  ra.route_cnt = g.route_cnt;
+  ra.route_cnt = rcnt;
   ra.G = (uint32_t)G;
   pa.G = (uint32_t)G;
   pa.me = (uint32_t)g.rank;
@@ -397,7 +399,7 @@ int exchange_ids(int64_t n_bound, bool win, uint32_t seq, cudaStream_t st) {
     k_route_peer<<<grid_for(n_bound, 256, 4), 256, 0, st>>>(g.it, win ? 1u : 0u, g.N, ra, g.scr);
     LAUNCHED();
   }
-  k_route_publish<<<1, 32, 0, st>>>(g.route_cnt, pa);
+  k_route_publish<<<1, 32, 0, st>>>(rcnt, pa);
   LAUNCHED();
   const int slot = win ? 2 : 0;
   if (int rc = flags_write_all(st, (uint32_t)(slot * G + g.rank), seq)) return rc;
@@ -1001,7 +1003,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.qnode, std::max<uint64_t>(1, g.W * g.C));
   DA(g.qreuse, std::max<uint64_t>(1, g.W * g.C));
   DA(g.stg_nodes, std::max<uint64_t>(1, 2 * g.C));
-  DA(g.route_cnt, G);
+  DA(g.route_cnt, 2 * G);
   if (g.opt.update_period > 1) {
     DA(g.line_info, g.L);
     CK(cudaMemset(g.line_info, 0xFF, g.L * sizeof(uint32_t)));

@@ -29,7 +29,7 @@ def table_for(N: int, D: int, seed_f: int = 5, pinned: bool = False, home: int =
 
 def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1, table=None,
             check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False, P=1,
-            state_cb=None, storage_file=None):
+            state_cb=None, storage_file=None, two_streams=False):
     """Run trace[t][rank] through the library. Returns (history [K, 24] uint64, outs or None, bad_rows).
 
     check_rows: "full" compares every row with the closed form F(v); "none" skips it."""
@@ -50,14 +50,18 @@ def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0,
     dev = torch.device("cuda", torch.cuda.current_device())
     ids_d = [torch.from_numpy(x).to(dev) for x in mine]
     empty = torch.zeros(0, dtype=torch.int64, device=dev)
-    c.prefetch([ids_d[k] if k < K else empty for k in range(1, W + 1)], first_iter=1)
+    sb = None
+    if two_streams:  # window feeds on their own stream (the library orders them by events)
+        sb = torch.cuda.Stream()
+        torch.cuda.synchronize()
+    c.prefetch([ids_d[k] if k < K else empty for k in range(1, W + 1)], first_iter=1, stream=sb)
     outs = []
     bad = 0
     for t in range(K):
         out = torch.empty((max(1, ids_d[t].numel()), R), dtype=torch.uint8, device=dev)
         c.gather(ids_d[t], out)
         k = t + 1 + W
-        c.prefetch([ids_d[k] if k < K else empty], first_iter=k)
+        c.prefetch([ids_d[k] if k < K else empty], first_iter=k, stream=sb)
         if check_rows == "full" and ids_d[t].numel():
             host = out[: ids_d[t].numel()].cpu().numpy()
             nb, _ = synth.check_rows(host.view(np.uint32).reshape(-1, D), mine[t], D, seed_f)

@@ -66,7 +66,8 @@ def test_multiprocess_fuzz(tmp_path, G):
             assert np.array_equal(hg, ho[:, r, :]), (case, r, cfg, np.argwhere(hg != ho[:, r, :])[:3])
 
 
-@pytest.mark.parametrize("G,case", [(2, "ragged"), (3, "dups"), (2, "period"), (4, "rr"), (2, "file")])
+@pytest.mark.parametrize("G,case", [(2, "ragged"), (3, "dups"), (2, "period"), (4, "rr"), (2, "file"),
+                                    (3, "two_streams")])
 def test_multiprocess_edge_cases(tmp_path, G, case):
     """Ranks with empty batches, cross-rank duplicates, raw lists, victim-queue overflow,
     reinsert = 0, the periodic update and RR — per-home counters equal the oracle's."""
@@ -88,10 +89,13 @@ def test_multiprocess_edge_cases(tmp_path, G, case):
         cfg.update(policy="rr", pvp=0)
     if case == "file":  # NEXT N2: every home reads its rows from its own file (k_fill path)
         cfg.update(D=128, file=1)
+    if case == "two_streams":  # window feeds (and their exchange) on a second stream
+        cfg.update(two_streams=True)
     np.savez(tmp_path / "trace.npz", scores=sc, **{f"t{t}_r{r}": tr[t][r] for t in range(K) for r in range(G)})
     json.dump(cfg, open(tmp_path / "cfg.json", "w"))
     launch(G, tmp_path, "edge", str(tmp_path))
     cfg.pop("file", None)
+    cfg.pop("two_streams", None)
     ho = run_oracle(tr, G=G, scores=sc, **cfg)
     for r in range(G):
         assert json.load(open(tmp_path / f"r{r}.json"))["bad"] == 0
