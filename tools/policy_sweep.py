@@ -15,6 +15,7 @@ one ID space); training seeds = 10% of the paper range; fanout (5,2,2,2), batch 
 per GPU; W = 256, T = 32. Epoch 0 warms up, epoch 1 is measured (R23).
 
 usage: python tools/policy_sweep.py OUT.json [--nodes N] [--gpus 2,4,8] [--sizes 1,2,5,10,20]
+                                     [--window W] [--period P] [--policies ...] [--private] [--scores rpr]
 """
 from __future__ import annotations
 
@@ -46,7 +47,7 @@ def typed_trace(g, N, G, batch, fanout, iters_per_epoch, epochs, train, W, seed_
     return trace
 
 
-def run_point(trace_merged, N, lines, ways, scores, policy, pvp, W, V, iters_per_epoch):
+def run_point(trace_merged, N, lines, ways, scores, policy, pvp, W, V, iters_per_epoch, period=1):
     import torch
     from paper_2407_15264_b200 import LsmGnn
     D = 4  # 16-byte rows
@@ -54,7 +55,7 @@ def run_point(trace_merged, N, lines, ways, scores, policy, pvp, W, V, iters_per
     dev = torch.device("cuda", 0)
     ids = [torch.from_numpy(np.asarray(x, np.int64)).to(dev) for x in trace_merged]
     mb = max(1, max(x.numel() for x in ids))
-    c = LsmGnn(N, D, lines, ways, V, scores, policy=policy, pvp=pvp, window=W, max_batch_ids=mb)
+    c = LsmGnn(N, D, lines, ways, V, scores, policy=policy, pvp=pvp, window=W, max_batch_ids=mb, period=period)
     table = torch.zeros((N, 16), dtype=torch.uint8, pin_memory=True)
     c.attach_storage(table)
     empty = torch.zeros(0, dtype=torch.int64, device=dev)
@@ -87,10 +88,13 @@ def main():
     ap.add_argument("--private", action="store_true", help="add M-GIDS rows: independent per-GPU caches")
     ap.add_argument("--scores", default="degree", choices=["degree", "rpr"],
                     help="static information: degree, or reverse PageRank (the paper's choice, P:645)")
+    ap.add_argument("--window", type=int, default=256, help="W (the paper: 256, P:607; 64 in its W sweep)")
+    ap.add_argument("--period", type=int, default=1, help="dynamic-information update period P (the paper: 4)")
+    ap.add_argument("--no-pvp-row", action="store_true", help="skip the hybrid+PVP row")
     args = ap.parse_args()
     import synth
     N = args.nodes
-    W, ways, batch, fanout = 256, 32, 2048, (5, 2, 2, 2)
+    W, ways, batch, fanout = args.window, 32, 2048, (5, 2, 2, 2)
     n_paper = int(0.46 * N)
     train = np.arange(0, n_paper, 10, dtype=np.int64)  # 10% of the paper range (a typed ID range)
     t0 = time.time()
@@ -105,7 +109,7 @@ def main():
     results = {"workload": {"N": N, "typed_ranges": {"paper": [0, n_paper], "author": [n_paper, int(0.997 * N)],
                                                      "fos+institute": [int(0.997 * N), N]},
                             "train": int(train.size), "fanout": list(fanout), "batch_per_gpu": batch, "W": W,
-                            "T": W // 8, "ways": ways, "scores": "u8 rank-quantised " + ("reverse PageRank (d=0.85, tol 1e-6, <=100 it)"
+                            "T": max(1, W // 8), "period": args.period, "ways": ways, "scores": "u8 rank-quantised " + ("reverse PageRank (d=0.85, tol 1e-6, <=100 it)"
                                                                            if args.scores == "rpr" else "degree"), "row_bytes_run": 16,
                             "bytes_reported_for_row": 4096,
                             "note": "G-GPU runs executed as 1 home x G*L lines on merged batches (I8, exact "
@@ -119,11 +123,12 @@ def main():
         print(f"G={G}: {ipe} iterations/epoch, trace in {time.time() - t0:.0f}s", flush=True)
         for pct in [float(x) for x in args.sizes.split(",")]:
             lines_total = int(N * pct / 100) // (ways * G) * ways * G
-            runs = [(p, 0) for p in args.policies.split(",")] + [("hybrid", 1)]
+            runs = [(p, 0) for p in args.policies.split(",")] + ([] if args.no_pvp_row else [("hybrid", 1)])
             for pol, pvp in runs:
                 V = 16384 * W * G if pvp else 0
-                r = run_point(merged, N, lines_total, ways, scores, pol, pvp, W, V, ipe)
-                r.update({"G": G, "cache_pct": pct, "lines_per_gpu": lines_total // G, "policy": pol, "pvp": pvp})
+                r = run_point(merged, N, lines_total, ways, scores, pol, pvp, W, V, ipe, args.period)
+                r.update({"G": G, "cache_pct": pct, "lines_per_gpu": lines_total // G, "policy": pol, "pvp": pvp,
+                          "W": W, "P": args.period})
                 results["points"].append(r)
                 print(json.dumps(r), flush=True)
             # M-GIDS baseline: G independent PRIVATE caches of L lines each, every
