@@ -256,11 +256,18 @@ class LsmGnn:
     def kernel_launches() -> int:
         return int(load_library().lsmgnn_kernel_launches())
 
+    def __enter__(self) -> "LsmGnn":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
     def close(self) -> None:
         """Free this rank's home. With G > 1 every rank first drains its GPU work and meets the
         others at a barrier, so no peer is still pulling from memory about to be freed."""
-        if _LIB is None:
-            return
+        if _LIB is None or getattr(self, "_closed", False):
+            return  # (a second close must not free a home created after this one)
+        self._closed = True
         if self.world > 1:
             import torch
             import torch.distributed as dist
