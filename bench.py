@@ -235,7 +235,20 @@ def main():
     if args.impl == "reference":
         return run_reference(args, wl, G, rank)
 
+    # inputs first: the trace generator forks worker processes, best done before CUDA,
+    # NCCL and their threads exist in this process
+    K, Wu = args.steps, args.warmup
+    E = 0 if args.no_e2e else args.e2e_steps
+    W = wl.window
+    pvp = wl.pvp if args.pvp is None else args.pvp
+    lines = args.lines or wl.lines_per_gpu
+    GK = args.graph_steps if (G == 1 and not args.graph) else 0
+    iters = Wu + K + E + GK + W + 1
+    g_, trace, scores = build_inputs(wl, G, rank, iters, only_mine=G > 1)
+
     import torch
+    if not torch.cuda.is_available():
+        sys.exit("bench.py: no CUDA device — the gather path has no CPU fallback (use --impl reference for the oracle)")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     ndev = torch.cuda.device_count()
     local = local % ndev  # ranks may share a device on a 1-GPU pool (CUDA IPC within one GPU)
@@ -254,14 +267,6 @@ def main():
     from paper_2407_15264_b200 import LsmGnn
     from tests.harness import table_for
 
-    K, Wu = args.steps, args.warmup
-    E = 0 if args.no_e2e else args.e2e_steps
-    W = wl.window
-    pvp = wl.pvp if args.pvp is None else args.pvp
-    lines = args.lines or wl.lines_per_gpu
-    GK = args.graph_steps if (G == 1 and not args.graph) else 0
-    iters = Wu + K + E + GK + W + 1
-    g_, trace, scores = build_inputs(wl, G, rank, iters, only_mine=G > 1)
     mine = [np.asarray(trace[t][rank], np.int64) for t in range(iters)]
     max_ids = max(x.size for row in trace for x in row)
     if G > 1:  # every rank must size its inboxes identically (the layout is checked at connect)
