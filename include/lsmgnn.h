@@ -145,7 +145,10 @@ int lsmgnn_attach_storage(const void* host_rows_for_my_home, const char* nvme_pa
  * (cudaIpcMemHandle of its shared arena + layout) into buf (cap >= lsmgnn_handle_bytes()).
  * The binding all-gathers the blobs over the torch process group and passes the
  * concatenation (world * lsmgnn_handle_bytes() bytes, rank order) to lsmgnn_connect,
- * which opens every peer mapping. Not needed when world == 1. */
+ * which opens every peer mapping. The blob also carries the GPU's UUID: when a peer runs on
+ * this rank's own GPU (a test setup), the two pull phases of lsmgnn_gather both run after the
+ * homes' fills instead of overlapping them (LSMGNN_SPLIT_PULL=0/1 overrides).
+ * Not needed when world == 1. */
 size_t lsmgnn_handle_bytes(void);
 int lsmgnn_export_handle(void* buf, size_t cap);
 int lsmgnn_connect(const void* peer_handles, int32_t world);

@@ -477,7 +477,7 @@ struct SetParams {
   uint32_t* line_info;   // period > 1: per-line snapshot (reuse iteration / kInfoNone / kInfoFresh)
   uint32_t warp_bytes;   // per-warp shared memory
   uint32_t bypass_base;  // pool row of the bypass staging area
-  uint32_t deliver;      // kDelivered when k_serve delivers filled rows (G = 1), else 0
+  uint32_t deliver;      // kDelivered: node_loc marks rows filled this batch (k_serve / k_pull phases)
 };
 
 enum { C_HIT, C_VHIT, C_STOR, C_INS, C_BYP, C_EVICT, C_EV0, C_EV1, C_EV2, C_EV3, C_ENR, C_N };
@@ -940,12 +940,17 @@ __global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, ui
 // Requester: out[i] = row of ids[i] at its home. The location (cache slot, staging row)
 // is looked up in the home's node_loc table (peer-mapped when home != me) — the
 // "respond" step as a one-sided read — and the row is copied with 16-byte vectors.
+// Two phases per batch (G > 1): PHASE 0 copies the rows already in place when the homes
+// have finished k_set (hits, PVP-staged rows served in place) and zero-fills bad IDs; it runs
+// on a second stream concurrently with the homes' PCIe-bound k_fill. PHASE 1 copies the
+// rows k_fill wrote (node_loc bit kDelivered = "filled this batch") once every home has
+// signalled "served".
 struct PullArgs {
   const uint4* pool[8];
   const uint32_t* node_loc[8];
   uint32_t G;
 };
-template <int UNROLL, int OUT>
+template <int UNROLL, int OUT, int PHASE>
 __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __restrict__ out, uint32_t nvec) {
   const int64_t* __restrict__ ids = it->ids;
   const int64_t n = it->n;
@@ -955,11 +960,13 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
     const int64_t x = ids[i];
     uint4* dst = out + (size_t)i * nvec;
     if (x < 0 || (uint64_t)x >= N) {  // ERANGE: zero-filled row
-      for (uint32_t k = lane_id(); k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
+      if (PHASE == 0)
+        for (uint32_t k = lane_id(); k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
       continue;
     }
     const uint32_t v = (uint32_t)x, g = v % a.G, q = v / a.G;
     const uint32_t loc = a.node_loc[g][q];
+    if (((loc & kDelivered) != 0) != (PHASE == 1)) continue;
     warp_copy_row<UNROLL, kDev, OUT>(dst, a.pool[g] + (size_t)(loc & ~kDelivered) * nvec, nvec);
   }
 }

@@ -44,6 +44,7 @@ struct Handle {  // exported per rank for lsmgnn_connect
   uint64_t arena_bytes;
   uint64_t layout_sig;
   int32_t rank, world;
+  unsigned char gpu_uuid[16];  // ranks sharing one GPU (tests) are detected by UUID
 };
 
 // Persistent worker threads of the file tier (N2): started when a storage file is attached,
@@ -195,6 +196,14 @@ struct Ctx {
 
   // streams / events
   cudaStream_t side = nullptr;
+  // G > 1: the first pull phase (rows in place after k_set) runs on pull_st while k_fill runs
+  cudaStream_t pull_st = nullptr;
+  cudaEvent_t ev_set = nullptr, ev_pull0 = nullptr;
+  // Pull phase 0 on its own stream, concurrent with k_fill (the default on distinct GPUs). Ranks
+  // that share one GPU without MPS time-slice it, and the extra cross-process dependency then
+  // costs more than the overlap gains (profiles/r01_n2_pull_ab.md), so a rank that finds a
+  // peer on its own GPU runs both phases after "served". LSMGNN_SPLIT_PULL=0/1 overrides.
+  bool split_pull = true;
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
@@ -292,7 +301,8 @@ ScanSync scan_sync(uint32_t* words, uint64_t n) {
 
 // arena views (local or peer)
 uint32_t* flags_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_flags); }
-// flag slots: [0,G) route from r; [G,2G) served by home g; [2G,3G) window from r; [3G,4G) window ack from g
+// flag slots: [0,G) route from r; [G,2G) served by home g; [2G,3G) window from r; [3G,4G) window ack from g;
+// [4G,5G) located by home g (k_set done: node_loc final, rows of hits and staged nodes in place)
 uint32_t* icnt_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_icnt); }
 uint32_t* wcnt_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_wcnt); }
 uint32_t* inbox_of(char* base) { return reinterpret_cast<uint32_t*>(base + g.off_inbox); }
@@ -466,6 +476,9 @@ int free_all() {
   if (g.ev_fork) cudaEventDestroy(g.ev_fork);
   if (g.ev_join) cudaEventDestroy(g.ev_join);
   if (g.side) cudaStreamDestroy(g.side);
+  if (g.pull_st) cudaStreamDestroy(g.pull_st);
+  if (g.ev_set) cudaEventDestroy(g.ev_set);
+  if (g.ev_pull0) cudaEventDestroy(g.ev_pull0);
   if (g.ev_main) cudaEventDestroy(g.ev_main);
   for (auto e : g.ev_gend)
     if (e) cudaEventDestroy(e);
@@ -593,7 +606,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   sp.g_skey = g.g_skey;
   sp.warp_bytes = g.warp_bytes;
   sp.bypass_base = (uint32_t)g.bypass_base;
-  sp.deliver = G == 1 ? kDelivered : 0u;
+  sp.deliver = kDelivered;
   sp.period = (uint32_t)std::max(1, g.opt.update_period);
   sp.line_info = g.line_info;
   if (sp.period > 1) {  // the periodic window scan; k_snapshot exits when t mod P != 0
@@ -647,6 +660,32 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     prof_end(4, st);
     prof_begin(5, st);
   } else {
+    // Pull phase 0 (S7/S8 for the rows already in place): once every home has run k_set
+    // ("located"), copy hit and staged rows from local / peer HBM on pull_st while this
+    // home's k_fill streams the misses over PCIe.
+    if (int rc = flags_write_all(st, (uint32_t)(4 * G + g.rank), stamp_host)) return rc;
+    PullArgs pa{};
+    for (int h = 0; h < G; ++h) {
+      pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
+      pa.node_loc[h] = loc_of(g.peer_arena[h]);
+    }
+    pa.G = (uint32_t)G;
+    const int pblocks = grid_for(n_bound * 32, 256, 8);
+#define PULL(PH, S)                                                                        \
+  do {                                                                                     \
+    if (wide && !out_host) k_pull<8, kDev, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec); \
+    else if (wide) k_pull<8, kHost, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);        \
+    else if (!out_host) k_pull<2, kDev, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);    \
+    else k_pull<2, kHost, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);                 \
+  } while (0)
+    if (n_bound > 0 && g.split_pull) {
+      CK(cudaEventRecord(g.ev_set, st));
+      CK(cudaStreamWaitEvent(g.pull_st, g.ev_set, 0));
+      if (int rc = flags_wait_all(g.pull_st, &flags_of(g.arena)[4 * G], stamp_host)) return rc;
+      PULL(0, g.pull_st);
+      LAUNCHED();
+      CK(cudaEventRecord(g.ev_pull0, g.pull_st));
+    }
     prof_begin(4, st);
     if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
     const int blocks = g.sms * std::min(4, g.geom_per_sm);
@@ -656,24 +695,22 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce);
     LAUNCHED();
     prof_end(4, st);
-    // homes signal "served", requesters wait for every home, then pull
+    // homes signal "served", requesters wait for every home, then pull the filled rows
+    // (phase 1); the gather ends after both phases
     prof_begin(5, st);
     if (int rc = flags_write_all(st, (uint32_t)(G + g.rank), stamp_host)) return rc;
     if (int rc = flags_wait_all(st, &flags_of(g.arena)[G], stamp_host)) return rc;
     if (n_bound > 0) {
-      PullArgs pa{};
-      for (int h = 0; h < G; ++h) {
-        pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
-        pa.node_loc[h] = loc_of(g.peer_arena[h]);
+      if (g.split_pull) {
+        CK(cudaStreamWaitEvent(st, g.ev_pull0, 0));
+      } else {
+        PULL(0, st);
+        LAUNCHED();
       }
-      pa.G = (uint32_t)G;
-      const int pblocks = grid_for(n_bound * 32, 256, 8);
-      if (wide && !out_host) k_pull<8, kDev><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
-      else if (wide) k_pull<8, kHost><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
-      else if (!out_host) k_pull<2, kDev><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
-      else k_pull<2, kHost><<<pblocks, 256, 0, st>>>(g.it, g.N, pa, o4, g.nvec);
+      PULL(1, st);
       LAUNCHED();
     }
+#undef PULL
   }
   prof_end(5, st);
   k_end<<<1, 32, 0, st>>>(g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev);
@@ -958,7 +995,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
 
   // ---- shared arena
   size_t o = 0;
-  g.off_flags = o; o = align_up(o + 4 * G * sizeof(uint32_t), 256);
+  g.off_flags = o; o = align_up(o + 5 * G * sizeof(uint32_t), 256);
   g.off_icnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
   g.off_wcnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
   g.off_inbox = o; o = align_up(o + (size_t)G * g.cap * sizeof(uint32_t), 256);
@@ -1046,6 +1083,9 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   CK(cudaEventCreateWithFlags(&g.ev_pvp, cudaEventDisableTiming));
   CK(cudaFuncSetAttribute(k_set, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(g.warp_bytes * g.set_warps)));
   if (G > 1) {
+    CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g.ev_set, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g.ev_pull0, cudaEventDisableTiming));
     cudaDriverEntryPointQueryResult q1, q2;
     CK(cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void**>(&g.waitv), cudaEnableDefault, &q1));
     CK(cudaGetDriverEntryPoint("cuStreamWriteValue32", reinterpret_cast<void**>(&g.writev), cudaEnableDefault, &q2));
@@ -1103,6 +1143,9 @@ int lsmgnn_export_handle(void* buf, size_t cap) {
   h.layout_sig = (g.off_pool * 1315423911ull) ^ (g.pool_rows << 17) ^ g.cap ^ ((uint64_t)g.R << 40);
   h.rank = g.rank;
   h.world = g.world;
+  cudaDeviceProp prop{};
+  CK(cudaGetDeviceProperties(&prop, g.device));
+  std::memcpy(h.gpu_uuid, &prop.uuid, sizeof h.gpu_uuid);
   std::memcpy(buf, &h, sizeof h);
   return 0;
 }
@@ -1127,6 +1170,11 @@ int lsmgnn_connect(const void* peer_handles, int32_t world) {
     if (e != cudaSuccess) return set_err(LSMGNN_ECOMM, "cudaIpcOpenMemHandle(peer %d): %s", r, cudaGetErrorString(e));
     g.peer_arena[r] = reinterpret_cast<char*>(p);
   }
+  bool gpu_shared = false;
+  for (int r = 0; r < world; ++r)
+    if (r != g.rank && std::memcmp(hs[r].gpu_uuid, mine.gpu_uuid, sizeof mine.gpu_uuid) == 0) gpu_shared = true;
+  const char* sp = std::getenv("LSMGNN_SPLIT_PULL");
+  g.split_pull = sp ? std::atoi(sp) != 0 : !gpu_shared;
   g.connected = true;
   return 0;
 }

@@ -27,11 +27,15 @@ def free_port():
     return p
 
 
-def launch(G, tmp, *args, timeout=600):
+def launch(G, tmp, *args, timeout=600, split=1):
+    """split: LSMGNN_SPLIT_PULL for the ranks — 1 forces pull phase 0 onto its own stream
+    concurrent with k_fill (the default on distinct GPUs), 0 runs both phases after "served"
+    (the default when ranks share a GPU, as here); both must be bit-exact."""
+    env = dict(os.environ, LSMGNN_SPLIT_PULL=str(split))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py"), *args]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
 
 
@@ -52,12 +56,13 @@ def random_mp_case(seed, G):
     return cfg, tr, rng.integers(0, 256, N).astype(np.uint8)
 
 
+@pytest.mark.parametrize("split", [0, 1])
 @pytest.mark.parametrize("G", [2, 3])
-def test_multiprocess_fuzz(tmp_path, G):
+def test_multiprocess_fuzz(tmp_path, G, split):
     """Random small G-home cases (one process launch runs them all): every home's counters
     equal the oracle's."""
     n = int(os.environ.get("LSMGNN_MP_FUZZ", "12"))
-    launch(G, tmp_path, "fuzz", str(tmp_path), str(n), timeout=1200)
+    launch(G, tmp_path, "fuzz", str(tmp_path), str(n), timeout=1200, split=split)
     for case in range(n):
         cfg, tr, sc = random_mp_case(case, G)
         ho = run_oracle(tr, G=G, scores=sc, **cfg)
@@ -66,9 +71,9 @@ def test_multiprocess_fuzz(tmp_path, G):
             assert np.array_equal(hg, ho[:, r, :]), (case, r, cfg, np.argwhere(hg != ho[:, r, :])[:3])
 
 
-@pytest.mark.parametrize("G,case", [(2, "ragged"), (3, "dups"), (2, "period"), (4, "rr"), (2, "file"),
-                                    (3, "two_streams")])
-def test_multiprocess_edge_cases(tmp_path, G, case):
+@pytest.mark.parametrize("G,case,split", [(2, "ragged", 1), (3, "dups", 0), (3, "dups", 1), (2, "period", 1),
+                                          (4, "rr", 0), (2, "file", 1), (3, "two_streams", 1)])
+def test_multiprocess_edge_cases(tmp_path, G, case, split):
     """Ranks with empty batches, cross-rank duplicates, raw lists, victim-queue overflow,
     reinsert = 0, the periodic update and RR — per-home counters equal the oracle's."""
     rng = np.random.default_rng(G * 7 + len(case))
@@ -93,7 +98,7 @@ def test_multiprocess_edge_cases(tmp_path, G, case):
         cfg.update(two_streams=True)
     np.savez(tmp_path / "trace.npz", scores=sc, **{f"t{t}_r{r}": tr[t][r] for t in range(K) for r in range(G)})
     json.dump(cfg, open(tmp_path / "cfg.json", "w"))
-    launch(G, tmp_path, "edge", str(tmp_path))
+    launch(G, tmp_path, "edge", str(tmp_path), split=split)
     cfg.pop("file", None)
     cfg.pop("two_streams", None)
     ho = run_oracle(tr, G=G, scores=sc, **cfg)
@@ -103,10 +108,10 @@ def test_multiprocess_edge_cases(tmp_path, G, case):
         assert np.array_equal(hg, ho[:, r, :]), (case, r, np.argwhere(hg != ho[:, r, :])[:3])
 
 
-@pytest.mark.parametrize("G,policy,pvp", [(2, "hybrid", 1), (2, "lru", 0), (3, "hybrid", 0), (4, "static", 1),
-                                         (8, "hybrid", 1), (8, "hybrid", 0)])
-def test_multiprocess_parity(tmp_path, G, policy, pvp):
-    launch(G, tmp_path, "gather", str(tmp_path), policy, str(pvp))
+@pytest.mark.parametrize("G,policy,pvp,split", [(2, "hybrid", 1, 1), (2, "lru", 0, 0), (3, "hybrid", 0, 1),
+                                               (4, "static", 1, 0), (8, "hybrid", 1, 1), (8, "hybrid", 0, 0)])
+def test_multiprocess_parity(tmp_path, G, policy, pvp, split):
+    launch(G, tmp_path, "gather", str(tmp_path), policy, str(pvp), split=split)
     N, D = 16384, 128
     g = synth.plcite(N, 8)
     tr = synth.make_trace(g, G, 256, (10, 5), 20)
@@ -135,13 +140,13 @@ def test_multiprocess_parity(tmp_path, G, policy, pvp):
                 assert np.array_equal(hg[:, f], h1[:, f].astype(np.int64)), f
 
 
-@pytest.mark.parametrize("G,pvp", [(2, 1), (3, 0)])
-def test_multiprocess_gpu_sampler_window(tmp_path, G, pvp):
+@pytest.mark.parametrize("G,pvp,split", [(2, 1, 1), (3, 0, 0)])
+def test_multiprocess_gpu_sampler_window(tmp_path, G, pvp, split):
     """NEXT N3 at G > 1: every rank samples its own batches on the GPU and feeds the shared
     window with lsmgnn_prefetch_dev (the length never leaves the device); per-home counters
     equal the oracle's G-home run over the sampler oracle's lists, rows equal F(v)."""
     import oracle
-    launch(G, tmp_path, "sampler", str(tmp_path), str(pvp))
+    launch(G, tmp_path, "sampler", str(tmp_path), str(pvp), split=split)
     N, D, W, K, B, fan = 16384, 128, 8, 20, 256, (10, 5)
     g = synth.plcite(N, 8)
     perm = synth.epoch_seeds(N, 0)
