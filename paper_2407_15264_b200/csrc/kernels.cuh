@@ -954,20 +954,37 @@ template <int UNROLL, int OUT, int PHASE>
 __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __restrict__ out, uint32_t nvec) {
   const int64_t* __restrict__ ids = it->ids;
   const int64_t n = it->n;
+  const int lane = (int)lane_id();
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n; i += nwarps) {
-    const int64_t x = ids[i];
-    uint4* dst = out + (size_t)i * nvec;
-    if (x < 0 || (uint64_t)x >= N) {  // ERANGE: zero-filled row
-      if (PHASE == 0)
-        for (uint32_t k = lane_id(); k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
-      continue;
+  // A warp takes kChunk consecutive requests: its lanes read the IDs and the (local or
+  // peer) node_loc words at once — one dependent round trip per chunk instead of two per
+  // row, which matters most when node_loc is a peer's (NVLink latency) — then the warp
+  // copies the rows of this phase one by one.
+  constexpr uint32_t kChunk = 16;
+  for (int64_t c0 = warp * kChunk; c0 < n; c0 += nwarps * kChunk) {
+    const uint32_t m = (uint32_t)min((int64_t)kChunk, n - c0);
+    uint32_t loc_l = kInvalid, g_l = 0;
+    if ((uint32_t)lane < m) {
+      const int64_t x = ids[c0 + lane];
+      if (x >= 0 && (uint64_t)x < N) {
+        const uint32_t v = (uint32_t)x;
+        g_l = v % a.G;
+        loc_l = a.node_loc[g_l][v / a.G];
+      }
     }
-    const uint32_t v = (uint32_t)x, g = v % a.G, q = v / a.G;
-    const uint32_t loc = a.node_loc[g][q];
-    if (((loc & kDelivered) != 0) != (PHASE == 1)) continue;
-    warp_copy_row<UNROLL, kDev, OUT>(dst, a.pool[g] + (size_t)(loc & ~kDelivered) * nvec, nvec);
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t loc = __shfl_sync(0xffffffffu, loc_l, (int)j);
+      const uint32_t g = __shfl_sync(0xffffffffu, g_l, (int)j);
+      uint4* dst = out + (size_t)(c0 + j) * nvec;
+      if (loc == kInvalid) {  // ERANGE: zero-filled row
+        if (PHASE == 0)
+          for (uint32_t k = lane; k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
+        continue;
+      }
+      if (((loc & kDelivered) != 0) != (PHASE == 1)) continue;
+      warp_copy_row<UNROLL, kDev, OUT>(dst, a.pool[g] + (size_t)(loc & ~kDelivered) * nvec, nvec);
+    }
   }
 }
 
@@ -1030,21 +1047,27 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
       }
     }
   }
-  // ---- delivery of the rows no fill delivers, in chunks from the shared counter
+  // ---- delivery of the rows no fill delivers, in chunks from the shared counter. The
+  // chunk's IDs and locations are looked up by its lanes at once (one dependent round trip
+  // per chunk instead of two per row), then its rows are copied one after the other.
   for (;;) {
     uint32_t c0 = 0;
     if (lane == 0) c0 = atomicAdd(&scr->pull_next, kChunk);
     c0 = __shfl_sync(0xffffffffu, c0, 0);
     if ((int64_t)c0 >= n) break;
-    const int64_t c1 = min((int64_t)c0 + kChunk, n);
-    for (int64_t i = c0; i < c1; ++i) {
-      const int64_t x = ids[i];
-      uint4* dst = out + (size_t)i * nvec;
-      if (x < 0 || (uint64_t)x >= N) {
+    const uint32_t m = (uint32_t)min((int64_t)kChunk, n - (int64_t)c0);
+    uint32_t loc_l = kDelivered;  // lanes >= m: nothing to copy
+    if ((uint32_t)lane < m) {
+      const int64_t x = ids[c0 + lane];
+      loc_l = (x < 0 || (uint64_t)x >= N) ? kInvalid : node_loc[(uint32_t)x];
+    }
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint32_t loc = __shfl_sync(0xffffffffu, loc_l, (int)j);
+      uint4* dst = out + (size_t)(c0 + j) * nvec;
+      if (loc == kInvalid) {  // ERANGE: zero-filled row
         for (uint32_t k = lane; k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
         continue;
       }
-      const uint32_t loc = node_loc[(uint32_t)x];
       if (loc & kDelivered) continue;
       warp_copy_row<UNROLL, kDev, OUT>(dst, pool + (size_t)loc * nvec, nvec);
     }

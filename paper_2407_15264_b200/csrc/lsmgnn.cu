@@ -670,7 +670,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       pa.node_loc[h] = loc_of(g.peer_arena[h]);
     }
     pa.G = (uint32_t)G;
-    const int pblocks = grid_for(n_bound * 32, 256, 8);
+    const int pblocks = grid_for(n_bound * 2, 256, 8);  // a warp per 16 requests
 #define PULL(PH, S)                                                                        \
   do {                                                                                     \
     if (wide && !out_host) k_pull<8, kDev, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec); \
