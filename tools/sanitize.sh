@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # compute-sanitizer memcheck / racecheck / synccheck on the config-1-shaped smoke run (G = 1)
-# and memcheck on a 2-process G = 2 run (ranks share one GPU). Writes gpurun_out/sanitize_*.log
+# and memcheck on a 2-process G = 2 run (ranks share one GPU, each rank instrumented). Writes gpurun_out/sanitize_*.log
 # and a one-line-per-tool summary to gpurun_out/sanitize_summary.txt.
 set -u
 cd "$(dirname "$0")/.."
@@ -17,8 +17,20 @@ for tool in memcheck racecheck; do
     -k "multi_tile_set_scan and hybrid" > $out/sanitize_${tool}_multitile.log 2>&1
   echo "G=1 multi-tile $tool rc=$? : $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $out/sanitize_${tool}_multitile.log | tail -1) $(grep -Eo '[0-9]+ passed' $out/sanitize_${tool}_multitile.log)" >> $out/sanitize_summary.txt
 done
-timeout 1200 compute-sanitizer --tool memcheck --target-processes all --print-limit 20 \
-  python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr 127.0.0.1 --master-port 29533 \
-  tests/mp_worker.py gather /tmp hybrid 1 > $out/sanitize_memcheck_g2.log 2>&1
-echo "G=2 memcheck rc=$? : $(grep -E 'ERROR SUMMARY' $out/sanitize_memcheck_g2.log | tr '\n' ' ')" >> $out/sanitize_summary.txt
+# G = 2: each rank runs under its own compute-sanitizer (torch.distributed env set by hand, so
+# the ranks themselves are instrumented), both pull orders; the ranks' outputs are
+# checked (rows bad = 0)
+for split in 0 1; do
+  d=/tmp/san_g2_s$split; rm -rf $d; mkdir -p $d
+  port=$((29533 + split))
+  for r in 0 1; do
+    LSMGNN_SPLIT_PULL=$split RANK=$r LOCAL_RANK=$r WORLD_SIZE=2 LOCAL_WORLD_SIZE=2 MASTER_ADDR=127.0.0.1 MASTER_PORT=$port \
+      timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python tests/mp_worker.py gather $d hybrid 1 \
+      > $out/sanitize_memcheck_g2_s${split}_r$r.log 2>&1 &
+  done
+  wait
+  for r in 0 1; do
+    echo "G=2 split=$split rank $r memcheck: $(grep -E 'ERROR SUMMARY' $out/sanitize_memcheck_g2_s${split}_r$r.log | tr '\n' ' ') output: $(cat $d/r$r.json 2>&1 | head -c 60)" >> $out/sanitize_summary.txt
+  done
+done
 cat $out/sanitize_summary.txt
