@@ -31,7 +31,10 @@ def launch(G, tmp, *args, timeout=600, split=1):
     """split: LSMGNN_SPLIT_PULL for the ranks — 1 forces pull phase 0 onto its own stream
     concurrent with k_fill (the default on distinct GPUs), 0 runs both phases after "served"
     (the default when ranks share a GPU, as here); both must be bit-exact."""
-    env = dict(os.environ, LSMGNN_SPLIT_PULL=str(split))
+    env = dict(os.environ)
+    env.pop("LSMGNN_SPLIT_PULL", None)
+    if split is not None:  # None: the library's own choice (ranks here share a GPU => unsplit)
+        env["LSMGNN_SPLIT_PULL"] = str(split)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
            os.path.join(ROOT, "tests", "mp_worker.py"), *args]
@@ -72,7 +75,7 @@ def test_multiprocess_fuzz(tmp_path, G, split):
 
 
 @pytest.mark.parametrize("G,case,split", [(2, "ragged", 1), (3, "dups", 0), (3, "dups", 1), (2, "period", 1),
-                                          (4, "rr", 0), (2, "file", 1), (3, "two_streams", 1)])
+                                          (4, "rr", None), (2, "file", 1), (3, "two_streams", 1)])
 def test_multiprocess_edge_cases(tmp_path, G, case, split):
     """Ranks with empty batches, cross-rank duplicates, raw lists, victim-queue overflow,
     reinsert = 0, the periodic update and RR — per-home counters equal the oracle's."""
