@@ -43,7 +43,12 @@ _LIB = None
 
 
 def build() -> str:
-    """Compile liboracle.so (gcc -O2, single-threaded)."""
+    """Compile liboracle.so (gcc -O2, single-threaded). ORACLE_SO_OVERRIDE names another
+    build of the same sources to load instead (tests/test_oracle_mutants.py loads
+    deliberately broken builds that the pins must reject)."""
+    override = os.environ.get("ORACLE_SO_OVERRIDE")
+    if override:
+        return override
     deps = _SRCS + [os.path.join(_HERE, "lsm_oracle.h")]
     if not os.path.exists(_SO) or os.path.getmtime(_SO) < max(os.path.getmtime(p) for p in deps):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-o", _SO, *_SRCS])

@@ -35,8 +35,15 @@ def run_checked(o, trace, C):
         o.feed(k, trace[k] if k < K else empty)
     allc = []
     for t in range(K):
+        before = [o.tags(g)[0].copy() for g in range(G)]
         c, _ = o.gather(t, trace[t])
         allc.append(c)
+        # R10: a line hit by batch t is protected for the whole batch — still resident after it
+        req = set(np.concatenate(trace[t]).tolist()) if trace[t] else set()
+        for g in range(G):
+            hit = req & set(before[g][before[g] >= 0].tolist())
+            after = o.tags(g)[0]
+            assert hit <= set(after[after >= 0].tolist()), f"t={t} home {g}: a hit line was evicted"
         # I3: requests = sum of list lengths routed by v mod G; unique = |union| (brute force)
         ids = np.concatenate(trace[t]) if trace[t] else np.zeros(0, np.int64)
         for g in range(G):
@@ -210,3 +217,31 @@ def test_north_star_reuse_protected(seed):
         o.pvp_prefetch(t)
         o.feed(t + 1 + W, trace[t + 1 + W] if t + 1 + W < K else empty)
     assert evicted_with_reuse > 0  # the situation occurs
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pvp_staging_single_use(seed):
+    """P:397-400 (R15-R17): the prefetching buffer holds the rows staged for the next
+    iteration only. When the PVP copy is skipped after some gathers (the caller did not call
+    prefetch), no victim-buffer hit can occur in the following gather: victim_hits(t) <=
+    pvp_prefetched(t) at every t, and every row is served once from staging at most."""
+    rng = np.random.default_rng(900 + seed)
+    G, A, S, W, C = 1 + seed % 2, 2, 3, 4, 4
+    N = 30 * G
+    o = Oracle(G, N, 16, S * A, A, rng.integers(0, 256, N).astype(np.uint8), policy="hybrid", pvp=1, W=W,
+               V=C * W, reinsert=int(seed % 3 == 0))
+    trace = rand_trace(rng, G, N, 40, 20)
+    K = len(trace)
+    empty = [np.zeros(0, np.int64)] * G
+    for k in range(1, W + 1):
+        o.feed(k, trace[k] if k < K else empty)
+    vh = 0
+    for t in range(K):
+        c, _ = o.gather(t, trace[t])
+        assert np.all(c[:, F["victim_hits"]] <= c[:, F["pvp_prefetched"]]), t
+        vh += int(c[:, F["victim_hits"]].sum())
+        if rng.random() < 0.6:
+            o.pvp_prefetch(t)
+        o.feed(t + 1 + W, trace[t + 1 + W] if t + 1 + W < K else empty)
+    assert vh > 0  # the case exercises the victim buffer
+

@@ -325,6 +325,28 @@ def test_update_period_hand_derived():
     assert (tot(c, "evict_noreuse"), tot(c, "evict_far"), tot(c, "evict_fresh"), tot(c, "evict_near")) == (1, 1, 1, 0)
 
 
+def test_update_period_stale_snapshot_is_fresh():
+    """R6: with P = 4 the window scan runs at t = 0 and t = 4 only. Hand
+    derivation (1 line, W = 8): t0 node 0 missed and installed; t4 scan records its next
+    reuse 5; t5 hit; t6 (no scan) node 1 misses and evicts node 0, whose recorded reuse 5
+    has passed (<= 6) — no valid dynamic information, so the line is Fresh, not Near."""
+    o = Oracle(1, 4, 16, 1, 1, np.zeros(4, np.uint8), policy="hybrid", pvp=0, W=8, P=4)
+    c = run_trace(o, [[np.array(b, np.int64)] for b in [[0], [], [], [], [], [0], [1]]])
+    assert (tot(c[5], "hits"), tot(c[6], "evictions")) == (1, 1)
+    assert (tot(c[6], "evict_noreuse"), tot(c[6], "evict_far"), tot(c[6], "evict_fresh"),
+            tot(c[6], "evict_near")) == (0, 0, 1, 0)
+
+
+@pytest.mark.parametrize("T,cls", [(0, "evict_far"), (2, "evict_far"), (3, "evict_near")])
+def test_threshold_default_w_over_8(T, cls):
+    """P:365 (R4): the threshold defaults to W/8. Hand derivation (1 line, W = 16): node 0
+    installed at t0, node 1 evicts it at t1 while its next reuse is iteration 4, d = 3:
+    Far under the default T = 16/8 = 2 (and T = 2), Near once T >= 3."""
+    o = Oracle(1, 4, 16, 1, 1, np.zeros(4, np.uint8), policy="hybrid", pvp=0, W=16, T=T)
+    c = run_trace(o, [[np.array(b, np.int64)] for b in [[0], [1], [], [], [0]]])
+    assert tot(c[1], "evictions") == 1 and tot(c[1], cls) == 1
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_update_period_never_reduces_to_static(seed):
     """With P longer than the trace, only the t = 0 scan happens (on an empty cache): every
