@@ -17,8 +17,10 @@ timeout 900 ncu --set full --import-source on --clock-control none -k regex:"^k_
 python tools/ncu_kernels_json.py $out/ncu_kernels_latest.json $out/ncu/final_serve.ncu-rep $out/ncu/final_set.ncu-rep \
   $out/ncu/final_dedup.ncu-rep $out/ncu/final_scan.ncu-rep
 cp $out/ncu_kernels_latest.json profiles/ncu_kernels_latest.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file $out/final_launches.csv $B \
-  > /dev/null 2>&1
+# steady state: skip the 800 launches of init + the W-batch window bootstrap, then 20 steps
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 800 -c 200 --csv \
+  --log-file $out/final_launches.csv python bench.py --steps 20 --warmup 3 --no-ablation --no-e2e \
+  --no-cpu-baseline --graph-steps 0 --no-file-tier > /dev/null 2>&1
 timeout 1500 python bench.py > $out/final_bench.json 2> $out/final_bench.err
 tail -c 400 $out/final_bench.err
 ls -la $out/ncu
