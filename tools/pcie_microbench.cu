@@ -38,6 +38,40 @@ __global__ void k_ldg(const uint4* __restrict__ host, const uint32_t* __restrict
   }
 }
 
+// 256-bit loads (sm_100: ld.global.v8.u32 -> LDG.E.ENL2.256): 32 B per lane, 1 KiB per warp
+// instruction; U loads in flight per lane (U = 4: a whole 4 KiB row). HINT = 1 adds .L2::256B.
+template <int U, int HINT>
+__global__ void k_ldg256(const uint4* __restrict__ host, const uint32_t* __restrict__ rows, uint32_t n,
+                         uint4* __restrict__ dst, int nvec) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n32 = nvec / 2;  // 32-byte units per row
+  for (uint32_t e = warp; e < n; e += nw) {
+    const uint4* s = host + (size_t)rows[e] * nvec;
+    uint4* d = dst + (size_t)e * nvec;
+    for (int i = lane; i < n32; i += 32 * U) {
+      uint4 v[U][2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (i + 32 * u < n32) {
+        const uint4* p = s + 2 * (i + 32 * u);
+        if (HINT)
+          asm volatile("ld.global.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(v[u][0].x), "=r"(v[u][0].y), "=r"(v[u][0].z), "=r"(v[u][0].w),
+                         "=r"(v[u][1].x), "=r"(v[u][1].y), "=r"(v[u][1].z), "=r"(v[u][1].w) : "l"(p));
+        else
+          asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(v[u][0].x), "=r"(v[u][0].y), "=r"(v[u][0].z), "=r"(v[u][0].w),
+                         "=r"(v[u][1].x), "=r"(v[u][1].y), "=r"(v[u][1].z), "=r"(v[u][1].w) : "l"(p));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) if (i + 32 * u < n32) {
+        d[2 * (i + 32 * u)] = v[u][0];
+        d[2 * (i + 32 * u) + 1] = v[u][1];
+      }
+    }
+  }
+}
+
 // device rows -> pinned host rows (the e2e out path), 8 x 16 B per lane in flight
 __global__ void k_d2h(const uint4* __restrict__ src, uint32_t n, uint4* __restrict__ hout, int nvec) {
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -177,6 +211,12 @@ int main(int argc, char** argv) {
     timeit(nm, [&] { k_ldg<8, 2><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
     snprintf(nm, 64, "bulk.prefetch.L2 + ldg U=8 grid=%d", blocks);
     timeit(nm, [&] { k_ldg<8, 3><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
+    snprintf(nm, 64, "ldg.256 (v8) U=4 grid=%d", blocks);
+    timeit(nm, [&] { k_ldg256<4, 0><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
+    snprintf(nm, 64, "ldg.256 (v8) L2::256B U=4 grid=%d", blocks);
+    timeit(nm, [&] { k_ldg256<4, 1><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
+    snprintf(nm, 64, "ldg.256 (v8) U=2 grid=%d", blocks);
+    timeit(nm, [&] { k_ldg256<2, 0><<<blocks, 256>>>((const uint4*)hdev, drows, n, (uint4*)dst, R / 16); });
   }
   for (int stages : {4}) {
     for (int warps : {8}) {
