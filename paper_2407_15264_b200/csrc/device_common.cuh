@@ -75,6 +75,14 @@ struct IterState {
   uint32_t done;              // grid-completion counter (k_mask_clear)
 };
 
+// Programmatic dependent launch (PDL): a kernel launched with programmatic stream
+// serialization may start while its predecessor on the stream is still running; it waits
+// here until the predecessor has completed and its memory is visible, then lets its own
+// successor be scheduled early. Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // Warp-aggregated atomicAdd of `inc` per lane: one atomic per warp. Must be called

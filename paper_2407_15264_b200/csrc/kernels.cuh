@@ -38,6 +38,7 @@ struct BeginArgs {
   volatile uint32_t* overflow;     // ... and flagged here (pinned host word, sticky EINVAL)
 };
 __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, BeginArgs a) {
+  pdl_prologue();
   const uint64_t t = a.t_host >= 0 ? (uint64_t)a.t_host : it->t_next;
   unsigned long long* rec = hist + (size_t)(t % kHist) * F_NFIELDS;
   const int i = threadIdx.x;
@@ -79,6 +80,7 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
 // mirrored to pinned host memory; it->t_next = t + 1 (the next graph replay's iteration).
 __global__ void k_end(IterState* it, unsigned long long* hist, unsigned long long* cum, Scratch* scr, uint32_t R,
                       volatile uint32_t* bad_mirror) {
+  pdl_prologue();
   __shared__ unsigned long long s_rec[F_NFIELDS];
   const int f = threadIdx.x;  // one field per thread (blockDim = 32 >= F_NFIELDS)
   const uint64_t t = it->t;
@@ -109,6 +111,7 @@ __global__ void k_end(IterState* it, unsigned long long* hist, unsigned long lon
 __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host,
                             const int64_t* n_dev, const int64_t* const* ids_ring, const int64_t* n_ring,
                             uint32_t ring_len, uint32_t Wp1, int64_t cap, volatile uint32_t* overflow) {
+  pdl_prologue();
   if (threadIdx.x != 0) return;
   const uint64_t k = k_host >= 0 ? (uint64_t)k_host : it->wk_next;
   it->wk = k;
@@ -135,6 +138,7 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
 __global__ void k_route_local(const IterState* it, uint64_t N, uint32_t* __restrict__ ring, uint64_t stride,
                               uint32_t* __restrict__ ring_len, Scratch* scr, uint32_t* __restrict__ mask,
                               uint32_t MW) {
+  pdl_prologue();
   const int64_t* __restrict__ ids = it->wids;
   const int64_t n = it->wn;
   const uint32_t slot = it->wslot;
@@ -169,6 +173,7 @@ struct RouteArgs {
   uint32_t G;
 };
 __global__ void k_route_peer(const IterState* it, uint32_t window, uint64_t N, RouteArgs a, Scratch* scr) {
+  pdl_prologue();
   __shared__ uint32_t s_cnt[8], s_base[8];
   const int64_t* __restrict__ ids = window ? it->wids : it->ids;
   const int64_t n = window ? it->wn : it->n;
@@ -200,6 +205,7 @@ struct PublishArgs {
   uint32_t G, me;
 };
 __global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
+  pdl_prologue();
   const uint32_t g = threadIdx.x;
   if (g < a.G) {
     a.peer_cnt[g][a.me] = route_cnt[g];
@@ -234,6 +240,7 @@ __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __re
                         uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* hist,
                         unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt, uint32_t direct,
                         uint64_t N) {
+  pdl_prologue();
   const uint32_t stamp = it->stamp;
   unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
   uint32_t nreq = 0, npeer = 0;
@@ -336,6 +343,7 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt,
                                                const IterState* it, uint32_t G, unsigned long long* hist,
                                                uint32_t* __restrict__ poff, uint32_t big_P, ScanSync sy,
                                                uint32_t seq_add) {
+  pdl_prologue();
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_carry[2];
   __shared__ uint32_t s_c[kScanTile + kScanTile / 32];
@@ -421,6 +429,7 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt,
 __global__ void k_bucket(const uint32_t* __restrict__ uniq, const Scratch* scr, uint32_t G, uint32_t S,
                          const uint32_t* __restrict__ off, uint32_t* __restrict__ set_cnt,
                          uint32_t* __restrict__ bucket) {
+  pdl_prologue();
   const uint32_t n = scr->nuniq;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t v = uniq[i];
@@ -436,6 +445,7 @@ __global__ void k_bucket(const uint32_t* __restrict__ uniq, const Scratch* scr, 
 // before the feature aggregation stage"), run every P-th iteration.
 __global__ void k_snapshot(const uint32_t* __restrict__ tags, uint32_t L, uint32_t G, const uint32_t* __restrict__ mask,
                            uint32_t MW, uint32_t W, const IterState* it, uint32_t* __restrict__ line_info) {
+  pdl_prologue();
   if (!it->upd) return;  // not a scan iteration (t mod P != 0)
   const uint32_t p0 = it->p0, t = (uint32_t)it->t;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
@@ -523,6 +533,7 @@ __device__ __forceinline__ uint64_t policy_key(const SetParams& p, uint32_t v, u
 }
 
 __global__ void k_set(SetParams p) {
+  pdl_prologue();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_ctr[C_N];
   const uint32_t lane = lane_id();
@@ -838,6 +849,7 @@ __global__ void k_set(SetParams p) {
 __global__ void k_qscatter(const Cand* __restrict__ cands, const Scratch* scr, uint32_t W,
                            const uint32_t* __restrict__ qoff, uint32_t* __restrict__ qcnt,
                            uint32_t* __restrict__ qb) {
+  pdl_prologue();
   const uint32_t n = scr->ncand;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t k = cands[i].reuse % W;
@@ -852,6 +864,7 @@ __global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, c
                                                uint32_t* __restrict__ qnode, uint32_t* __restrict__ qreuse,
                                                FillEnt* __restrict__ fills, uint32_t C, const IterState* it,
                                                unsigned long long* rec_hist) {
+  pdl_prologue();
   __shared__ uint32_t hist[256];
   unsigned long long* rec = rec_hist + (size_t)it->rec_idx * F_NFIELDS;
   __shared__ uint32_t s_prefix, s_want, s_taken;
@@ -922,6 +935,7 @@ template <int UNROLL>
 __global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
                        const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
                        uint32_t bounce) {
+  pdl_prologue();
   const uint32_t n = scr->nfill;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -952,6 +966,7 @@ struct PullArgs {
 };
 template <int UNROLL, int OUT, int PHASE>
 __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __restrict__ out, uint32_t nvec) {
+  pdl_prologue();
   const int64_t* __restrict__ ids = it->ids;
   const int64_t n = it->n;
   const int lane = (int)lane_id();
@@ -1004,6 +1019,7 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
                         const unsigned long long* __restrict__ head, const uint32_t* __restrict__ nxt,
                         const IterState* it, uint64_t N,
                         const uint32_t* __restrict__ node_loc, uint4* __restrict__ out, uint32_t bounce) {
+  pdl_prologue();
   constexpr uint32_t kChunk = 16;
   const uint32_t stamp = it->stamp;
   const int64_t* __restrict__ ids = it->ids;
@@ -1081,6 +1097,7 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
 // k_route_local / k_win_gather store the new batch and set its bits.
 __global__ void k_mask_clear(const uint32_t* __restrict__ ring, uint64_t stride, uint32_t* ring_len, IterState* it,
                              uint32_t G, uint32_t MW, uint32_t* __restrict__ mask) {
+  pdl_prologue();
   const uint32_t bit = it->wslot;
   const uint32_t* __restrict__ list = ring + (size_t)bit * stride;
   const uint32_t n = ring_len[bit];
@@ -1102,6 +1119,7 @@ __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t*
                              uint32_t nsrc, uint32_t cap, uint32_t* __restrict__ ring, uint64_t stride,
                              uint32_t* ring_len, const IterState* it, uint32_t G, uint32_t MW,
                              uint32_t* __restrict__ mask) {
+  pdl_prologue();
   const uint32_t slot_i = it->wslot;
   uint32_t* __restrict__ slot = ring + (size_t)slot_i * stride;
   const uint32_t m = 1u << (slot_i & 31);
@@ -1129,6 +1147,7 @@ __global__ void k_pvp(const IterState* it, uint32_t W, uint32_t L, uint32_t C, u
                       uint4* __restrict__ pool, uint32_t* __restrict__ stg_base,
                       uint32_t* __restrict__ vst_stamp, uint32_t* __restrict__ vst_idx, Scratch* scr,
                       uint32_t nvec) {
+  pdl_prologue();
   // runs after gather(t): stage victim queue (t+1) mod W for iteration t+1
   const uint64_t t1 = it->t + 1;
   const uint32_t k = (uint32_t)(t1 % W), stamp1 = (uint32_t)(t1 + 1), par = (uint32_t)(t1 & 1);

@@ -204,6 +204,7 @@ struct Ctx {
   // costs more than the overlap gains (profiles/r01_n2_pull_ab.md), so a rank that finds a
   // peer on its own GPU runs both phases after "served". LSMGNN_SPLIT_PULL=0/1 overrides.
   bool split_pull = true;
+  bool pdl = false;  // programmatic dependent launch on the G = 1 chain (launch_pdl)
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
@@ -536,12 +537,37 @@ BeginArgs begin_args(int64_t t_host, const int64_t* ids, int64_t n, const int64_
 
 int read_storage_rows(cudaStream_t st);  // file tier (below)
 
+// Kernel launch with programmatic dependent launch (PDL) on the single-home step chain: the
+// next kernel is scheduled while its predecessor drains and waits in pdl_prologue() for its
+// results (kernels.cuh), hiding launch latency between the ~10 short kernels of a step.
+// Off at G > 1 (stream memory operations sit between the kernels) and with LSMGNN_NO_PDL=1.
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g.pdl ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) return set_err(LSMGNN_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
+  return 0;
+}
+#define KLAUNCH(kern, grid, block, smem, st, ...)                                         \
+  do {                                                                                  \
+    if (int rc_l = launch_pdl(kern, dim3(grid), dim3(block), (size_t)(smem), st, __VA_ARGS__)) return rc_l; \
+  } while (0)
+
 // gather kernels; n_bound = host bound of this rank's request count (grid sizing only);
 // stamp_host = t + 1 for the G > 1 flag protocol (direct calls only).
 int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host, bool graph, uint32_t stamp_host,
                   cudaStream_t st) {
   const int G = g.world;
-  k_begin<<<1, 32, 0, st>>>(g.it, g.hist, g.scr, ba);
+  KLAUNCH(k_begin, 1, 32, 0, st, g.it, g.hist, g.scr, ba);
   LAUNCHED();
   // ---- S1/S2 route + exchange
   prof_begin(0, st);
@@ -557,15 +583,15 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   // ---- S3 dedup + set grouping
   prof_begin(1, st);
   const int64_t maxreq = (int64_t)g.cap * G;
-  k_dedup<<<grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st>>>(
+  KLAUNCH(k_dedup, grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st, 
       inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, g.it, g.mark,
       g.uniq, g.set_cnt, g.scr, g.hist, G == 1 ? g.head : nullptr, g.nxt, G == 1 ? 1u : 0u, g.N);
   LAUNCHED();
-  k_scan<<<scan_tiles(g.S), 1024, 0, st>>>(g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr,
+  KLAUNCH(k_scan, scan_tiles(g.S), 1024, 0, st, g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr,
                                            (uint32_t)g.C, g.scr, g.mark, g.it, (uint32_t)G, g.hist, g.poff, g.P,
                                            scan_sync(g.scan_set, g.S), 0u);
   LAUNCHED();
-  k_bucket<<<grid_for(std::max<int64_t>(n_bound, 1) * G, 256, 4), 256, 0, st>>>(g.uniq, g.scr, (uint32_t)G,
+  KLAUNCH(k_bucket, grid_for(std::max<int64_t>(n_bound, 1) * G, 256, 4), 256, 0, st, g.uniq, g.scr, (uint32_t)G,
                                                                                  (uint32_t)g.S, g.set_off, g.set_cnt,
                                                                                  g.bucket);
   LAUNCHED();
@@ -610,14 +636,14 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   sp.period = (uint32_t)std::max(1, g.opt.update_period);
   sp.line_info = g.line_info;
   if (sp.period > 1) {  // the periodic window scan; k_snapshot exits when t mod P != 0
-    k_snapshot<<<grid_for((int64_t)g.L, 256, 4), 256, 0, st>>>(g.tags, (uint32_t)g.L, (uint32_t)G, g.mask, g.MW, g.W,
+    KLAUNCH(k_snapshot, grid_for((int64_t)g.L, 256, 4), 256, 0, st, g.tags, (uint32_t)g.L, (uint32_t)G, g.mask, g.MW, g.W,
                                                                 g.it, g.line_info);
     LAUNCHED();
   }
   {
     const int64_t blocks =
         std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(8, g.geom_per_sm));
-    k_set<<<(int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st>>>(sp);
+    KLAUNCH(k_set, (int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st, sp);
     LAUNCHED();
   }
   prof_end(2, st);
@@ -625,12 +651,12 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   if (g.C) {
     prof_begin(3, st);
     const int qg = grid_for(g.ucap, 256, 2);
-    k_scan<<<scan_tiles(g.W), 1024, 0, st>>>(g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr,
+    KLAUNCH(k_scan, scan_tiles(g.W), 1024, 0, st, g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr,
                                              nullptr, 0, scan_sync(g.scan_q, g.W), 1u);
     LAUNCHED();
-    k_qscatter<<<qg, 256, 0, st>>>(g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
+    KLAUNCH(k_qscatter, qg, 256, 0, st, g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
     LAUNCHED();
-    k_admit<<<g.W, 256, 0, st>>>(g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint32_t)g.C, g.it,
+    KLAUNCH(k_admit, g.W, 256, 0, st, g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint32_t)g.C, g.it,
                                  g.hist);
     LAUNCHED();
     prof_end(3, st);
@@ -649,7 +675,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
     const int blocks = g.sms * std::min(4, g.geom_per_sm);
 #define SERVE(U, O)                                                                                                  \
-  k_serve<U, O><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.it, g.N, \
+  KLAUNCH((k_serve<U, O>), blocks, 256, 0, st, g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.it, g.N, \
                                         loc_of(g.arena), o4, bounce)
     if (wide && !out_host) SERVE(8, kDev);
     else if (wide) SERVE(8, kHost);
@@ -713,7 +739,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
 #undef PULL
   }
   prof_end(5, st);
-  k_end<<<1, 32, 0, st>>>(g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev);
+  KLAUNCH(k_end, 1, 32, 0, st, g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev);
   LAUNCHED();
   return 0;
 }
@@ -723,17 +749,17 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
 int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* n_dev, const int64_t* const* ids_ring,
                   const int64_t* n_ring, uint32_t ring_len, int64_t n_bound, cudaStream_t st) {
   const int G = g.world;
-  k_win_begin<<<1, 32, 0, st>>>(g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1,
+  KLAUNCH(k_win_begin, 1, 32, 0, st, g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1,
                                 (int64_t)g.cap, g.bad_dev_overflow);
   LAUNCHED();
   const uint64_t stride = g.cap * G;
   // drop the bits of the iteration that last used this slot (k - (W+1)), then empty the slot
-  k_mask_clear<<<grid_for((int64_t)stride, 256, 2), 256, 0, st>>>(g.ring, stride, g.ring_len, g.it, (uint32_t)G, g.MW,
+  KLAUNCH(k_mask_clear, grid_for((int64_t)stride, 256, 2), 256, 0, st, g.ring, stride, g.ring_len, g.it, (uint32_t)G, g.MW,
                                                                    g.mask);
   LAUNCHED();
   if (G == 1) {
     if (n_bound > 0) {
-      k_route_local<<<grid_for(n_bound, 256), 256, 0, st>>>(g.it, g.N, g.ring, stride, g.ring_len, g.scr, g.mask,
+      KLAUNCH(k_route_local, grid_for(n_bound, 256), 256, 0, st, g.it, g.N, g.ring, stride, g.ring_len, g.scr, g.mask,
                                                             g.MW);
       LAUNCHED();
     }
@@ -1082,6 +1108,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   CK(cudaEventCreateWithFlags(&g.ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_pvp, cudaEventDisableTiming));
   CK(cudaFuncSetAttribute(k_set, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(g.warp_bytes * g.set_warps)));
+  g.pdl = G == 1 && !std::getenv("LSMGNN_NO_PDL");
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g.ev_set, cudaEventDisableTiming));
