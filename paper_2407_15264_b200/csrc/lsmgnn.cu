@@ -1395,11 +1395,11 @@ int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, i
   SampCounts* c = g.s_counts;
   auto xscan = [&](const uint32_t* x, const uint32_t* n_ptr, uint32_t* y, uint64_t nmax) -> int {
     const int nb = (int)std::max<uint64_t>(1, (nmax + 4095) / 4096);
-    k_xscan_blocks<<<nb, 1024, 0, st>>>(x, n_ptr, 0, y, g.s_bsum);
+    KLAUNCH(k_xscan_blocks, nb, 1024, 0, st, x, n_ptr, 0, y, g.s_bsum);
     LAUNCHED();
-    k_xscan_sums<<<1, 1024, 0, st>>>(g.s_bsum, (uint32_t)nb);
+    KLAUNCH(k_xscan_sums, 1, 1024, 0, st, g.s_bsum, (uint32_t)nb);
     LAUNCHED();
-    k_xscan_add<<<grid_for((int64_t)nmax, 256, 4), 256, 0, st>>>(y, n_ptr, 0, g.s_bsum);
+    KLAUNCH(k_xscan_add, grid_for((int64_t)nmax, 256, 4), 256, 0, st, y, n_ptr, 0, g.s_bsum);
     LAUNCHED();
     return 0;
   };
@@ -1407,16 +1407,16 @@ int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, i
   auto unique_first = [&](const uint32_t* a, const uint32_t* n_ptr, uint64_t nmax, auto* outp, uint32_t* n_out) -> int {
     const uint32_t hi = g.s_hi--;
     const int gr = grid_for((int64_t)std::max<uint64_t>(nmax, 1), 256, 4);
-    k_fo_mark<<<gr, 256, 0, st>>>(a, n_ptr, 0, g.s_tab, hi);
+    KLAUNCH(k_fo_mark, gr, 256, 0, st, a, n_ptr, 0, g.s_tab, hi);
     LAUNCHED();
-    k_fo_flag<<<gr, 256, 0, st>>>(a, n_ptr, 0, g.s_tab, hi, g.s_keep);
+    KLAUNCH(k_fo_flag, gr, 256, 0, st, a, n_ptr, 0, g.s_tab, hi, g.s_keep);
     LAUNCHED();
     if (int rc = xscan(g.s_keep, n_ptr, g.s_pos, nmax)) return rc;
-    k_fo_compact<<<gr, 256, 0, st>>>(a, n_ptr, 0, g.s_keep, g.s_pos, outp, n_out);
+    KLAUNCH((k_fo_compact<std::remove_pointer_t<decltype(outp)>>), gr, 256, 0, st, a, n_ptr, 0, g.s_keep, g.s_pos, outp, n_out);
     LAUNCHED();
     return 0;
   };
-  k_samp_init<<<grid_for(std::max<int64_t>(nseeds, 1), 256, 4), 256, 0, st>>>(seeds, (uint32_t)nseeds, g.s_raw,
+  KLAUNCH(k_samp_init, grid_for(std::max<int64_t>(nseeds, 1), 256, 4), 256, 0, st, seeds, (uint32_t)nseeds, g.s_raw,
                                                                               g.s_front, c);
   LAUNCHED();
   uint64_t fmax = (uint64_t)nseeds;
@@ -1424,24 +1424,24 @@ int lsmgnn_sample(const int64_t* seeds, int64_t nseeds, const int32_t* fanout, i
     const uint32_t f = (uint32_t)fanout[l];
     const uint64_t lmax = fmax * f;
     const int gr = grid_for((int64_t)std::max<uint64_t>(fmax, 1), 256, 4);
-    k_samp_count<<<gr, 256, 0, st>>>(g.s_front, c, g.s_indptr, f, g.s_cnt);
+    KLAUNCH(k_samp_count, gr, 256, 0, st, g.s_front, c, g.s_indptr, f, g.s_cnt);
     LAUNCHED();
     if (int rc = xscan(g.s_cnt, &c->nf, g.s_off, fmax)) return rc;
-    k_xscan_total<<<1, 1, 0, st>>>(g.s_off, g.s_cnt, &c->nf, 0, &c->layer_n);
+    KLAUNCH(k_xscan_total, 1, 1, 0, st, g.s_off, g.s_cnt, &c->nf, 0, &c->layer_n);
     LAUNCHED();
-    k_samp_draw<<<grid_for((int64_t)std::max<uint64_t>(fmax, 1) * 32, 256, 8), 256, 0, st>>>(
+    KLAUNCH(k_samp_draw, grid_for((int64_t)std::max<uint64_t>(fmax, 1) * 32, 256, 8), 256, 0, st, 
         g.s_front, c, g.s_indptr, g.s_indices, f, g.s_off, g.s_layer, seed, (uint64_t)t, (uint64_t)r, (uint64_t)l);
     LAUNCHED();
-    k_samp_append<<<grid_for((int64_t)std::max<uint64_t>(lmax, 1), 256, 4), 256, 0, st>>>(g.s_layer, c, g.s_raw);
+    KLAUNCH(k_samp_append, grid_for((int64_t)std::max<uint64_t>(lmax, 1), 256, 4), 256, 0, st, g.s_layer, c, g.s_raw);
     LAUNCHED();
     // next frontier = first-occurrence unique of this layer's draws
     if (int rc = unique_first(g.s_layer, &c->layer_n, lmax, g.s_front, &c->nf)) return rc;
-    k_samp_advance<<<1, 1, 0, st>>>(c);
+    KLAUNCH(k_samp_advance, 1, 1, 0, st, c);
     LAUNCHED();
     fmax = lmax;
   }
   if (int rc = unique_first(g.s_raw, &c->nraw, bound, out, &c->nout)) return rc;
-  k_samp_out_count<<<1, 1, 0, st>>>(c, count_dev);
+  KLAUNCH(k_samp_out_count, 1, 1, 0, st, c, count_dev);
   LAUNCHED();
   return 0;
 }

@@ -27,6 +27,7 @@ struct SampCounts {   // device-resident sizes of one sampling call
 // raw[0..n) = frontier[0..n) = seeds; counts initialised.
 __global__ void k_samp_init(const int64_t* __restrict__ seeds, uint32_t n, uint32_t* __restrict__ raw,
                             uint32_t* __restrict__ frontier, SampCounts* c) {
+  pdl_prologue();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     raw[i] = (uint32_t)seeds[i];
     frontier[i] = (uint32_t)seeds[i];
@@ -40,6 +41,7 @@ __global__ void k_samp_init(const int64_t* __restrict__ seeds, uint32_t n, uint3
 // cnt[p] = min(deg(frontier[p]), f)
 __global__ void k_samp_count(const uint32_t* __restrict__ frontier, const SampCounts* c, const int64_t* indptr,
                              uint32_t f, uint32_t* __restrict__ cnt) {
+  pdl_prologue();
   const uint32_t nf = c->nf;
   for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < nf; p += gridDim.x * blockDim.x) {
     const uint32_t x = frontier[p];
@@ -53,6 +55,7 @@ __global__ void k_samp_count(const uint32_t* __restrict__ frontier, const SampCo
 __global__ void k_samp_draw(const uint32_t* __restrict__ frontier, const SampCounts* c, const int64_t* indptr,
                             const int32_t* indices, uint32_t f, const uint32_t* __restrict__ off,
                             uint32_t* __restrict__ layer, uint64_t seed, uint64_t t, uint64_t r, uint64_t l) {
+  pdl_prologue();
   // warp per frontier node, lane per draw: every neighbour read of a node is in flight at once
   // (the reads are latency-bound when the CSR is in host memory)
   const uint32_t nf = c->nf;
@@ -83,6 +86,7 @@ __global__ void k_samp_draw(const uint32_t* __restrict__ frontier, const SampCou
 // decreases from call to call, so stale entries of earlier calls never win the minimum.
 __global__ void k_fo_mark(const uint32_t* __restrict__ a, const uint32_t* n_ptr, uint32_t n_off,
                           unsigned long long* __restrict__ tab, uint32_t hi) {
+  pdl_prologue();
   const uint32_t n = *n_ptr - n_off;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     atomicMin(&tab[a[i]], ((unsigned long long)hi << 32) | i);
@@ -90,6 +94,7 @@ __global__ void k_fo_mark(const uint32_t* __restrict__ a, const uint32_t* n_ptr,
 // step 2: keep[i] = this position is its node's first occurrence
 __global__ void k_fo_flag(const uint32_t* __restrict__ a, const uint32_t* n_ptr, uint32_t n_off,
                           const unsigned long long* __restrict__ tab, uint32_t hi, uint32_t* __restrict__ keep) {
+  pdl_prologue();
   const uint32_t n = *n_ptr - n_off;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     keep[i] = tab[a[i]] == (((unsigned long long)hi << 32) | i);
@@ -99,6 +104,7 @@ template <typename OutT>
 __global__ void k_fo_compact(const uint32_t* __restrict__ a, const uint32_t* n_ptr, uint32_t n_off,
                              const uint32_t* __restrict__ keep, const uint32_t* __restrict__ pos,
                              OutT* __restrict__ out, uint32_t* n_out) {
+  pdl_prologue();
   const uint32_t n = *n_ptr - n_off;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     if (keep[i]) out[pos[i]] = (OutT)a[i];
@@ -110,6 +116,7 @@ __global__ void k_fo_compact(const uint32_t* __restrict__ a, const uint32_t* n_p
 __global__ void __launch_bounds__(1024) k_xscan_blocks(const uint32_t* __restrict__ x, const uint32_t* n_ptr,
                                                        uint32_t n_off, uint32_t* __restrict__ y,
                                                        uint32_t* __restrict__ bsum) {
+  pdl_prologue();
   __shared__ uint32_t s_warp[32];
   const uint32_t n = *n_ptr - n_off;
   const uint32_t base = blockIdx.x * 4096u;
@@ -151,6 +158,7 @@ __global__ void __launch_bounds__(1024) k_xscan_blocks(const uint32_t* __restric
   if (tid == 1023) bsum[blockIdx.x] = run;
 }
 __global__ void __launch_bounds__(1024) k_xscan_sums(uint32_t* __restrict__ bsum, uint32_t nb) {
+  pdl_prologue();
   __shared__ uint32_t s[1024];
   const uint32_t tid = threadIdx.x;
   s[tid] = tid < nb ? bsum[tid] : 0u;
@@ -165,21 +173,24 @@ __global__ void __launch_bounds__(1024) k_xscan_sums(uint32_t* __restrict__ bsum
 }
 __global__ void k_xscan_add(uint32_t* __restrict__ y, const uint32_t* n_ptr, uint32_t n_off,
                             const uint32_t* __restrict__ bsum) {
+  pdl_prologue();
   const uint32_t n = *n_ptr - n_off;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] += bsum[i >> 12];
 }
 // total = y[n-1] + x[n-1] after the add pass
 __global__ void k_xscan_total(const uint32_t* __restrict__ y, const uint32_t* __restrict__ x, const uint32_t* n_ptr,
                               uint32_t n_off, uint32_t* total_out) {
+  pdl_prologue();
   const uint32_t n = *n_ptr - n_off;
   *total_out = n ? y[n - 1] + x[n - 1] : 0u;
 }
 // raw[nraw + i] = layer[i]; the single-thread k_samp_advance then moves nraw
 __global__ void k_samp_append(const uint32_t* __restrict__ layer, const SampCounts* c, uint32_t* __restrict__ raw) {
+  pdl_prologue();
   const uint32_t n = c->layer_n, base = c->nraw;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) raw[base + i] = layer[i];
 }
-__global__ void k_samp_advance(SampCounts* c) { c->nraw += c->layer_n; }
-__global__ void k_samp_out_count(const SampCounts* c, int64_t* count_dev) { *count_dev = c->nout; }
+__global__ void k_samp_advance(SampCounts* c) { pdl_prologue(); c->nraw += c->layer_n; }
+__global__ void k_samp_out_count(const SampCounts* c, int64_t* count_dev) { pdl_prologue(); *count_dev = c->nout; }
 
 }  // namespace lsm
