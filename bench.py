@@ -458,7 +458,8 @@ def main():
                    "victim_lines": wl.victim_lines if pvp else 0, "parallelism": f"shared cache over {G} GPU" if ndev >= G else
                    f"shared cache over {G} homes on {ndev} GPU (ranks share a device: protocol test, not a "
                    f"multi-GPU throughput)",
-                   "l2": "inputs larger than L2: cache 400 MB, out ~550 MB/step, host table 4 GB",
+                   "l2": f"inputs larger than L2 (126 MB): cache {lines * R / 1e6:.0f} MB per home, out "
+                         f"~{d['requests'] / K * R / 1e6:.0f} MB/step, host table {wl.N * R / 1e9:.1f} GB",
                    "seeds": wl.seeds},
         "gpu_launches": int(launches),
         "clocks": clk,
