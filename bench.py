@@ -243,7 +243,7 @@ def main():
     pvp = wl.pvp if args.pvp is None else args.pvp
     lines = args.lines or wl.lines_per_gpu
     GK = args.graph_steps if (G == 1 and not args.graph) else 0
-    iters = Wu + K + E + GK + W + 1
+    iters = Wu + K + 2 * E + GK + W + 1  # E strict e2e steps + E device-result e2e steps
     g_, trace, scores = build_inputs(wl, G, rank, iters, only_mine=G > 1)
 
     import torch
@@ -373,6 +373,39 @@ def main():
         e2e = {"value": round(eb / tsum / 1e9, 4), "unit": "GB/s", "h2d_bytes_per_step": int(h2d / E),
                "d2h_bytes_per_step": int(d2h / E), "steps": E,
                "what": "lsmgnn_gather_host: pinned host IDs -> device, gather, rows -> pinned host, synchronous"}
+        # variant: the gathered rows stay in HBM for the consumer (a training step reads them
+        # there); each step copies its IDs from pinned host memory and reads back the step's
+        # per-iteration counters (192 B, lsmgnn_stats) — the "result" a trainer would check
+        dids = torch.empty(maxn, dtype=torch.int64, device=dev)
+        hids2 = [torch.from_numpy(mine[Wu + K + E + i]).pin_memory() for i in range(E)]
+        torch.cuda.synchronize()
+        if G > 1:
+            torch.distributed.barrier()
+        tsum2, eb2, h2d2 = 0.0, 0, 0
+        for i in range(E):
+            t = Wu + K + E + i
+            n = hids2[i].numel()
+            t0 = time.perf_counter()
+            dids[:n].copy_(hids2[i], non_blocking=True)
+            c.gather(dids[:n], out)
+            k = t + 1 + W
+            c.prefetch([ids_d[k]], first_iter=k)
+            c.stats(0)  # device -> host read of the step's counters (synchronises)
+            tsum2 += time.perf_counter() - t0
+            eb2 += n * wl.R
+            h2d2 += n * 8
+        if G > 1:
+            x = torch.tensor([tsum2, float(eb2)], dtype=torch.float64, device=cdev)
+            tm = x[:1].clone()
+            torch.distributed.all_reduce(tm, op=torch.distributed.ReduceOp.MAX)
+            sm = x[1:].clone()
+            torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+            tsum2, eb2 = float(tm.item()), float(sm.item())
+        e2e["device_result"] = {
+            "value": round(eb2 / tsum2 / 1e9, 4), "unit": "GB/s", "h2d_bytes_per_step": int(h2d2 / E),
+            "d2h_bytes_per_step": 192, "steps": E,
+            "what": "pinned host IDs -> device (copy in the timed region), lsmgnn_gather into HBM, window feed, "
+                    "lsmgnn_stats read back per step (host wall clock, synchronous)"}
 
     # ---- the same step replayed as one CUDA graph per iteration (device-resident iteration state)
     graph_replay = None
@@ -386,7 +419,7 @@ def main():
         gb.record(st)
         torch.cuda.synchronize()
         tg = ga.elapsed_time(gb) / 1e3
-        gbytes = sum(mine[Wu + K + E + i].size for i in range(GK)) * wl.R
+        gbytes = sum(mine[Wu + K + 2 * E + i].size for i in range(GK)) * wl.R
         graph_replay = {"steps": GK, "value": round(gbytes / tg / 1e9, 4), "unit": "GB/s",
                         "ms_per_step": round(tg / GK * 1e3, 4),
                         "what": "lsmgnn_graph_capture once, then one cudaGraphLaunch per step (gather + window feed)"}
