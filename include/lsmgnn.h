@@ -25,6 +25,17 @@
  *   - errors detected on the device (a node ID >= num_nodes) set a sticky flag; the
  *     next call (or lsmgnn_stats) returns LSMGNN_ERANGE and the out rows of those
  *     IDs are zero-filled.
+ *
+ * Environment (read at init / connect / attach; defaults are the measured best):
+ *   LSMGNN_NO_PDL=1           plain launches instead of programmatic dependent launch on the
+ *                             single-home step chain and the sampler
+ *   LSMGNN_SPLIT_PULL=0|1     G > 1 pull order: 1 = rows in place copied during the fill
+ *                             (default on distinct GPUs), 0 = both phases after "served"
+ *                             (default when a peer shares this rank's GPU)
+ *   LSMGNN_NO_BATCH_MEMOP=1   one stream memory operation per flag instead of batched
+ *   LSMGNN_STORAGE_BUFFERED=1 file tier through the page cache instead of O_DIRECT
+ *   LSMGNN_IO_THREADS=n       file-tier pread workers per batch (default 64)
+ *   LSMGNN_GEOMETRY=small     one CTA per SM for every grid (launch-geometry tests)
  */
 #ifndef LSMGNN_H
 #define LSMGNN_H
