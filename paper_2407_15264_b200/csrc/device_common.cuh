@@ -87,6 +87,30 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 // Warp-aggregated atomicAdd of `inc` per lane: one atomic per warp. Must be called
 // by all 32 lanes (inactive lanes pass inc = 0). Returns this lane's base offset.
+// CTA-wide reservation of one slot per thread with want == true: one atomicAdd per CTA on the
+// shared counter instead of one per warp (a hot single address). Every thread of the CTA must
+// call it (CTA-uniform control flow). Slot order within the CTA follows thread order.
+__device__ __forceinline__ uint32_t block_reserve(uint32_t* ctr, bool want) {
+  __shared__ uint32_t s_cnt[32];
+  __shared__ uint32_t s_base;
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const uint32_t b = __ballot_sync(0xffffffffu, want);
+  if (lane == 0) s_cnt[w] = __popc(b);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (uint32_t i = 0; i < nw; ++i) {
+      const uint32_t c = s_cnt[i];
+      s_cnt[i] = tot;
+      tot += c;
+    }
+    s_base = tot ? atomicAdd(ctr, tot) : 0u;
+  }
+  __syncthreads();
+  const uint32_t r = s_base + s_cnt[w] + __popc(b & ((1u << lane) - 1u));
+  __syncthreads();  // s_cnt / s_base are reused by the next call
+  return r;
+}
 __device__ __forceinline__ uint32_t warp_reserve(uint32_t* ctr, uint32_t inc) {
   const uint32_t lane = lane_id();
   uint32_t incl = inc;

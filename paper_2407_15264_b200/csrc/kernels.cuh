@@ -155,7 +155,7 @@ __global__ void k_route_local(const IterState* it, uint64_t N, uint32_t* __restr
       v = (uint32_t)x;
       if (!ok) atomicAdd(&scr->bad_ids, 1u);
     }
-    const uint32_t pos = warp_reserve(cnt, ok ? 1u : 0u);
+    const uint32_t pos = block_reserve(cnt, ok);
     if (ok) {
       list[pos] = v;
       atomicOr(&mask[(size_t)v * MW + (slot >> 5)], 1u << (slot & 31));  // G = 1: q = v
@@ -262,7 +262,7 @@ __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __re
           atomicAdd(&scr->bad_ids, 1u);
         }
       }
-      const uint32_t pos = warp_reserve(&scr->nuniq, first ? 1u : 0u);
+      const uint32_t pos = block_reserve(&scr->nuniq, first);
       if (first) uniq[pos] = v;
     }
   } else {
@@ -279,7 +279,7 @@ __global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __re
           ++nreq;
           if (r != me) ++npeer;
         }
-        const uint32_t pos = warp_reserve(&scr->nuniq, first ? 1u : 0u);
+        const uint32_t pos = block_reserve(&scr->nuniq, first);
         if (first) uniq[pos] = v;
       }
     }
