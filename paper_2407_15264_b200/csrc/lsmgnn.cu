@@ -714,7 +714,9 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     }
     prof_begin(4, st);
     if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
-    const int blocks = g.sms * std::min(4, g.geom_per_sm);
+    // 2 CTAs per SM: the PCIe-bound fill saturates the link from 1 CTA/SM
+    // (profiles/r01_pcie_microbench.txt) and leaves room on every SM for pull phase 0
+    const int blocks = g.sms * std::min(2, g.geom_per_sm);
     if (wide)
       k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce);
     else
