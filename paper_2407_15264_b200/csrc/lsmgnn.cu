@@ -824,6 +824,11 @@ int launch_pvp(cudaStream_t st) {
     CK(cudaEventRecord(g.ev_main, st));
     CK(cudaStreamWaitEvent(g.side, g.ev_main, 0));
   }
+  // ... and after the window feed this prefetch call just issued: started alongside the feed
+  // kernels, the PCIe-bound copy held the SMs they need and delayed the feed (and everything
+  // queued behind it on the caller's stream, e.g. training) by its whole duration
+  // (profiles/r01_pvp_overlap.md); after the feed it overlaps the caller's next work instead
+  if (g.feed_recorded) CK(cudaStreamWaitEvent(g.side, g.ev_feed, 0));
   uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
   const int blocks = g.sms * std::min(2, g.geom_per_sm);
   prof_begin(7, g.side);
