@@ -320,3 +320,45 @@ def test_determinism_launch_geometry(cfg1_g1, monkeypatch):
     h2, _, bad2 = run_gpu(tr, **kw)
     assert bad1 == 0 and bad2 == 0
     compare(h1, h2, "geometry")
+
+
+@pytest.mark.parametrize("out_kind", ["pinned", "pageable"])
+def test_gather_host_end_to_end(cfg1_g1, out_kind):
+    """lsmgnn_gather_host (the e2e entry point: host IDs in, host rows out, copies inside the
+    call): rows equal F(v) and every per-iteration counter equals the oracle's. Pinned `out`
+    is written by the serve kernel over PCIe; pageable `out` goes through device staging."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    from .harness import table_for
+    _, tr, sc = cfg1_g1
+    N, D, W, K = 16384, 128, 8, len(tr)
+    mine = [np.asarray(tr[t][0], np.int64) for t in range(K)]
+    c = LsmGnn(N, D, 1024, 8, 512, sc, policy="hybrid", pvp=1, window=W, max_batch_ids=max(x.size for x in mine))
+    c.attach_storage(table_for(N, D, 5, pinned=True))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ids_d = [torch.from_numpy(x).to(dev) for x in mine]
+    empty = torch.zeros(0, dtype=torch.int64, device=dev)
+    c.prefetch([ids_d[k] if k < K else empty for k in range(1, W + 1)], first_iter=1)
+    bad = 0
+    for t in range(K):
+        hid = torch.from_numpy(mine[t]).pin_memory()
+        n = mine[t].size
+        if out_kind == "pinned":
+            hout = torch.empty((max(n, 1), 4 * D), dtype=torch.uint8, pin_memory=True)
+            c.gather_host(hid, hout)
+            rows = hout[:n].numpy()
+        else:
+            hout = np.empty((max(n, 1), 4 * D), np.uint8)
+            c.gather_host(hid, hout)
+            rows = hout[:n]
+        k = t + 1 + W
+        c.prefetch([ids_d[k] if k < K else empty], first_iter=k)
+        if n:
+            nb, _ = synth.check_rows(rows.view(np.uint32).reshape(-1, D), mine[t], D, 5)
+            bad += nb
+    torch.cuda.synchronize()
+    hg = c.history(0, K)
+    c.close()
+    assert bad == 0
+    ho = run_oracle(tr, G=1, N=N, D=D, L=1024, A=8, scores=sc, policy="hybrid", pvp=1, W=W, V=512)[:, 0, :]
+    compare(hg, ho, f"gather_host {out_kind}")
