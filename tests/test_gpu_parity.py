@@ -362,3 +362,39 @@ def test_gather_host_end_to_end(cfg1_g1, out_kind):
     assert bad == 0
     ho = run_oracle(tr, G=1, N=N, D=D, L=1024, A=8, scores=sc, policy="hybrid", pvp=1, W=W, V=512)[:, 0, :]
     compare(hg, ho, f"gather_host {out_kind}")
+
+
+def test_launch_count_and_profile(cfg1_g1):
+    """lsmgnn_kernel_launches and lsmgnn_profile/_read (what bench.py's gpu_launches and phases
+    come from): a G = 1 step without PVP or periodic update is 10 kernels (begin, dedup, scan,
+    bucket, set, serve, end + window feed: win_begin, mask_clear, route_local), and the profiled
+    phase spans cover the step's phases with non-negative times."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    from .harness import table_for
+    _, tr, sc = cfg1_g1
+    N, D, W, K = 16384, 128, 8, len(tr)
+    mine = [np.asarray(tr[t][0], np.int64) for t in range(K)]
+    c = LsmGnn(N, D, 1024, 8, 0, sc, policy="hybrid", pvp=0, window=W, max_batch_ids=max(x.size for x in mine))
+    c.attach_storage(table_for(N, D, 5, pinned=True))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ids_d = [torch.from_numpy(x).to(dev) for x in mine]
+    out = torch.empty((max(x.size for x in mine), 4 * D), dtype=torch.uint8, device=dev)
+    c.prefetch(ids_d[1:W + 1], first_iter=1)
+    steps = K - W - 1
+    c.profile(True)
+    c.profile_read()
+    n0 = c.kernel_launches()
+    for t in range(steps):
+        c.gather(ids_d[t], out)
+        c.prefetch([ids_d[t + 1 + W]], first_iter=t + 1 + W)
+    torch.cuda.synchronize()
+    n1 = c.kernel_launches()
+    prof = c.profile_read()
+    c.profile(False)
+    c.close()
+    assert n1 - n0 == 10 * steps, (n1 - n0, steps)
+    for ph in ("route", "dedup", "probe_replace", "fill", "window"):
+        ms, cnt = prof[ph]
+        assert cnt == steps and ms >= 0.0, (ph, prof[ph])
+    assert prof["fill"][0] > 0.0
