@@ -509,6 +509,10 @@ def main():
                   "pcie_h2d_GBps_over_step": round(d["bytes_h2d_storage"] / T / 1e9, 2),
                   "victim_d2h_GBps_over_step": round(d["bytes_d2h_victim"] / T / 1e9, 2),
                   "pvp_h2d_GBps_over_step": round(d["bytes_h2d_pvp"] / T / 1e9, 2),
+                  # rows this home served to other ranks (one-sided pulls over NVLink at G > 1;
+                  # ranks sharing one GPU move them within its HBM) and to its own rank
+                  "nvlink_out_GBps_over_step": round(d["bytes_nvlink"] / T / 1e9, 2),
+                  "local_hbm_GBps_over_step": round((d["bytes_out"] - d["bytes_nvlink"]) / T / 1e9, 2),
                   "bypassed_per_step": d["bypassed"] / K, "evictions_per_step": d["evictions"] / K},
         "phases": phases,
         # T_roof = max over tiers of bytes / peak, per step; reported as T_roof / T_meas
