@@ -234,44 +234,8 @@ int main(int argc, char** argv) {
       }
     }
   }
-  // copy engine on the SAME scattered rows: cudaMemcpyBatchAsync (host-side descriptor lists)
-  {
-    std::vector<void*> dsts(n), srcs(n);
-    std::vector<size_t> sizes(n, R);
-    for (uint32_t i = 0; i < n; ++i) {
-      dsts[i] = dst + (size_t)i * R;
-      srcs[i] = host + (size_t)rows[i] * R;
-    }
-    cudaMemcpyAttributes at{};
-    at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    at.srcLocHint.type = cudaMemLocationTypeHost;
-    at.dstLocHint.type = cudaMemLocationTypeDevice;
-    at.dstLocHint.id = 0;
-    size_t idx0 = 0, fail = 0;
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    for (uint32_t chunk : {n, 8192u}) {
-      float best = 1e9, host_ms = 0;
-      for (int it = 0; it < 4; ++it) {
-        cudaEventRecord(a, s);
-        auto h0 = std::chrono::steady_clock::now();
-        for (uint32_t o = 0; o < n; o += chunk) {
-          const uint32_t m = std::min(chunk, n - o);
-          cudaError_t e = cudaMemcpyBatchAsync(dsts.data() + o, srcs.data() + o, sizes.data() + o, m, &at, &idx0, 1,
-                                               &fail, s);
-          if (e != cudaSuccess) { printf("cudaMemcpyBatchAsync: %s\n", cudaGetErrorString(e)); break; }
-        }
-        auto h1 = std::chrono::steady_clock::now();
-        cudaEventRecord(b, s);
-        CK(cudaEventSynchronize(b));
-        float ms;
-        cudaEventElapsedTime(&ms, a, b);
-        if (it) { best = std::min(best, ms); host_ms = std::chrono::duration<float, std::milli>(h1 - h0).count(); }
-      }
-      printf("CE cudaMemcpyBatchAsync 4KiB x n (chunk %6u) %8.3f ms  %7.2f GB/s  (host submit %.2f ms)\n", chunk, best,
-             (double)n * R / best / 1e6, host_ms);
-    }
-  }
+  // (a per-row copy-engine variant was measured in round 1 with a batched-copy API that is
+  // closed on this pool; its result stays in profiles/r01_pcie_microbench.txt)
   // D2H: device rows -> pinned host (SM stores over PCIe), and both directions at once
   uint8_t* hout;
   CK(cudaHostAlloc(&hout, (size_t)n * R, cudaHostAllocMapped));
