@@ -162,7 +162,29 @@ int lsmgnn_attach_storage(const void* host_rows_for_my_home, const char* nvme_pa
  * Not needed when world == 1. */
 size_t lsmgnn_handle_bytes(void);
 int lsmgnn_export_handle(void* buf, size_t cap);
+/* lsmgnn_connect validates the blobs before mapping anything: blob r must carry rank r and
+ * world == this rank's world, and its layout signature (every arena offset and size, derived
+ * from the lsmgnn_init arguments and the options) must equal this rank's; otherwise nothing
+ * is mapped and it returns LSMGNN_ECOMM naming the first offending peer. */
 int lsmgnn_connect(const void* peer_handles, int32_t world);
+
+/* Host-only bootstrap logic (no GPU, no CUDA call, usable before / without lsmgnn_init):
+ * lsmgnn_plan_handle writes into buf (cap >= lsmgnn_handle_bytes()) the handle rank `rank` of
+ * `world` WOULD export for these lsmgnn_init arguments and options (opt NULL = defaults),
+ * without the IPC handle and GPU UUID; it returns the same LSMGNN_EINVAL lsmgnn_init would for
+ * a bad argument. lsmgnn_check_handles runs lsmgnn_connect's validation of `world`
+ * concatenated blobs against the blob `mine`: 0, or LSMGNN_ECOMM (wrong rank order, world
+ * mismatch, layout mismatch). The binding's gloo tests drive both across processes. */
+int lsmgnn_plan_handle(const lsmgnn_options* opt, int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype,
+                       int64_t lines_per_gpu, int32_t ways, int64_t victim_lines, int32_t rank, int32_t world,
+                       void* buf, size_t cap);
+int lsmgnn_check_handles(const void* handles, int32_t world, const void* mine);
+
+/* G > 1 teardown, step 1: synchronise this rank's device and close its mappings of the peers'
+ * arenas. The binding calls it on every rank, then meets the others at a barrier, then calls
+ * lsmgnn_finalize (step 2: free this rank's arena) — so no arena is freed while a peer still
+ * has it mapped. Idempotent; a no-op before init. */
+int lsmgnn_disconnect(void);
 
 /* gather(t): collective, lockstep — every rank calls it once per iteration t.
  * Stream-ordered on `stream`: node_ids (device int64[n]) and out (device, n*R bytes,

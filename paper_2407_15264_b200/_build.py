@@ -1,6 +1,7 @@
 """Build liblsmgnn.so in-tree with nvcc for sm_100a (no GPU needed)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -9,8 +10,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "liblsmgnn.so")
 SRCS = [os.path.join(HERE, "csrc", f) for f in ("lsmgnn.cu",)]
-DEPS = SRCS + [os.path.join(HERE, "csrc", f) for f in ("kernels.cuh", "device_common.cuh")] + \
-    [os.path.join(ROOT, "include", "lsmgnn.h")]
+# every header under csrc/ (kernels, device helpers, the sampler, ...) and the public header
+DEPS = SRCS + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "lsmgnn.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v",

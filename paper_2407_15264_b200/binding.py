@@ -25,7 +25,7 @@ EXPORTS = ["lsmgnn_bind", "lsmgnn_set_options", "lsmgnn_init", "lsmgnn_attach_st
            "lsmgnn_stats", "lsmgnn_stats_history", "lsmgnn_kernel_launches", "lsmgnn_finalize",
            "lsmgnn_last_error", "lsmgnn_profile", "lsmgnn_profile_read", "lsmgnn_sampler_attach", "lsmgnn_sample",
            "lsmgnn_prefetch_dev", "lsmgnn_graph_capture", "lsmgnn_graph_replay", "lsmgnn_debug_state",
-           "lsmgnn_sampler_place"]
+           "lsmgnn_sampler_place", "lsmgnn_plan_handle", "lsmgnn_check_handles", "lsmgnn_disconnect"]
 PHASES = ["route", "dedup", "probe_replace", "admit", "fill", "pull", "window", "pvp"]
 
 
@@ -83,6 +83,10 @@ def load_library(path: str = SO_PATH) -> ctypes.CDLL:
         "lsmgnn_graph_replay": ([vp], i32),
         "lsmgnn_debug_state": ([i32, vp, i64], i32),
         "lsmgnn_sampler_place": ([i32], i32),
+        "lsmgnn_plan_handle": ([ctypes.POINTER(Options), i64, i32, i32, i64, i32, i64, i32, i32, vp, ctypes.c_size_t],
+                               i32),
+        "lsmgnn_check_handles": ([vp, i32, vp], i32),
+        "lsmgnn_disconnect": ([], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -102,6 +106,33 @@ def _stream_ptr(stream) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
     return int(stream.cuda_stream)
+
+
+def plan_handle(num_nodes, feat_dim, lines_per_gpu, ways, victim_lines=0, *, rank=0, world=1, dtype=F32,
+                policy="hybrid", pvp=0, window=256, threshold=0, reinsert=1, max_batch_ids=1 << 20, period=1) -> bytes:
+    """Host-only (no GPU): the layout handle rank `rank` of `world` would export for these
+    lsmgnn_init arguments (lsmgnn_plan_handle); raises LsmGnnError for arguments init rejects."""
+    L = load_library()
+    opt = Options(1, POLICY[policy] if isinstance(policy, str) else int(policy), int(pvp), int(window),
+                  int(threshold), int(period), int(reinsert), int(max_batch_ids))
+    nb = L.lsmgnn_handle_bytes()
+    buf = ctypes.create_string_buffer(nb)
+    _check(L.lsmgnn_plan_handle(ctypes.byref(opt), int(num_nodes), int(feat_dim), int(dtype), int(lines_per_gpu),
+                                int(ways), int(victim_lines), int(rank), int(world), buf, nb))
+    return bytes(buf.raw)
+
+
+def check_handles(blobs, mine: bytes) -> int:
+    """lsmgnn_connect's validation of the all-gathered blobs (rank order) against `mine`:
+    returns the C return code (0 or LSMGNN_ECOMM = -6) without raising."""
+    L = load_library()
+    allb = ctypes.create_string_buffer(b"".join(blobs), max(1, sum(len(b) for b in blobs)))
+    me = ctypes.create_string_buffer(mine, len(mine))
+    return int(L.lsmgnn_check_handles(allb, len(blobs), me))
+
+
+def last_error() -> str:
+    return load_library().lsmgnn_last_error().decode()
 
 
 class LsmGnn:
@@ -272,7 +303,9 @@ class LsmGnn:
             import torch
             import torch.distributed as dist
             torch.cuda.synchronize(self.device)
-            dist.barrier(group=self._group)
+            dist.barrier(group=self._group)  # nobody pulls from a peer any more
+            _LIB.lsmgnn_disconnect()         # close this rank's mappings of the peers' arenas
+            dist.barrier(group=self._group)  # every mapping of every arena is closed
         _LIB.lsmgnn_finalize()
 
 

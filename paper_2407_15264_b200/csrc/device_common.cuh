@@ -85,11 +85,11 @@ __device__ __forceinline__ void pdl_prologue() {
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
-// Warp-aggregated atomicAdd of `inc` per lane: one atomic per warp. Must be called
-// by all 32 lanes (inactive lanes pass inc = 0). Returns this lane's base offset.
 // CTA-wide reservation of one slot per thread with want == true: one atomicAdd per CTA on the
 // shared counter instead of one per warp (a hot single address). Every thread of the CTA must
-// call it (CTA-uniform control flow). Slot order within the CTA follows thread order.
+// call it (CTA-uniform control flow), and blockDim.x must be a multiple of 32 (full-warp
+// ballots; every launch of a kernel using it has 256 threads). Slot order within the CTA
+// follows thread order.
 __device__ __forceinline__ uint32_t block_reserve(uint32_t* ctr, bool want) {
   __shared__ uint32_t s_cnt[32];
   __shared__ uint32_t s_base;
@@ -111,6 +111,8 @@ __device__ __forceinline__ uint32_t block_reserve(uint32_t* ctr, bool want) {
   __syncthreads();  // s_cnt / s_base are reused by the next call
   return r;
 }
+// Warp-aggregated atomicAdd of `inc` per lane: one atomic per warp. Must be called
+// by all 32 lanes (inactive lanes pass inc = 0). Returns this lane's base offset.
 __device__ __forceinline__ uint32_t warp_reserve(uint32_t* ctr, uint32_t inc) {
   const uint32_t lane = lane_id();
   uint32_t incl = inc;

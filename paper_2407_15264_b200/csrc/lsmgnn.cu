@@ -214,6 +214,10 @@ struct Ctx {
   cudaEvent_t ev_feed = nullptr;
   bool feed_recorded = false, feed_since_gather = false;
   cudaStream_t last_stream = nullptr;
+  // stream of the last gather: a gather issued on another stream first waits for the end of
+  // the previous one (k_begin resets the per-iteration state and scratch it still uses; at
+  // G > 1 the homes would otherwise rewrite node_loc / pool slots a pull of t still reads)
+  cudaStream_t gather_st = nullptr;
   int64_t* tmp_ids = nullptr;  // for lsmgnn_gather_host
   void* tmp_out = nullptr;
 
@@ -828,7 +832,9 @@ int launch_pvp(cudaStream_t st) {
   // kernels, the PCIe-bound copy held the SMs they need and delayed the feed (and everything
   // queued behind it on the caller's stream, e.g. training) by its whole duration
   // (profiles/r01_pvp_overlap.md); after the feed it overlaps the caller's next work instead
-  if (g.feed_recorded) CK(cudaStreamWaitEvent(g.side, g.ev_feed, 0));
+  // At G > 1 the feed event completes only after every rank's window exchange, which would
+  // gate this copy on the slowest rank; there the copy keeps its gather-only dependencies.
+  if (g.feed_recorded && g.world == 1) CK(cudaStreamWaitEvent(g.side, g.ev_feed, 0));
   uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
   const int blocks = g.sms * std::min(2, g.geom_per_sm);
   prof_begin(7, g.side);
@@ -939,6 +945,91 @@ int resolve_out(void*& out, bool& out_host, int64_t n) {
   return 0;
 }
 
+// ---- layout of one home (host only, no CUDA call): every size and arena offset follows from
+// (options, num_nodes, feat_dim, dtype, lines, ways, victim_lines, world). lsmgnn_init applies
+// it; lsmgnn_plan_handle evaluates it without a GPU (the handle checks are then testable on
+// any host). Returns LSMGNN_EINVAL with a message for any argument lsmgnn_init rejects.
+int plan_layout(Ctx& c, int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t lines_per_gpu,
+                int32_t ways, int64_t victim_lines) {
+  const int esz = dtype == LSMGNN_F32 ? 4 : (dtype == LSMGNN_F16 || dtype == LSMGNN_BF16) ? 2 : 0;
+  if (esz == 0) return set_err(LSMGNN_EINVAL, "bad dtype");
+  if (num_nodes < 1 || num_nodes > 0xFFFFFFF0ll) return set_err(LSMGNN_EINVAL, "num_nodes must be 1..2^32-16");
+  if (feat_dim < 1) return set_err(LSMGNN_EINVAL, "bad feat_dim");
+  const int64_t R = (int64_t)feat_dim * esz;
+  if (R % 16) return set_err(LSMGNN_EINVAL, "row bytes %lld not a multiple of 16 (DESIGN.md R22)", (long long)R);
+  if (ways < 1 || ways > 32) return set_err(LSMGNN_EINVAL, "ways must be 1..32");
+  if (lines_per_gpu < ways || lines_per_gpu % ways) return set_err(LSMGNN_EINVAL, "lines_per_gpu must be a positive multiple of ways");
+  if (lines_per_gpu >= (1ll << 31)) return set_err(LSMGNN_EINVAL, "lines_per_gpu too large");
+  const int G = c.world;
+  c.N = (uint64_t)num_nodes;
+  c.R = (uint32_t)R;
+  c.nvec = (uint32_t)(R / 16);
+  c.A = (uint32_t)ways;
+  c.L = (uint64_t)lines_per_gpu;
+  c.S = c.L / c.A;
+  c.Q = (c.N + G - 1) / G;
+  if (c.Q >= (uint64_t)kHostBit)  // FillEnt::src keeps a home row index in 31 bits
+    return set_err(LSMGNN_EINVAL, "ceil(num_nodes / world) must be < 2^31 (use more homes)");
+  c.W = (uint32_t)c.opt.window;
+  c.Wp1 = c.W + 1;
+  c.T = c.opt.threshold ? (uint32_t)c.opt.threshold : std::max<uint32_t>(1, c.W / 8);
+  c.MW = (c.Wp1 + 31) / 32;
+  c.C = c.opt.pvp ? (uint64_t)victim_lines / c.W : 0;
+  if (c.opt.pvp && c.C < 1) return set_err(LSMGNN_EINVAL, "pvp needs victim_lines >= window");
+  c.cap = (uint64_t)c.opt.max_batch_ids;
+  c.ucap = std::min<uint64_t>(c.cap * G, c.Q);  // unique nodes per batch at a home
+  c.bcap = c.ucap;                              // bypass staging rows
+  c.stage_base0 = c.L;
+  c.bypass_base = c.L + 2 * c.C;
+  c.pool_rows = c.L + 2 * c.C + c.bcap;
+  if (c.pool_rows >= (uint64_t)kHostBit) return set_err(LSMGNN_EINVAL, "pool too large for 31-bit rows");
+  // k_set per-warp shared memory: the largest possible bucket of one set
+  const uint64_t maxm = std::min<uint64_t>((c.Q + c.S - 1) / c.S, c.ucap);
+  c.P = 32;
+  while (c.P < maxm && c.P < 1024) c.P <<= 1;  // larger buckets fall back to global scratch
+  c.warp_bytes = (uint32_t)align_up(20ull * c.P + 4 * 32 * 4, 16);
+  c.set_warps = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(8, (160 * 1024) / c.warp_bytes));
+  // ---- shared arena: [flags | inbox_cnt | win_cnt | inbox | win_inbox | node_loc | pool]
+  size_t o = 0;
+  c.off_flags = o; o = align_up(o + 5 * G * sizeof(uint32_t), 256);
+  c.off_icnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
+  c.off_wcnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
+  c.off_inbox = o; o = align_up(o + (size_t)G * c.cap * sizeof(uint32_t), 256);
+  c.off_win = o;   o = align_up(o + (G > 1 ? (size_t)G * c.cap * sizeof(uint32_t) : 0), 256);
+  c.off_loc = o;   o = align_up(o + c.Q * sizeof(uint32_t), 4096);
+  c.off_pool = o;  o = align_up(o + c.pool_rows * (size_t)c.R, 4096);
+  c.arena_bytes = o;
+  return 0;
+}
+
+// The layout part of a rank's handle (everything but the IPC handle and the GPU UUID): two
+// ranks can map each other's arenas only if every offset and size agrees.
+void layout_handle(const Ctx& c, Handle* h) {
+  std::memset(h, 0, sizeof *h);
+  h->arena_bytes = c.arena_bytes;
+  uint64_t x = 1469598103934665603ull;  // FNV-1a over the layout words
+  const uint64_t words[] = {c.off_flags, c.off_icnt, c.off_wcnt, c.off_inbox, c.off_win, c.off_loc, c.off_pool,
+                            c.pool_rows, c.cap, c.R, c.N, c.L, c.A, c.W, c.C, (uint64_t)c.world};
+  for (uint64_t w : words)
+    for (int b = 0; b < 8; ++b) x = (x ^ ((w >> (8 * b)) & 0xFF)) * 1099511628211ull;
+  h->layout_sig = x;
+  h->rank = c.rank;
+  h->world = c.world;
+}
+
+// Every rank's handle must carry its own rank (rank order), the same world and the same
+// layout as this rank's; returns 0 or LSMGNN_ECOMM naming the first offending peer.
+int check_handles(const Handle* hs, int32_t world, const Handle& mine) {
+  if (world != mine.world) return set_err(LSMGNN_ECOMM, "world mismatch: %d handles for a world of %d", world, mine.world);
+  for (int r = 0; r < world; ++r) {
+    if (hs[r].rank != r) return set_err(LSMGNN_ECOMM, "handle %d carries rank %d (handles must be in rank order)", r, hs[r].rank);
+    if (hs[r].world != world) return set_err(LSMGNN_ECOMM, "peer %d was initialised for a world of %d, not %d", r, hs[r].world, world);
+    if (hs[r].layout_sig != mine.layout_sig || hs[r].arena_bytes != mine.arena_bytes)
+      return set_err(LSMGNN_ECOMM, "peer %d handle does not match this rank's layout (arguments or options differ)", r);
+  }
+  return 0;
+}
+
 }  // namespace
 
 // ====================================================================================== C-ABI
@@ -975,49 +1066,12 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
                 int64_t victim_lines, const uint8_t* static_scores) {
   if (g.inited) return set_err(LSMGNN_ESTATE, "already initialised");
   if (!g.opt_set) g.opt = default_options();
-  const int esz = dtype == LSMGNN_F32 ? 4 : (dtype == LSMGNN_F16 || dtype == LSMGNN_BF16) ? 2 : 0;
-  if (esz == 0) return set_err(LSMGNN_EINVAL, "bad dtype");
-  if (num_nodes < 1 || num_nodes > 0xFFFFFFF0ll) return set_err(LSMGNN_EINVAL, "num_nodes must be 1..2^32-16");
-  if (feat_dim < 1) return set_err(LSMGNN_EINVAL, "bad feat_dim");
-  const int64_t R = (int64_t)feat_dim * esz;
-  if (R % 16) return set_err(LSMGNN_EINVAL, "row bytes %lld not a multiple of 16 (DESIGN.md R22)", (long long)R);
-  if (ways < 1 || ways > 32) return set_err(LSMGNN_EINVAL, "ways must be 1..32");
-  if (lines_per_gpu < ways || lines_per_gpu % ways) return set_err(LSMGNN_EINVAL, "lines_per_gpu must be a positive multiple of ways");
-  if (lines_per_gpu >= (1ll << 31)) return set_err(LSMGNN_EINVAL, "lines_per_gpu too large");
+  if (int rc = plan_layout(g, num_nodes, feat_dim, dtype, lines_per_gpu, ways, victim_lines)) return rc;
   if (g.device < 0) CK(cudaGetDevice(&g.device));
   CK(cudaSetDevice(g.device));
   CK(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, g.device));
-
   const int G = g.world;
-  g.N = (uint64_t)num_nodes;
-  g.R = (uint32_t)R;
-  g.nvec = (uint32_t)(R / 16);
-  g.A = (uint32_t)ways;
-  g.L = (uint64_t)lines_per_gpu;
-  g.S = g.L / g.A;
-  g.Q = (g.N + G - 1) / G;
-  if (g.Q >= (uint64_t)kHostBit)  // FillEnt::src keeps a home row index in 31 bits
-    return set_err(LSMGNN_EINVAL, "ceil(num_nodes / world) must be < 2^31 (use more homes)");
-  g.W = (uint32_t)g.opt.window;
-  g.Wp1 = g.W + 1;
-  g.T = g.opt.threshold ? (uint32_t)g.opt.threshold : std::max<uint32_t>(1, g.W / 8);
-  g.MW = (g.Wp1 + 31) / 32;
-  g.C = g.opt.pvp ? (uint64_t)victim_lines / g.W : 0;
-  if (g.opt.pvp && g.C < 1) return set_err(LSMGNN_EINVAL, "pvp needs victim_lines >= window");
-  g.cap = (uint64_t)g.opt.max_batch_ids;
-  g.ucap = std::min<uint64_t>(g.cap * G, g.Q);  // unique nodes per batch at a home
-  g.bcap = g.ucap;                              // bypass staging rows
-  g.stage_base0 = g.L;
-  g.bypass_base = g.L + 2 * g.C;
-  g.pool_rows = g.L + 2 * g.C + g.bcap;
-  if (g.pool_rows >= (uint64_t)kHostBit) return set_err(LSMGNN_EINVAL, "pool too large for 31-bit rows");
-  // k_set per-warp shared memory: the largest possible bucket of one set
-  const uint64_t maxm = std::min<uint64_t>((g.Q + g.S - 1) / g.S, g.ucap);
-  g.P = 32;
-  while (g.P < maxm && g.P < 1024) g.P <<= 1;  // larger buckets fall back to global scratch
-  const bool big_sets = maxm > g.P;
-  g.warp_bytes = (uint32_t)align_up(20ull * g.P + 4 * 32 * 4, 16);
-  g.set_warps = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(8, (160 * 1024) / g.warp_bytes));
+  const bool big_sets = std::min<uint64_t>((g.Q + g.S - 1) / g.S, g.ucap) > g.P;
   if (const char* geo = getenv("LSMGNN_GEOMETRY")) {  // launch-geometry override: results must not change
     if (!strcmp(geo, "small")) {
       g.set_warps = 1;
@@ -1025,17 +1079,6 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     }
   }
 
-
-  // ---- shared arena
-  size_t o = 0;
-  g.off_flags = o; o = align_up(o + 5 * G * sizeof(uint32_t), 256);
-  g.off_icnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
-  g.off_wcnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
-  g.off_inbox = o; o = align_up(o + (size_t)G * g.cap * sizeof(uint32_t), 256);
-  g.off_win = o;   o = align_up(o + (G > 1 ? (size_t)G * g.cap * sizeof(uint32_t) : 0), 256);
-  g.off_loc = o;   o = align_up(o + g.Q * sizeof(uint32_t), 4096);
-  g.off_pool = o;  o = align_up(o + g.pool_rows * (size_t)g.R, 4096);
-  g.arena_bytes = o;
   CK(cudaMalloc(&g.arena, g.arena_bytes));
   CK(cudaMemset(g.arena, 0, g.off_pool));
   for (int h = 0; h < kMaxG; ++h) g.peer_arena[h] = nullptr;
@@ -1172,11 +1215,8 @@ int lsmgnn_export_handle(void* buf, size_t cap) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "export before init");
   if (!buf || cap < sizeof(Handle)) return set_err(LSMGNN_EINVAL, "buffer too small");
   Handle h{};
+  layout_handle(g, &h);
   CK(cudaIpcGetMemHandle(&h.ipc, g.arena));
-  h.arena_bytes = g.arena_bytes;
-  h.layout_sig = (g.off_pool * 1315423911ull) ^ (g.pool_rows << 17) ^ g.cap ^ ((uint64_t)g.R << 40);
-  h.rank = g.rank;
-  h.world = g.world;
   cudaDeviceProp prop{};
   CK(cudaGetDeviceProperties(&prop, g.device));
   std::memcpy(h.gpu_uuid, &prop.uuid, sizeof h.gpu_uuid);
@@ -1184,20 +1224,50 @@ int lsmgnn_export_handle(void* buf, size_t cap) {
   return 0;
 }
 
+int lsmgnn_plan_handle(const lsmgnn_options* opt, int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype,
+                       int64_t lines_per_gpu, int32_t ways, int64_t victim_lines, int32_t rank, int32_t world,
+                       void* buf, size_t cap) {
+  if (!buf || cap < sizeof(Handle)) return set_err(LSMGNN_EINVAL, "buffer too small");
+  if (world < 1 || world > kMaxG || rank < 0 || rank >= world)
+    return set_err(LSMGNN_EINVAL, "bad rank/world (%d/%d); world must be 1..%d", rank, world, kMaxG);
+  Ctx* c = new Ctx();  // a scratch context: nothing is allocated, no CUDA call is made
+  c->rank = rank;
+  c->world = world;
+  c->opt = opt ? *opt : default_options();
+  int rc = 0;
+  if (opt && opt->version != LSMGNN_ABI_VERSION) rc = set_err(LSMGNN_EINVAL, "bad options/version");
+  if (!rc) rc = plan_layout(*c, num_nodes, feat_dim, dtype, lines_per_gpu, ways, victim_lines);
+  if (!rc) {
+    Handle h{};
+    layout_handle(*c, &h);
+    std::memcpy(buf, &h, sizeof h);
+  }
+  delete c;
+  return rc;
+}
+
+int lsmgnn_check_handles(const void* handles, int32_t world, const void* mine) {
+  if (!handles || !mine || world < 1 || world > kMaxG) return set_err(LSMGNN_EINVAL, "bad handle arguments");
+  Handle me{};
+  std::memcpy(&me, mine, sizeof me);
+  std::vector<Handle> hs((size_t)world);
+  std::memcpy(hs.data(), handles, sizeof(Handle) * (size_t)world);
+  return check_handles(hs.data(), world, me);
+}
+
 int lsmgnn_connect(const void* peer_handles, int32_t world) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "connect before init");
-  if (world != g.world) return set_err(LSMGNN_EINVAL, "world mismatch");
-  if (world == 1) {
+  if (!peer_handles) return set_err(LSMGNN_EINVAL, "null handles");
+  if (world == 1 && g.world == 1) {
     g.connected = true;
     return 0;
   }
   Handle mine{};
   if (int rc = lsmgnn_export_handle(&mine, sizeof mine)) return rc;
-  const Handle* hs = reinterpret_cast<const Handle*>(peer_handles);
+  std::vector<Handle> hs((size_t)std::max(1, std::min<int32_t>(world, kMaxG)));
+  if (world >= 1 && world <= kMaxG) std::memcpy(hs.data(), peer_handles, sizeof(Handle) * (size_t)world);
+  if (int rc = check_handles(hs.data(), world, mine)) return rc;
   for (int r = 0; r < world; ++r) {
-    if (hs[r].rank != r || hs[r].world != world || hs[r].layout_sig != mine.layout_sig ||
-        hs[r].arena_bytes != mine.arena_bytes)
-      return set_err(LSMGNN_ECOMM, "peer %d handle does not match this rank's layout", r);
     if (r == g.rank) continue;
     void* p = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&p, hs[r].ipc, cudaIpcMemLazyEnablePeerAccess);
@@ -1232,10 +1302,13 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
     g.feed_since_gather = false;
   }
+  if (t > 0 && st != g.gather_st)  // same stream: already ordered (and PDL keeps chaining)
+    if (int rc = wait_gather_end(t - 1, st)) return rc;
   const BeginArgs ba = begin_args(t, node_ids, n, nullptr, nullptr, 0);
   if (int rc = launch_gather(ba, n, out, out_host, false, (uint32_t)(t + 1), st)) return rc;
   if (int rc = note_gather_end(t, st)) return rc;
   g.t_next = t + 1;
+  g.gather_st = st;
   g.last_stream = st;
   return 0;
 }
@@ -1572,6 +1645,7 @@ int lsmgnn_graph_replay(void* stream) {
   if (int rc = wait_gather_end(g.t_next - 1, st)) return rc;  // the replay's feed follows gather(t-1)
   CK(cudaGraphLaunch(g.graph_exec, st));
   if (int rc = note_gather_end(g.t_next, st)) return rc;
+  g.gather_st = st;
   if (int rc = feed_end(st)) return rc;  // the replay fed t+1+W itself
   g.launches += g.graph_launches;
   g.t_next += 1;
@@ -1620,6 +1694,19 @@ int lsmgnn_profile_read(double* ms, int64_t* cnt) {
     g.ev_pool.push_back(sp.b);
   }
   g.spans.clear();
+  return 0;
+}
+
+int lsmgnn_disconnect(void) {
+  if (!g.inited) return 0;
+  CK(cudaDeviceSynchronize());
+  for (int h = 0; h < kMaxG; ++h) {
+    if (g.peer_arena[h] && g.peer_arena[h] != g.arena) {
+      cudaIpcCloseMemHandle(g.peer_arena[h]);
+      g.peer_arena[h] = nullptr;
+    }
+  }
+  g.connected = g.world == 1;
   return 0;
 }
 

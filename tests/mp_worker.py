@@ -26,17 +26,53 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo")
     if mode == "cpu":
-        # host-side bootstrap logic: every rank contributes a blob, all see all in rank order
-        blob = bytes([rank]) * 8
-        blobs = [None] * world
-        dist.all_gather_object(blobs, blob)
-        assert blobs == [bytes([r]) * 8 for r in range(world)]
+        # host-side bootstrap logic of lsmgnn_connect, across two real processes over gloo: each
+        # rank plans the handle it would export (lsmgnn_plan_handle, no GPU), the blobs are
+        # all-gathered in rank order, and lsmgnn_connect's validation (lsmgnn_check_handles) runs
+        # on every rank — matching layouts pass; rank order, world and layout mismatches fail
+        from paper_2407_15264_b200 import LsmGnnError, check_handles, last_error, plan_handle
+        ECOMM = -6
+        res = {"rank": rank}
+
+        def exchange(blob):
+            blobs = [None] * world
+            dist.all_gather_object(blobs, blob)
+            return blobs
+
+        base = dict(num_nodes=16384, feat_dim=128, lines_per_gpu=1024, ways=8, victim_lines=512, pvp=1, window=8,
+                    max_batch_ids=4096)
+        mine = plan_handle(**base, rank=rank, world=world)
+        blobs = exchange(mine)
+        res["ok"] = check_handles(blobs, mine)
+        res["reversed"] = check_handles(blobs[::-1], mine)
+        res["reversed_msg"] = last_error()
+        res["short"] = check_handles(blobs[:1], mine)  # fewer handles than the world
+        # rank 1 initialised with different arguments / options / world: every rank must refuse
+        for name, change in (("lines", dict(lines_per_gpu=2048)), ("max_batch_ids", dict(max_batch_ids=4097)),
+                             ("pvp", dict(pvp=0)), ("window", dict(window=16)), ("row_bytes", dict(feat_dim=132))):
+            b = plan_handle(**dict(base, **change), rank=rank, world=world) if rank == 1 else mine
+            res[name] = check_handles(exchange(b), mine)
+            res[name + "_msg"] = last_error()
+        w3 = plan_handle(**base, rank=rank, world=3) if rank == 1 else mine
+        res["world"] = check_handles(exchange(w3), mine)
+        res["world_msg"] = last_error()
+        try:
+            plan_handle(**dict(base, feat_dim=3), rank=rank, world=world)  # R = 12 bytes
+            res["bad_args"] = "accepted"
+        except LsmGnnError as e:
+            res["bad_args"] = str(e)
+        try:
+            plan_handle(**base, rank=world, world=world)
+            res["bad_rank"] = "accepted"
+        except LsmGnnError as e:
+            res["bad_rank"] = str(e)
+        # the home partition each rank's batches are routed by (v mod G)
         import synth
         g = synth.plcite(4096, 4)
         tr = synth.make_trace(g, world, 32, (4, 2), 3)
-        mine = [tr[t][rank] for t in range(3)]
-        homes = [np.unique(x % world) for x in mine]
-        json.dump({"rank": rank, "homes": [h.tolist() for h in homes]}, open(os.path.join(outdir, f"r{rank}.json"), "w"))
+        res["homes"] = [np.unique(tr[t][rank] % world).tolist() for t in range(3)]
+        res["ECOMM"] = ECOMM
+        json.dump(res, open(os.path.join(outdir, f"r{rank}.json"), "w"))
         dist.barrier()
         dist.destroy_process_group()
         return

@@ -84,6 +84,17 @@ def run_checked(o, trace, C):
                 if byp and ins:
                     assert max(byp) <= min(ins)
         o.pvp_prefetch(t)
+        # I5 including the PVP staging buffer: a staged node is this home's, is staged once,
+        # and is neither cached nor still queued (the copy empties its queue)
+        for g in range(G):
+            stg = o.staging(g).tolist()
+            assert len(stg) == len(set(stg)) and all(x % G == g for x in stg)
+            tags, _ = o.tags(g)
+            assert not set(stg) & set(tags[tags >= 0].tolist()), f"t={t} home {g}: staged node also cached"
+            queued = set()
+            for k in range(W):
+                queued |= set(o.queue(g, k)[0].tolist())
+            assert not set(stg) & queued, f"t={t} home {g}: staged node still queued"
         o.feed(t + 1 + W, trace[t + 1 + W] if t + 1 + W < K else empty)
     return np.stack(allc)
 

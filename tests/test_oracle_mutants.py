@@ -56,6 +56,12 @@ MUTANTS = [
      "Part 1: out[i] = table[ids[i]]"),
     ("staging_not_cleared", "free(h->staging); h->staging = NULL; h->nstaging = 0;\n    cnt->pvp_prefetched",
      "cnt->pvp_prefetched", "P:398 prefetched rows are single-use"),
+    ("pvp_unused_dropped", "if (!contains_sorted(U, nu, h->staging[j])) cnt->pvp_unused++;",
+     "if (!contains_sorted(U, nu, h->staging[j])) {}", "§8(b): pvp_unused counts staged rows not requested"),
+    ("pvp_unused_inverted", "if (!contains_sorted(U, nu, h->staging[j])) cnt->pvp_unused++;",
+     "if (contains_sorted(U, nu, h->staging[j])) cnt->pvp_unused++;", "§8(c): pvp_unused = |staging \\ U|"),
+    ("queue_not_emptied", "h->pending_prefetched = (uint64_t)h->nstaging;\n        h->qlen[k] = 0;",
+     "h->pending_prefetched = (uint64_t)h->nstaging;", "§8(c): Q_g[(t+1) mod W] = ∅ after the copy"),
     ("update_period_ignored", "return o->c.P <= 1 || t % o->c.P == 0;", "return 1;", "R6: scan every P iterations"),
 ]
 

@@ -405,3 +405,28 @@ def test_admission_order_on_overflow(seed):
         o.pvp_prefetch(t)
         o.feed(t + 1 + W, trace[t + 1 + W] if t + 1 + W < K else empty)
     assert overflowed > 0
+
+def test_pvp_unused_window_mismatch():
+    """§8(b) "pvp_unused counts the mismatches" when the window batches differ from the gathered
+    ones: hand-derived trace (tests/golden/pvp_unused_window_mismatch.json) where the victim
+    staged for iteration 3 (the window said {2}) is not requested by the batch gathered ({4})."""
+    gold = json.load(open(os.path.join(GOLD, "pvp_unused_window_mismatch.json")))
+    su = gold["setup"]
+    o = Oracle(su["G"], su["N"], su["R"], su["L"], su["A"], np.zeros(su["N"], np.uint8), policy=su["policy"],
+               pvp=su["pvp"], W=su["W"], T=su["T"], V=su["V"])
+    win = [[np.array(b)] for b in gold["window_batches"]]
+    gat = [[np.array(b)] for b in gold["gathered_batches"]]
+    W, K = su["W"], len(gat)
+    empty = [np.zeros(0, np.int64)]
+    for k in range(1, W + 1):
+        o.feed(k, win[k] if k < K else empty)
+    rows = []
+    for t in range(K):
+        c, _ = o.gather(t, gat[t])
+        rows.append(c[0])
+        o.pvp_prefetch(t)
+        o.feed(t + 1 + W, win[t + 1 + W] if t + 1 + W < K else empty)
+    rows = np.stack(rows)
+    for k, want in gold["per_iteration"].items():
+        assert rows[:, F[k]].tolist() == want, k
+    assert o.staging(0).size == 0  # single use: nothing staged after the last prefetch
