@@ -71,6 +71,8 @@ class ClockSampler:
         self.path = f"/tmp/lsmgnn_clocks_{os.getpid()}.csv"
 
     def start(self):
+        """Start sampling and wait (<= 5 s) until the first sample is written: nvidia-smi takes a
+        while to come up, and the timed region of a short run is a fraction of a second."""
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -78,6 +80,12 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and self.proc.poll() is None:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.02)
 
     def stop(self) -> dict:
         if not self.proc:
@@ -116,6 +124,21 @@ def build_inputs(wl, G, rank, iters, only_mine=False):
     return g, trace, scores
 
 
+def config_dict(wl, args, G) -> dict:
+    """The `config` object of the JSON line — identical for both arms (--impl lsmgnn and
+    --impl reference) at the same arguments: it names the workload only."""
+    pvp = wl.pvp if args.pvp is None else args.pvp
+    lines = args.lines or wl.lines_per_gpu
+    return {"workload": f"{wl.name} (BASELINE.json configs[1], IGB-small-shaped)" if wl.name == "cfg2" else wl.name,
+            "N": wl.N, "row_bytes": wl.R, "payload": f"fp32 rows ({wl.D}-dim), copied bytewise",
+            "batch_per_rank": wl.batch, "fanout": list(wl.fanout), "lines_per_gpu": lines, "ways": wl.ways,
+            "window": wl.window, "threshold": max(1, wl.window // 8), "policy": args.policy, "pvp": pvp,
+            "victim_lines": wl.victim_lines if pvp else 0, "parallelism": f"shared cache over {G} GPU",
+            "l2": f"inputs larger than L2 (126 MB): cache {lines * wl.R / 1e6:.0f} MB per home, host table "
+                  f"{wl.N * wl.R / 1e9:.1f} GB, every step's rows to a {wl.R}-byte-row out buffer",
+            "seeds": wl.seeds}
+
+
 def run_reference(args, wl, G, rank):
     """--impl reference: the CPU oracle (as it stands) timed on the host cores, same metric."""
     if rank != 0:
@@ -148,10 +171,7 @@ def run_reference(args, wl, G, rank):
     line = {"impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": G,
             "steps": K, "warmup": Wu, "ms_per_step": round(tsum / K * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": wl.name + " (" + ("IGB-small-shaped" if wl.name == "cfg2" else wl.name) + ")",
-                       "N": wl.N, "row_bytes": wl.R, "batch_per_rank": wl.batch, "fanout": list(wl.fanout),
-                       "lines_per_gpu": args.lines or wl.lines_per_gpu, "ways": wl.ways, "window": wl.window,
-                       "policy": args.policy, "pvp": pvp},
+            "config": config_dict(wl, args, G),
             "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "host": dict(host_cpu(), pinned_cpu=core),
                              "sample": f"full {wl.name} iterations {Wu}..{Wu + K - 1} after {Wu} untimed, rows "
@@ -296,6 +316,9 @@ def main():
         if args.graph and t == 0:
             c.graph_capture(ids_d, out)
 
+    # clocks are sampled from before the warm-up to the end of the timed region
+    clocks = ClockSampler(local)
+    clocks.start()
     for t in range(Wu):
         step(t)
     torch.cuda.synchronize()
@@ -303,8 +326,6 @@ def main():
         torch.distributed.barrier()
     s0 = c.stats(1)
     l0 = c.kernel_launches()
-    clocks = ClockSampler(local)
-    clocks.start()
     if not args.no_profile:
         c.profile(True)
         c.profile_read()  # reset
@@ -439,9 +460,18 @@ def main():
         phases[name] = {"ms": round(ms, 3), "launch_spans": n, "share_of_step": round(ms / (T * 1e3), 4)}
     # algorithmic bytes: fill moves storage rows H2D + victim rows D2H, and
     # writes every installed/bypassed row into HBM; pull reads + writes R per request.
+    my_req = sum(mine[Wu + i].size for i in range(K))
+    my_remote = sum(int(np.count_nonzero(mine[Wu + i] % G != rank)) for i in range(K)) if G > 1 else 0
+    tb = tier_bytes(d, my_req, my_remote, R)
+    tb_max = dict(tb)
+    if G > 1:  # the slowest home sets T_roof: every tier's bytes, max over ranks
+        keys = sorted(tb)
+        x = torch.tensor([float(tb[k]) for k in keys], dtype=torch.float64, device=cdev)
+        torch.distributed.all_reduce(x, op=torch.distributed.ReduceOp.MAX)
+        tb_max = {k: float(v) for k, v in zip(keys, x.tolist())}
     fill_pcie = (d["storage_reads"] + 0) * R
     fill_ms = prof.get("fill", (0.0, 0))[0]
-    pull_bytes = 2 * d["requests"] * R
+    pull_bytes = 2 * my_req * R  # this rank's rows: read at their home + written to out
     pull_ms = prof.get("pull", (0.0, 0))[0]
     roof = None
     if fill_ms > 0:
@@ -475,25 +505,40 @@ def main():
         phases["pull"]["note"] = ("G = 1: delivery to out is fused into k_serve (fill phase); this span is empty "
                                   "(event overhead only), so no bandwidth is derived from it")
     elif pull_ms > 0:
+        # G > 1: the requester's pull reads its rows at the homes (peer rows over NVLink) and
+        # writes them to out. Fraction of the NVLink peer-copy peak for the rows from peers
+        # (this rank), and of HBM for all bytes the pull moves. With the split pull, phase 0
+        # runs on a second stream during the fill: the span timed here is the part after
+        # "served" (phase 1 + the wait for phase 0), so these are lower bounds on the rates.
         ach = pull_bytes / (pull_ms / 1e3) / 1e9
         phases["pull"]["hbm_GBps"] = round(ach, 1)
         phases["pull"]["frac_hbm"] = round(ach / hbm_peak, 4)
         phases["pull"]["hbm_peak_source"] = hbm_src
+        nvl = my_remote * R / (pull_ms / 1e3) / 1e9
+        phases["pull"]["nvlink_in_GBps"] = round(nvl, 2)
+        phases["pull"]["frac_nvlink"] = round(nvl / NVLINK_PEAK, 4)
+        phases["pull"]["nvlink_peak_source"] = "770 GB/s per direction, measured peer copy (B200_PROFILING.md)"
+        phases["pull"]["peer_bytes_per_step"] = int(my_remote * R / K)
+        if ndev < G:
+            phases["pull"]["note"] = "ranks share one GPU: 'peer' rows are IPC mappings of the same HBM, not NVLink"
+    if G > 1 and roof is not None and pull_ms > fill_ms and my_remote:
+        # the pull dominates this rank's step: report it against the NVLink peer-copy peak
+        nvl = my_remote * R / (pull_ms / 1e3) / 1e9
+        roof = {"bound": "nvlink", "kernel": "k_pull", "achieved": round(nvl, 2), "peak": NVLINK_PEAK, "unit": "GB/s",
+                "frac": round(nvl / NVLINK_PEAK, 4), "traffic": None,
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                "per_launch": {"algorithmic_bytes": int(my_remote * R / K), "units": "rows pulled from peer homes x R",
+                               "avg_ms": round(pull_ms / K, 4)},
+                "fill_roofline": roof}
     uniq = max(d["unique"], 1)
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": G, "steps": K, "warmup": Wu,
         "ms_per_step": round(T / K * 1e3, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"{wl.name} (BASELINE.json configs[1], IGB-small-shaped)" if wl.name == "cfg2"
-                   else wl.name, "N": wl.N, "row_bytes": R, "payload": "fp32 rows (1024-dim), copied bytewise",
-                   "batch_per_rank": wl.batch, "fanout": list(wl.fanout), "lines_per_gpu": lines, "ways": wl.ways,
-                   "window": W, "threshold": max(1, W // 8), "policy": args.policy, "pvp": pvp,
-                   "victim_lines": wl.victim_lines if pvp else 0, "parallelism": f"shared cache over {G} GPU" if ndev >= G else
-                   f"shared cache over {G} homes on {ndev} GPU (ranks share a device: protocol test, not a "
-                   f"multi-GPU throughput)",
-                   "l2": f"inputs larger than L2 (126 MB): cache {lines * R / 1e6:.0f} MB per home, out "
-                         f"~{d['requests'] / K * R / 1e6:.0f} MB/step, host table {wl.N * R / 1e9:.1f} GB",
-                   "seeds": wl.seeds},
+        "config": config_dict(wl, args, G),
+        "devices": {"ranks": G, "gpus_visible": ndev,
+                    "note": "one GPU per rank" if ndev >= G else "ranks share a device: a protocol test, not a "
+                                                                 "multi-GPU throughput"},
         "gpu_launches": int(launches),
         "clocks": clk,
         "roofline": roof,
@@ -515,8 +560,8 @@ def main():
                   "local_hbm_GBps_over_step": round((d["bytes_out"] - d["bytes_nvlink"]) / T / 1e9, 2),
                   "bypassed_per_step": d["bypassed"] / K, "evictions_per_step": d["evictions"] / K},
         "phases": phases,
-        # T_roof = max over tiers of bytes / peak, per step; reported as T_roof / T_meas
-        "step_roofline": step_roofline(d, K, T, R, pcie_peak, hbm_peak),
+        # T_roof = max over homes and tiers of bytes / peak, per step; reported as T_roof / T_meas
+        "step_roofline": step_roofline(tb_max, K, T, pcie_peak, hbm_peak, G),
     }
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, G, trace, scores, table.numpy(), args, lines)
@@ -757,19 +802,35 @@ def pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev, train_ms=1
     return res
 
 
-def step_roofline(d, K, T, R, pcie_peak, hbm_peak):
-    """Per-tier lower bound on the step time: H2D = storage + PVP rows,
-    D2H = admitted victims, HBM = every request's row written to out and read at its source,
-    plus every filled row written to its slot. T_roof = the slowest tier; frac = T_roof / T."""
-    h2d = (d["bytes_h2d_storage"] + d["bytes_h2d_pvp"]) / K
-    d2h = d["bytes_d2h_victim"] / K
-    hbm = (2 * d["requests"] + d["inserted"] + d["bypassed"]) * R / K
-    tiers = {"pcie_h2d": h2d / (pcie_peak * 1e9), "pcie_d2h": d2h / (pcie_peak * 1e9), "hbm": hbm / (hbm_peak * 1e9)}
+NVLINK_PEAK = 770.0  # GB/s per direction per GPU, measured peer copy (B200_PROFILING.md; 900 nominal)
+
+
+def tier_bytes(d, my_requests, my_remote, R):
+    """Bytes per tier of ONE home over the timed steps (SURVEY.md §8(d) algorithmic bytes):
+    H2D = storage + PVP rows; D2H = admitted victims; HBM = the rows this home serves (read at
+    their slot, one per request routed here) + this rank's out rows written + every filled row
+    written to its slot; NVLink in = this rank's rows pulled from peer homes; NVLink out = rows
+    peers pulled from this home (peer_requests x R)."""
+    return {"pcie_h2d": d["bytes_h2d_storage"] + d["bytes_h2d_pvp"], "pcie_d2h": d["bytes_d2h_victim"],
+            "hbm": (d["requests"] + my_requests + d["inserted"] + d["bypassed"]) * R,
+            "nvlink_in": my_remote * R, "nvlink_out": d["bytes_nvlink"]}
+
+
+def step_roofline(tb, K, T, pcie_peak, hbm_peak, G):
+    """Per-tier lower bound on the step time: T_roof = max over homes and tiers
+    of bytes / peak (tb holds each tier's max over homes); frac = T_roof / T_meas. NVLink tiers
+    against the measured 770 GB/s per direction (G > 1 only: at G = 1 nothing crosses NVLink)."""
+    peak = {"pcie_h2d": pcie_peak, "pcie_d2h": pcie_peak, "hbm": hbm_peak, "nvlink_in": NVLINK_PEAK,
+            "nvlink_out": NVLINK_PEAK}
+    tiers = {k: tb[k] / K / (peak[k] * 1e9) for k in tb if G > 1 or not k.startswith("nvlink")}
     bound = max(tiers, key=tiers.get)
     t_roof = tiers[bound]
     return {"bound_tier": bound, "t_roof_ms": round(t_roof * 1e3, 4), "t_meas_ms": round(T / K * 1e3, 4),
             "frac": round(t_roof / (T / K), 4), "tier_ms": {k: round(v * 1e3, 4) for k, v in tiers.items()},
-            "peaks_GBps": {"pcie": round(pcie_peak, 2), "hbm": hbm_peak}}
+            "tier_GB_per_step_max_over_homes": {k: round(tb[k] / K / 1e9, 4) for k in tiers},
+            "peaks_GBps": {"pcie": round(pcie_peak, 2), "hbm": hbm_peak, "nvlink": NVLINK_PEAK},
+            "peak_sources": {"pcie": "cudaMemcpy pinned H2D measured in this run", "hbm": "MEASURED_PEAKS.json",
+                             "nvlink": "B200_PROFILING.md measured peer copy per direction"}}
 
 
 def epoch_storage(wl, g, scores, lines, dev, policies=("hybrid", "static", "lru"), pvp_row=True):

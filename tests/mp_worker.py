@@ -108,6 +108,35 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         return
+    if mode == "mismatch":  # lsmgnn_connect must refuse a peer whose layout differs (ECOMM)
+        torch.cuda.set_device(rank % torch.cuda.device_count())
+        from paper_2407_15264_b200 import LsmGnn, LsmGnnError
+        from tests.harness import table_for
+        res = {"rank": rank, "mismatch_error": None}
+        try:
+            LsmGnn(4096, 32, 256 if rank == 0 else 512, 8, 0, None, window=4, max_batch_ids=64, rank=rank,
+                   world=world, group=dist.group.WORLD)
+        except LsmGnnError as e:
+            res["mismatch_error"] = str(e)
+        from paper_2407_15264_b200 import binding
+        binding._LIB.lsmgnn_finalize()
+        dist.barrier()
+        c = LsmGnn(4096, 32, 256, 8, 0, None, window=4, max_batch_ids=64, rank=rank, world=world,
+                   group=dist.group.WORLD)
+        c.attach_storage(table_for(4096, 32, pinned=True, home=rank, G=world))
+        ids = torch.arange(rank, 64 + rank, dtype=torch.int64, device="cuda")
+        out = torch.empty((64, 128), dtype=torch.uint8, device="cuda")
+        c.prefetch([ids] * 4, first_iter=1)
+        c.gather(ids, out)
+        torch.cuda.synchronize()
+        import synth
+        res["bad"] = int(synth.check_rows(out.cpu().numpy().view(np.uint32).reshape(64, 32), ids.cpu().numpy(), 32)[0])
+        res["retry_ok"] = True
+        c.close()
+        json.dump(res, open(os.path.join(outdir, f"r{rank}.json"), "w"))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if mode == "cfg3":  # full-size configs[2]: trace from the driver's npz
         torch.cuda.set_device(rank % torch.cuda.device_count())
         import synth

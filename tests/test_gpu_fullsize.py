@@ -7,7 +7,9 @@ counter is compared with the oracle and every gathered row with the closed form 
 
 configs[2] (IGB-medium-shaped, 10M nodes, 2 ranks, PVP, 4 GiB cache per GPU, 16K-line
 victim queues) runs as 2 processes sharing the GPU; it needs ~75 GB of pinned host memory
-and several minutes, so it only runs with LSMGNN_FULL=1 (its log is kept in profiles/).
+and several minutes, so it only runs with LSMGNN_FULL=1 (its log is kept in profiles/); a
+reduced configs[2] (2M nodes, same row width, cache fraction, window and PVP) runs in the
+default suite.
 """
 import json
 import os
@@ -40,6 +42,26 @@ def test_cfg2_full_size_bench_configuration():
     assert bad == 0
     compare(hg[:K], ho[:K], "cfg2 full size")
     assert ho[:K, 8].sum() > 0  # bypass regime (oversubscribed sets) exercised
+
+
+def test_cfg3_reduced_two_ranks(tmp_path):
+    """configs[2] (IGB-medium-shaped) reduced to run in the default GPU suite: 2 homes (2
+    processes), 4 KiB fp32 rows, fanout (10,5,5), W = 256, hybrid with the PVP on, the same
+    per-GPU cache fraction (10% of the nodes per GPU, 32-way), 2M nodes, batch 2048 per rank,
+    victim queues of C = 1,024 lines (V = 262,144 per home). Every counter of every home equals
+    the oracle's, every row equals F(v); both pull orders."""
+    G, K = 2, 10
+    N, batch = 2_000_000, 2048
+    g = synth.plcite(N, 12)
+    tr = synth.make_trace_parallel(g, G, batch, (10, 5, 5), K)
+    sc = synth.static_scores(g)
+    from .test_gpu_multiproc import _run_edge
+    cfg = dict(N=N, D=1024, L=100_000, A=32, policy="hybrid", pvp=1, W=256, V=256 * 1024, reinsert=1, P=1)
+    for split in (1, 0):
+        d = tmp_path / f"split{split}"
+        d.mkdir()
+        ho = _run_edge(d, G, tr, sc, cfg, split)
+    assert ho[..., 5].sum() > 0 and ho[..., 8].sum() > 0  # victim hits; bypassed (oversubscribed sets)
 
 
 @pytest.mark.skipif(os.environ.get("LSMGNN_FULL") != "1", reason="set LSMGNN_FULL=1 (needs ~75 GB pinned host RAM)")

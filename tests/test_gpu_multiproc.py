@@ -162,3 +162,54 @@ def test_multiprocess_gpu_sampler_window(tmp_path, G, pvp, split):
         hg = np.load(tmp_path / f"hist{r}.npy")
         assert np.array_equal(hg, ho[:, r, :]), (r, np.argwhere(hg != ho[:, r, :])[:3])
     assert ho[:, :, 2].sum() > 0
+
+def _run_edge(tmp_path, G, tr, sc, cfg, split):
+    np.savez(tmp_path / "trace.npz", scores=sc, **{f"t{t}_r{r}": tr[t][r] for t in range(len(tr)) for r in range(G)})
+    json.dump(cfg, open(tmp_path / "cfg.json", "w"))
+    launch(G, tmp_path, "edge", str(tmp_path), split=split)
+    cfg = dict(cfg)
+    cfg.pop("file", None)
+    cfg.pop("two_streams", None)
+    ho = run_oracle(tr, G=G, scores=sc, **cfg)
+    for r in range(G):
+        assert json.load(open(tmp_path / f"r{r}.json"))["bad"] == 0
+        hg = np.load(tmp_path / f"hist{r}.npy")
+        assert np.array_equal(hg, ho[:, r, :]), (r, np.argwhere(hg != ho[:, r, :])[:3])
+    return ho
+
+
+@pytest.mark.parametrize("G,split,V", [(2, 0, 512), (2, 1, 512), (3, 1, 64), (3, 0, 64)])
+def test_multiprocess_full_row_width(tmp_path, G, split, V):
+    """configs[0]'s trace across G homes at the bench's 4 KiB rows with the PVP on: k_fill<8>
+    (victim D2H + fills), k_pull<8, kDev, 0/1> (both pull orders), k_pvp<8> per home; V = 64
+    overflows the victim queues."""
+    N = 16384
+    g = synth.plcite(N, 8)
+    tr = synth.make_trace(g, G, 256, (10, 5), 20)
+    sc = synth.static_scores(g)
+    cfg = dict(N=N, D=1024, L=1024, A=8, policy="hybrid", pvp=1, W=8, V=V, reinsert=1, P=1)
+    ho = _run_edge(tmp_path, G, tr, sc, cfg, split)
+    assert ho[..., 5].sum() > 0 and ho[..., 14].sum() > 0  # victim hits, admissions
+    assert ho[..., 2].sum() > 0  # peer requests crossed homes
+
+
+def test_multiprocess_file_tier_full_row_width(tmp_path):
+    """File tier (N2) at 4 KiB rows across 2 homes (O_DIRECT reads into the bounce buffer,
+    k_fill<8> reads it), PVP on."""
+    N = 16384
+    g = synth.plcite(N, 8)
+    tr = synth.make_trace(g, 2, 256, (10, 5), 14)
+    sc = synth.static_scores(g)
+    cfg = dict(N=N, D=1024, L=1024, A=8, policy="hybrid", pvp=1, W=8, V=512, reinsert=1, P=1, file=1)
+    _run_edge(tmp_path, 2, tr, sc, cfg, 1)
+
+
+def test_connect_rejects_mismatched_layout(tmp_path):
+    """lsmgnn_connect on the GPU: rank 1 initialised with other arguments -> both ranks get
+    LSMGNN_ECOMM before anything is mapped; a matching retry in the same processes connects."""
+    launch(2, tmp_path, "mismatch", str(tmp_path))
+    for r in range(2):
+        d = json.load(open(tmp_path / f"r{r}.json"))
+        assert d["mismatch_error"] and "layout" in d["mismatch_error"], d
+        assert d["retry_ok"] and d["bad"] == 0, d
+

@@ -322,8 +322,9 @@ def test_determinism_launch_geometry(cfg1_g1, monkeypatch):
     compare(h1, h2, "geometry")
 
 
+@pytest.mark.parametrize("D", [128, 1024])
 @pytest.mark.parametrize("out_kind", ["pinned", "pageable"])
-def test_gather_host_end_to_end(cfg1_g1, out_kind):
+def test_gather_host_end_to_end(cfg1_g1, out_kind, D):
     """lsmgnn_gather_host (the e2e entry point: host IDs in, host rows out, copies inside the
     call): rows equal F(v) and every per-iteration counter equals the oracle's. Pinned `out`
     is written by the serve kernel over PCIe; pageable `out` goes through device staging."""
@@ -331,8 +332,9 @@ def test_gather_host_end_to_end(cfg1_g1, out_kind):
     from paper_2407_15264_b200 import LsmGnn
     from .harness import table_for
     _, tr, sc = cfg1_g1
-    N, D, W, K = 16384, 128, 8, len(tr)
+    N, W, K = 16384, 8, len(tr)
     mine = [np.asarray(tr[t][0], np.int64) for t in range(K)]
+    # D = 1024: the bench's 4 KiB rows (k_serve<8, kHost> for pinned out — the e2e path)
     c = LsmGnn(N, D, 1024, 8, 512, sc, policy="hybrid", pvp=1, window=W, max_batch_ids=max(x.size for x in mine))
     c.attach_storage(table_for(N, D, 5, pinned=True))
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -361,7 +363,7 @@ def test_gather_host_end_to_end(cfg1_g1, out_kind):
     c.close()
     assert bad == 0
     ho = run_oracle(tr, G=1, N=N, D=D, L=1024, A=8, scores=sc, policy="hybrid", pvp=1, W=W, V=512)[:, 0, :]
-    compare(hg, ho, f"gather_host {out_kind}")
+    compare(hg, ho, f"gather_host {out_kind} D{D}")
 
 
 def test_launch_count_and_profile(cfg1_g1):
@@ -398,3 +400,72 @@ def test_launch_count_and_profile(cfg1_g1):
         ms, cnt = prof[ph]
         assert cnt == steps and ms >= 0.0, (ph, prof[ph])
     assert prof["fill"][0] > 0.0
+
+# ----------------------------------------------------------------------------- full row width
+# The bench's rows are 4 KiB (1024 fp32 words): nvec = 256 selects the UNROLL = 8 kernel
+# instantiations (k_serve<8>, k_pvp<8>, k_fill<8>, k_pull<8,..>). These cases run them against
+# the oracle at that width.
+
+@pytest.mark.parametrize("policy,V", [("hybrid", 64), ("hybrid", 512), ("dynamic", 64)])
+def test_full_row_width_pvp(cfg1_g1, policy, V):
+    """configs[0] trace on one home at R = 4 KiB with the PVP on: k_serve<8> fills with victim
+    D2H into the pinned queues, serves staged rows and bypass rows; k_pvp<8> copies 4 KiB
+    victim rows back. V = 64 (C = 8 per queue) overflows the queues (admission by node order)."""
+    g, tr, sc = cfg1_g1
+    kw = dict(N=16384, D=1024, L=1024, A=8, scores=sc, policy=policy, pvp=1, W=8, V=V)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"4KiB {policy}/V{V}")
+    assert ho[:, F["victim_hits"]].sum() > 0 and ho[:, F["victim_admitted"]].sum() > 0
+    assert ho[:, F["bypassed"]].sum() > 0
+    if V == 64:
+        assert ho[:, F["victim_dropped"]].sum() > 0
+
+
+def test_full_row_width_pvp_unused():
+    """Windows that differ from the gathered batches (§8(b): "pvp_unused counts the
+    mismatches"): staged 4 KiB rows the batch does not request are counted, not served."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    from oracle import Oracle
+    from .harness import table_for
+    rng = np.random.default_rng(41)
+    N, D, L, A, W, V, K = 3000, 1024, 64, 8, 4, 4 * 32, 30
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    win = [[rng.integers(0, N, int(rng.integers(20, 120)))] for _ in range(K)]
+    # gathered batch = the window batch with a random third of its IDs replaced
+    gat = []
+    for (x,) in win:
+        y = x.copy()
+        sel = rng.random(y.size) < 0.33
+        y[sel] = rng.integers(0, N, int(sel.sum()))
+        gat.append([y])
+    o = Oracle(1, N, 4 * D, L, A, sc, policy="hybrid", pvp=1, W=W, V=V)
+    empty = [np.zeros(0, np.int64)]
+    for k in range(1, W + 1):
+        o.feed(k, win[k])
+    c = LsmGnn(N, D, L, A, V, sc, policy="hybrid", pvp=1, window=W, max_batch_ids=200)
+    c.attach_storage(table_for(N, D, pinned=True))
+    dw = [torch.from_numpy(np.asarray(x[0], np.int64)).cuda() for x in win] + \
+        [torch.zeros(0, dtype=torch.int64, device="cuda")] * (W + 1)
+    dg = [torch.from_numpy(np.asarray(x[0], np.int64)).cuda() for x in gat]
+    c.prefetch(dw[1:W + 1], first_iter=1)
+    out = torch.empty((200, 4 * D), dtype=torch.uint8, device="cuda")
+    rows, bad = [], 0
+    for t in range(K):
+        oc, _ = o.gather(t, gat[t])
+        rows.append(oc[0])
+        o.pvp_prefetch(t)
+        o.feed(t + 1 + W, win[t + 1 + W] if t + 1 + W < K else empty)
+        c.gather(dg[t], out)
+        c.prefetch([dw[t + 1 + W]], first_iter=t + 1 + W)
+        n = dg[t].numel()
+        bad += synth.check_rows(out[:n].cpu().numpy().view(np.uint32).reshape(n, D), gat[t][0], D)[0]
+    hg = c.history(0, K)
+    c.close()
+    ho = np.stack(rows)
+    assert bad == 0
+    compare(hg, ho, "pvp_unused 4KiB")
+    assert ho[:, F["pvp_unused"]].sum() > 0 and ho[:, F["victim_hits"]].sum() > 0
+
