@@ -45,7 +45,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-profile", action="store_true")
-    p.add_argument("--no-ablation", action="store_true", help="skip the PVP on/off ablation")
+    p.add_argument("--no-ablation", action="store_true", help="skip the extra measurements (PVP ablation, ...)")
+    p.add_argument("--extras", default="pvp_ablation,gpu_sampler_pipeline,storage_per_epoch,hbm_regime,file_tier",
+                   help="comma list of the extra measurements to run (G = 1)")
     p.add_argument("--no-file-tier", action="store_true", help="skip the file-tier (N2) measurement")
     p.add_argument("--file-dir", default="/tmp", help="directory for the file tier's backing file")
     p.add_argument("--lines", type=int, default=None, help="override lines per GPU")
@@ -567,11 +569,16 @@ def main():
         line["cpu_baseline"] = cpu_baseline(wl, G, trace, scores, table.numpy(), args, lines)
     c.close()
     if not args.no_ablation and G == 1:
-        line["pvp_ablation"] = optional(pvp_ablation, wl, scores, table, ids_d, lines, args, max_ids, dev)
-        line["gpu_sampler_pipeline"] = optional(gpu_sampler_pipeline, wl, g_, scores, table, lines, args, dev)
-        line["storage_per_epoch"] = optional(epoch_storage, wl, g_, scores, lines, dev)
-        line["hbm_regime"] = optional(hbm_regime, wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src)
-        if not args.no_file_tier:
+        ex = set(args.extras.split(","))
+        if "pvp_ablation" in ex:
+            line["pvp_ablation"] = optional(pvp_ablation, wl, scores, table, ids_d, lines, args, max_ids, dev)
+        if "gpu_sampler_pipeline" in ex:
+            line["gpu_sampler_pipeline"] = optional(gpu_sampler_pipeline, wl, g_, scores, table, lines, args, dev)
+        if "storage_per_epoch" in ex:
+            line["storage_per_epoch"] = optional(epoch_storage, wl, g_, scores, lines, dev)
+        if "hbm_regime" in ex:
+            line["hbm_regime"] = optional(hbm_regime, wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src)
+        if "file_tier" in ex and not args.no_file_tier:
             line["file_tier"] = optional(file_tier, wl, scores, ids_d, lines, args, max_ids, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -51,7 +51,8 @@ struct Scratch {
   uint32_t staged[2];  // rows the PVP staged, by iteration parity
   uint32_t pvp_done;   // grid-completion counter of the PVP kernel
   uint32_t pull_next;  // k_serve: next request index handed to a delivering warp
-  uint32_t pad[6];
+  uint32_t serve_done; // k_serve: CTAs finished (the last one closes the record)
+  uint32_t pad[5];
 };
 
 // Per-iteration values, resident on the device. k_begin / k_win_begin write them (from host
@@ -147,7 +148,40 @@ __device__ __forceinline__ int first_bit_in(const uint32_t* row, int lo, int hi)
 // Next reuse distance d in 1..W of a node from its window mask row, 0 = none.
 // Bit position of iteration k is k mod (W+1); at gather(t) the window is t+1..t+W
 // (PAPER.md P:352-354 window buffer; R5). p0 = (t+1) mod (W+1).
+// Rows of up to 16 words (W <= 511) are loaded in one round trip (independent loads into
+// registers) and scanned there; longer rows take the word-by-word scan below.
+__device__ __forceinline__ int next_reuse_d_seq(const uint32_t* row, int p0, int W);
 __device__ __forceinline__ int next_reuse_d(const uint32_t* row, int p0, int W) {
+  const int Wp1 = W + 1, MW = (Wp1 + 31) >> 5;
+  if (MW > 16) return next_reuse_d_seq(row, p0, W);
+  uint32_t w[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w[i] = i < MW ? row[i] : 0u;
+  // positions [p0, Wp1) come first (d = pos - p0 + 1), then the wrapped part [0, p0 - 1)
+  // (d = Wp1 - p0 + pos + 1); position p0 - 1 (iteration t) is not in the window
+  // (p0 = 0: the window is [0, W) and position W is iteration t)
+  const int hi_end = p0 == 0 ? W : Wp1;
+  int first_hi = -1, first_lo = -1;
+#pragma unroll
+  for (int i = 15; i >= 0; --i) {
+    if (i >= MW) continue;
+    const int b0 = i << 5;
+    const uint32_t x = w[i];
+    // bits at positions in [p0, hi_end)
+    uint32_t hi = x, lo = x;
+    if (p0 > b0) hi &= (p0 - b0 >= 32) ? 0u : (~0u << (p0 - b0));
+    if (hi_end - b0 < 32) hi &= hi_end - b0 <= 0 ? 0u : ((1u << (hi_end - b0)) - 1u);
+    // bits at positions < p0 - 1
+    const int lim = p0 - 1 - b0;
+    lo &= lim <= 0 ? 0u : (lim >= 32 ? ~0u : ((1u << lim) - 1u));
+    if (hi) first_hi = b0 + __ffs(hi) - 1;
+    if (lo) first_lo = b0 + __ffs(lo) - 1;
+  }
+  if (first_hi >= 0) return first_hi - p0 + 1;
+  if (first_lo >= 0) return (Wp1 - p0) + first_lo + 1;
+  return 0;
+}
+__device__ __forceinline__ int next_reuse_d_seq(const uint32_t* row, int p0, int W) {
   const int Wp1 = W + 1;
   int end1 = p0 + W < Wp1 ? p0 + W : Wp1;
   int pos = first_bit_in(row, p0, end1);
@@ -201,6 +235,96 @@ __device__ __forceinline__ void warp_copy_row(uint4* __restrict__ dst, const uin
   }
   for (; i < nvec; i += 32) st16<DST>(dst + i, ld16<SRC>(src + i));
 }
+
+// ---- TMA bulk row copies (cp.async.bulk, sm_90+; the B200 path for whole-row HBM copies)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* g, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(g), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* g, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most k committed bulk groups still have to READ their shared-memory source
+__device__ __forceinline__ void bulk_wait_read(uint32_t k) {
+  switch (k) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory"); break;
+  }
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// A warp's ring of ST row stages in shared memory, driven by its lane 0: rows are loaded with
+// cp.async.bulk (global -> shared, completion on the stage's mbarrier) and stored with
+// cp.async.bulk (shared -> global, bulk groups), up to ST - 1 loads in flight behind the store
+// being issued. The counters run across calls so that stage phases stay consistent.
+constexpr uint32_t kMaxStages = 8;
+struct RowRing {
+  uint8_t* buf;    // ST * R bytes of this warp's shared memory
+  uint64_t* bar;   // ST mbarriers
+  uint32_t* pend;  // ST entries: the row index (into dst[]) whose load occupies the stage
+  uint32_t ST, R;
+  uint32_t nl, ns, phase;  // loads issued, stores issued (lane 0), phase bit per stage
+};
+__device__ __forceinline__ void ring_init(RowRing& r) {  // lane 0; then __syncwarp
+  for (uint32_t s = 0; s < r.ST; ++s) mbar_init(&r.bar[s], 1);
+  mbar_fence_init();
+  r.nl = r.ns = r.phase = 0;
+}
+// Lane 0: copy rows j in `mask` (bit j) from src[j] to dst[j] (R bytes each, 16-B aligned),
+// returning when every store has been issued (its completion is awaited by ring_drain or the
+// next stage reuse).
+__device__ __forceinline__ void ring_copy(RowRing& r, const void* const* src, void* const* dst, uint32_t mask) {
+  const uint32_t total = __popc(mask);
+  uint32_t issued = 0, stored = 0;
+  while (stored < total) {
+    while (issued < total && r.nl - r.ns < r.ST) {
+      const uint32_t j = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t s = r.nl % r.ST;
+      // the stage's last store (number nl - ST) must have read it; later stores may still read
+      if (r.nl >= r.ST) bulk_wait_read(r.ns + r.ST - 1 - r.nl);
+      mbar_expect_tx(&r.bar[s], r.R);
+      bulk_g2s(r.buf + (size_t)s * r.R, src[j], r.R, &r.bar[s]);
+      r.pend[s] = j;
+      ++r.nl;
+      ++issued;
+    }
+    const uint32_t s = r.ns % r.ST;
+    mbar_wait_parity(&r.bar[s], (r.phase >> s) & 1u);
+    r.phase ^= 1u << s;
+    bulk_s2g(dst[r.pend[s]], r.buf + (size_t)s * r.R, r.R);
+    bulk_commit();
+    ++r.ns;
+    ++stored;
+  }
+}
+__device__ __forceinline__ void ring_drain() { bulk_wait_all(); }  // lane 0, before the kernel ends
 
 template <typename T>
 __device__ __forceinline__ void warp_bitonic_sort(T* a, int P) {

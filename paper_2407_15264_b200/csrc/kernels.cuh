@@ -75,35 +75,21 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
   }
 }
 
-// Close the record: algorithmic bytes per tier, cumulative sums; the staging count of
-// the next parity is reset so that a missing PVP call stages nothing. The ERANGE counter is
-// mirrored to pinned host memory; it->t_next = t + 1 (the next graph replay's iteration).
-__global__ void k_end(IterState* it, unsigned long long* hist, unsigned long long* cum, Scratch* scr, uint32_t R,
-                      volatile uint32_t* bad_mirror) {
+// Close the record (G > 1, after the pulls; at G = 1 the last CTA of k_serve does it):
+// end_record below, one warp.
+struct EndArgs {
+  IterState* it;
+  unsigned long long* hist;
+  unsigned long long* cum;
+  Scratch* scr;
+  uint32_t R;
+  volatile uint32_t* bad_mirror;
+};
+__device__ __forceinline__ void end_record(IterState* it, unsigned long long* hist, unsigned long long* cum,
+                                           Scratch* scr, uint32_t R, volatile uint32_t* bad_mirror);
+__global__ void k_end(EndArgs a) {
   pdl_prologue();
-  __shared__ unsigned long long s_rec[F_NFIELDS];
-  const int f = threadIdx.x;  // one field per thread (blockDim = 32 >= F_NFIELDS)
-  const uint64_t t = it->t;
-  unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
-  if (f == 0) {
-    rec[F_UNIQUE] = scr->nuniq;
-    rec[F_REQ] = scr->nreq;
-    rec[F_BOUT] = (unsigned long long)scr->nreq * R;
-    rec[F_BNVL] = rec[F_PEER] * R;
-    rec[F_BH2D] = rec[F_STOR] * R;
-    rec[F_BPVP] = rec[F_PREF] * R;
-    rec[F_BD2H] = rec[F_VADM] * R;
-  }
-  __syncthreads();
-  if (f < F_NFIELDS) s_rec[f] = rec[f];
-  __syncthreads();
-  if (f > 0 && f < F_NFIELDS) cum[f] += s_rec[f];
-  if (f == 0) {
-    cum[F_ITER] = t;
-    scr->staged[(t + 1) & 1] = 0;
-    *bad_mirror = scr->bad_ids;
-    it->t_next = t + 1;  // direct calls and graph replays may be mixed
-  }
+  end_record(a.it, a.hist, a.cum, a.scr, a.R, a.bad_mirror);
 }
 
 // Start the window feed of one batch (iteration wk): k_host >= 0 from the host, else (graph
@@ -132,34 +118,44 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
 }
 
 // ------------------------------------------------------------------------------ S10 (G = 1)
-// Window feed at one home: validate the caller's int64 IDs (it->wids/wn), write them (u32)
-// into ring slot it->wslot, and set each node's reuse bit of the slot. (The gather side of
-// S1 at G = 1 is fused into k_dedup.)
-__global__ void k_route_local(const IterState* it, uint64_t N, uint32_t* __restrict__ ring, uint64_t stride,
-                              uint32_t* __restrict__ ring_len, Scratch* scr, uint32_t* __restrict__ mask,
-                              uint32_t MW) {
+// Window feed at one home, one launch: store the batch of iteration k (u32, position i of the
+// caller's list at slot entry i; an invalid ID counts toward ERANGE and is stored as kInvalid)
+// into ring slot k mod (W+1) and set each node's reuse bit of the slot. The slot's previous
+// bits (iteration k - W - 1) were cleared by k_dedup of gather(k - W - 1), which this launch
+// follows. k_host >= 0: iteration, IDs and count are kernel arguments (direct calls; block 0
+// also advances it->wk_next so that graph replays can follow); k_host < 0 (graph replay):
+// k_win_begin published them in IterState. (The gather side of S1 at G = 1 is fused into
+// k_dedup.)
+__global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host, uint32_t Wp1,
+                              uint64_t N, uint32_t* __restrict__ ring, uint64_t stride, uint32_t* __restrict__ ring_len,
+                              Scratch* scr, uint32_t* __restrict__ mask, uint32_t MW) {
   pdl_prologue();
-  const int64_t* __restrict__ ids = it->wids;
-  const int64_t n = it->wn;
-  const uint32_t slot = it->wslot;
+  const int64_t* __restrict__ ids;
+  int64_t n;
+  uint32_t slot;
+  if (k_host >= 0) {
+    ids = ids_host;
+    n = n_host;
+    slot = (uint32_t)((uint64_t)k_host % Wp1);
+  } else {
+    ids = it->wids;
+    n = it->wn;
+    slot = it->wslot;
+  }
   uint32_t* __restrict__ list = ring + (size_t)slot * stride;
-  uint32_t* cnt = ring_len + slot;
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += gstride) {
-    const int64_t i = base + threadIdx.x;
-    bool ok = false;
-    uint32_t v = 0;
-    if (i < n) {
-      const int64_t x = ids[i];
-      ok = x >= 0 && (uint64_t)x < N;
-      v = (uint32_t)x;
-      if (!ok) atomicAdd(&scr->bad_ids, 1u);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = ids[i];
+    if (x >= 0 && (uint64_t)x < N) {
+      list[i] = (uint32_t)x;
+      atomicOr(&mask[(size_t)x * MW + (slot >> 5)], 1u << (slot & 31));  // G = 1: q = v
+    } else {
+      list[i] = kInvalid;
+      atomicAdd(&scr->bad_ids, 1u);
     }
-    const uint32_t pos = block_reserve(cnt, ok);
-    if (ok) {
-      list[pos] = v;
-      atomicOr(&mask[(size_t)v * MW + (slot >> 5)], 1u << (slot & 31));  // G = 1: q = v
-    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ring_len[slot] = (uint32_t)n;
+    if (k_host >= 0) it->wk_next = (uint64_t)k_host + 1;
   }
 }
 
@@ -214,80 +210,100 @@ __global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
 }
 
 // ------------------------------------------------------------------------------ S3
-// Home: one representative per distinct node (stamp table indexed by q = v / G),
-// appended to uniq[]; per-set counts for the bucket pass. Requests and peer requests
-// are counted here (every count but `requests` is over unique nodes, R11).
+// Home: one representative per distinct node (stamp table indexed by q = v / G), written
+// straight into its cache set's bucket: bucket[s * BC + set_cnt[s]++] (BC = the most distinct
+// nodes one set can receive in a batch, ceil(Q / S) capped by the batch capacity), so no scan
+// or scatter pass is needed; k_set sorts each bucket before any order-dependent step and
+// resets set_cnt. Requests and peer requests are counted here (every count but `requests` is
+// over unique nodes, R11).
 // G = 1 (direct): the caller's int64 IDs are read straight from it->ids and validated here
 // (S1 fused away; an ID >= N counts toward ERANGE and is skipped), and every request
 // position i is threaded onto its node's list for the fused delivery of k_serve:
 // head[q] = stamp<<32 | last position, nxt[i] = previous (kInvalid = end).
 // G > 1: the IDs come from the inbox segments of the nsrc requesters.
-__device__ __forceinline__ void dedup_one(uint32_t v, uint32_t pos, uint32_t G, uint32_t S, uint32_t stamp,
+// S10 (window): the same launch drops the reuse bits of iteration t (ring slot t mod (W+1)):
+// gather(t) reads iterations t+1..t+W only, and gather(t-1), the last reader of those bits,
+// has completed; the feed of t+1+W (which rewrites the slot) is ordered after this kernel.
+__device__ __forceinline__ bool dedup_one(uint32_t v, uint32_t pos, uint32_t G, uint32_t S, uint32_t BC, uint32_t stamp,
                                           uint32_t* __restrict__ mark, uint32_t* __restrict__ set_cnt,
-                                          unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt,
-                                          bool* first) {
+                                          uint32_t* __restrict__ bucket, unsigned long long* __restrict__ head,
+                                          uint32_t* __restrict__ nxt) {
   const uint32_t q = v / G;
-  *first = atomicExch(&mark[q], stamp) != stamp;
-  if (*first) atomicAdd(&set_cnt[q % S], 1u);
+  const bool first = atomicExch(&mark[q], stamp) != stamp;
+  if (first) {
+    const uint32_t s = q % S;
+    bucket[(size_t)s * BC + atomicAdd(&set_cnt[s], 1u)] = v;
+  }
   if (head) {
     const unsigned long long old = atomicExch(&head[q], ((unsigned long long)stamp << 32) | pos);
     nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
   }
+  return first;
 }
-__global__ void k_dedup(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
-                        uint32_t nsrc, uint32_t cap, uint32_t me, uint32_t G, uint32_t S,
-                        const IterState* it, uint32_t* __restrict__ mark, uint32_t* __restrict__ uniq,
-                        uint32_t* __restrict__ set_cnt, Scratch* scr, unsigned long long* hist,
-                        unsigned long long* __restrict__ head, uint32_t* __restrict__ nxt, uint32_t direct,
-                        uint64_t N) {
+struct DedupArgs {
+  const uint32_t* inbox;
+  const uint32_t* inbox_cnt;
+  uint32_t nsrc, cap, me, G, S, BC;
+  uint32_t* mark;
+  uint32_t* bucket;
+  uint32_t* set_cnt;
+  unsigned long long* head;  // G = 1: request lists of the fused delivery
+  uint32_t* nxt;
+  uint32_t direct;
+  uint64_t N;
+  // window slot of iteration t: its list and the reuse mask (bit t mod (W+1) is cleared)
+  const uint32_t* ring;
+  uint64_t ring_stride;
+  const uint32_t* ring_len;
+  uint32_t* mask;
+  uint32_t MW, Wp1;
+};
+__global__ void k_dedup(DedupArgs a, const IterState* it, Scratch* scr, unsigned long long* hist) {
   pdl_prologue();
   const uint32_t stamp = it->stamp;
   unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
-  uint32_t nreq = 0, npeer = 0;
   const uint32_t stride = gridDim.x * blockDim.x;
-  if (direct) {
+  {  // S10: clear the bits of iteration t (its window list is in ring slot t mod (W+1))
+    const uint32_t slot = (uint32_t)(it->t % a.Wp1);
+    const uint32_t* __restrict__ list = a.ring + (size_t)slot * a.ring_stride;
+    const uint32_t nl = a.ring_len[slot];
+    const uint32_t m = ~(1u << (slot & 31));
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
+      const uint32_t v = list[i];
+      if (v != kInvalid) atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
+    }
+  }
+  uint32_t nreq = 0, npeer = 0, nfirst = 0;
+  if (a.direct) {
     const int64_t* __restrict__ ids = it->ids;
     const int64_t n = it->n;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
-      const int64_t i = base + threadIdx.x;
-      bool first = false;
-      uint32_t v = 0;
-      if (i < n) {
-        const int64_t x = ids[i];
-        if (x >= 0 && (uint64_t)x < N) {
-          v = (uint32_t)x;
-          dedup_one(v, (uint32_t)i, G, S, stamp, mark, set_cnt, head, nxt, &first);
-          ++nreq;
-        } else {
-          atomicAdd(&scr->bad_ids, 1u);
-        }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const int64_t x = ids[i];
+      if (x >= 0 && (uint64_t)x < a.N) {
+        nfirst += dedup_one((uint32_t)x, (uint32_t)i, a.G, a.S, a.BC, stamp, a.mark, a.set_cnt, a.bucket, a.head,
+                            a.nxt);
+        ++nreq;
+      } else {
+        atomicAdd(&scr->bad_ids, 1u);
       }
-      const uint32_t pos = block_reserve(&scr->nuniq, first);
-      if (first) uniq[pos] = v;
     }
   } else {
-    for (uint32_t r = 0; r < nsrc; ++r) {
-      const uint32_t n = inbox_cnt[r];
-      const uint32_t* in = inbox + (size_t)r * cap;
-      for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
-        const uint32_t i = base + threadIdx.x;
-        bool first = false;
-        uint32_t v = 0;
-        if (i < n) {
-          v = in[i];
-          dedup_one(v, i, G, S, stamp, mark, set_cnt, head, nxt, &first);
-          ++nreq;
-          if (r != me) ++npeer;
-        }
-        const uint32_t pos = block_reserve(&scr->nuniq, first);
-        if (first) uniq[pos] = v;
+    for (uint32_t r = 0; r < a.nsrc; ++r) {
+      const uint32_t n = a.inbox_cnt[r];
+      const uint32_t* in = a.inbox + (size_t)r * a.cap;
+      for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        nfirst += dedup_one(in[i], i, a.G, a.S, a.BC, stamp, a.mark, a.set_cnt, a.bucket, a.head, a.nxt);
+        ++nreq;
+        if (r != a.me) ++npeer;
       }
     }
   }
   nreq = __reduce_add_sync(0xffffffffu, nreq);
   npeer = __reduce_add_sync(0xffffffffu, npeer);
+  nfirst = __reduce_add_sync(0xffffffffu, nfirst);
   if (lane_id() == 0) {
     if (nreq) atomicAdd(&scr->nreq, nreq);
+    if (nfirst) atomicAdd(&scr->nuniq, nfirst);
     if (npeer) atomicAdd(&rec[F_PEER], (unsigned long long)npeer);
   }
 }
@@ -322,84 +338,55 @@ __device__ __forceinline__ uint32_t pow2_at_least_32(uint32_t m) {
   return p;
 }
 
-// Exclusive scan of cnt[0..n) into off[0..n], one CTA (1024 threads) per tile of 4096 counts.
-// Each CTA scans its tile in shared memory (coalesced loads and stores; each thread owns 4
-// contiguous counts, skewed against bank conflicts), publishes the tile total, and takes
-// its carry from the totals of the tiles before it (look-back on per-tile flags stamped
-// with `seq`, unique per launch site and iteration). With poff, also the offsets of the
-// global scratch of the sets too large for k_set's shared memory (bucket > big_P): each
-// gets a power-of-two region. The CTAs also count staged PVP rows that this batch did not
-// request (pvp_unused).
+// Exclusive scan of cnt[0..n) into off[0..n], one CTA (1024 threads) per tile of 4096 counts
+// (the per-queue victim-candidate counts of the admission step). Each CTA scans its tile in
+// shared memory (coalesced loads and stores; each thread owns 4 contiguous counts, skewed
+// against bank conflicts), publishes the tile total, and takes its carry from the totals of the
+// tiles before it (look-back on per-tile flags stamped with `seq`, unique per iteration).
 constexpr uint32_t kScanTile = 4096;
 struct ScanSync {
-  uint32_t* flag;  // [tiles] seq once agg/pagg of the tile are published
+  uint32_t* flag;  // [tiles] seq once agg of the tile is published
   uint32_t* agg;   // [tiles] tile totals
-  uint32_t* pagg;  // [tiles] tile totals of the oversized-set regions
 };
 __device__ __forceinline__ uint32_t scan_skew(uint32_t j) { return j + (j >> 5); }
 __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt, uint32_t* __restrict__ off,
-                                               uint32_t n, const uint32_t* __restrict__ stg_base, uint32_t C,
-                                               const Scratch* scr, const uint32_t* __restrict__ mark,
-                                               const IterState* it, uint32_t G, unsigned long long* hist,
-                                               uint32_t* __restrict__ poff, uint32_t big_P, ScanSync sy,
-                                               uint32_t seq_add) {
+                                               uint32_t n, const IterState* it, ScanSync sy) {
   pdl_prologue();
   __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_carry[2];
+  __shared__ uint32_t s_carry;
   __shared__ uint32_t s_c[kScanTile + kScanTile / 32];
-  __shared__ uint32_t s_p[kScanTile + kScanTile / 32];
   const uint32_t tid = threadIdx.x, b = blockIdx.x;
   const uint32_t base = b * kScanTile;
-  const uint32_t seq = 2u * it->stamp + seq_add;
+  const uint32_t seq = it->stamp;
   for (uint32_t j = tid; j < kScanTile; j += 1024) s_c[scan_skew(j)] = base + j < n ? cnt[base + j] : 0u;
   __syncthreads();
-  uint32_t v[4], sum = 0, psum = 0;
+  uint32_t v[4], sum = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     v[k] = s_c[scan_skew(tid * 4 + k)];
     sum += v[k];
-    if (v[k] > big_P) psum += pow2_at_least_32(v[k]);
   }
   uint32_t run = block_exclusive_1024(sum, s_warp);
   const uint32_t total = s_warp[31];
-  uint32_t prun = 0, ptotal = 0;
-  if (poff) {
-    prun = block_exclusive_1024(psum, s_warp);
-    ptotal = s_warp[31];
-  }
   if (gridDim.x > 1) {
-    if (tid == 0) {  // publish this tile's totals
+    if (tid == 0) {  // publish this tile's total
       sy.agg[b] = total;
-      sy.pagg[b] = ptotal;
       __threadfence();
       *(volatile uint32_t*)&sy.flag[b] = seq;
     }
     if (tid < 32) {  // carry = totals of the tiles before this one
-      uint32_t c = 0, pc = 0;
+      uint32_t c = 0;
       for (uint32_t j = tid; j < b; j += 32) {
         while (*(volatile const uint32_t*)&sy.flag[j] != seq) {
         }
         __threadfence();
         c += *(volatile const uint32_t*)&sy.agg[j];
-        pc += *(volatile const uint32_t*)&sy.pagg[j];
       }
       c = __reduce_add_sync(0xffffffffu, c);
-      pc = __reduce_add_sync(0xffffffffu, pc);
-      if (tid == 0) {
-        s_carry[0] = c;
-        s_carry[1] = pc;
-      }
+      if (tid == 0) s_carry = c;
     }
     __syncthreads();
-    run += s_carry[0];
-    prun += s_carry[1];
-  }
-  if (poff) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      s_p[scan_skew(tid * 4 + k)] = prun;
-      if (v[k] > big_P) prun += pow2_at_least_32(v[k]);
-    }
+    run += s_carry;
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -407,36 +394,8 @@ __global__ void __launch_bounds__(1024) k_scan(const uint32_t* __restrict__ cnt,
     run += v[k];
   }
   __syncthreads();
-  for (uint32_t j = tid; j < kScanTile && base + j < n; j += 1024) {
-    off[base + j] = s_c[scan_skew(j)];
-    if (poff) poff[base + j] = s_p[scan_skew(j)];
-  }
+  for (uint32_t j = tid; j < kScanTile && base + j < n; j += 1024) off[base + j] = s_c[scan_skew(j)];
   if (b == gridDim.x - 1 && tid == 1023) off[n] = run;  // the grand total
-  // pvp_unused: staged rows whose node this batch did not request
-  if (stg_base) {
-    const uint32_t par = it->par, stamp = it->stamp;
-    const uint32_t* stg_nodes = stg_base + (size_t)par * C;
-    const uint32_t ns = scr->staged[par];
-    uint32_t unused = 0;
-    for (uint32_t j = b * 1024 + tid; j < ns; j += gridDim.x * 1024) unused += mark[stg_nodes[j] / G] != stamp;
-    unused = __reduce_add_sync(0xffffffffu, unused);
-    if ((tid & 31) == 0 && unused)
-      atomicAdd(&hist[(size_t)it->rec_idx * F_NFIELDS + F_UNUSED], (unsigned long long)unused);
-  }
-}
-
-// Scatter unique nodes into their set's bucket. set_cnt is decremented back to zero.
-__global__ void k_bucket(const uint32_t* __restrict__ uniq, const Scratch* scr, uint32_t G, uint32_t S,
-                         const uint32_t* __restrict__ off, uint32_t* __restrict__ set_cnt,
-                         uint32_t* __restrict__ bucket) {
-  pdl_prologue();
-  const uint32_t n = scr->nuniq;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t v = uniq[i];
-    const uint32_t s = (v / G) % S;
-    const uint32_t pos = off[s] + atomicSub(&set_cnt[s], 1u) - 1u;
-    bucket[pos] = v;
-  }
 }
 
 // ------------------------------------------------------------------------------ S4 (period > 1)
@@ -461,8 +420,9 @@ __global__ void k_snapshot(const uint32_t* __restrict__ tags, uint32_t L, uint32
 
 // ------------------------------------------------------------------------------ S4 + S5
 struct SetParams {
-  const uint32_t* set_off;
-  const uint32_t* bucket;
+  uint32_t* set_cnt;     // distinct nodes per set this batch (k_dedup); k_set resets it to 0
+  const uint32_t* bucket;  // set s's nodes at bucket[s * BC, + set_cnt[s])
+  uint32_t BC, BCp;      // bucket capacity per set; global-scratch region per oversized set (pow2 >= BC)
   uint32_t* tags;
   uint32_t* last_use;
   uint32_t* rr;
@@ -480,7 +440,6 @@ struct SetParams {
   uint32_t S, A, G, W, T, MW;
   uint32_t policy, pvp, reinsert;
   uint32_t P;            // per-warp shared capacity (power of two); larger buckets use g_* scratch
-  const uint32_t* poff;  // global scratch offset of each oversized set (k_scan)
   uint32_t *g_sv, *g_sk, *g_sidx;
   unsigned long long* g_skey;
   uint32_t period;       // dynamic-information update period; 1 = exact every batch
@@ -488,6 +447,10 @@ struct SetParams {
   uint32_t warp_bytes;   // per-warp shared memory
   uint32_t bypass_base;  // pool row of the bypass staging area
   uint32_t deliver;      // kDelivered: node_loc marks rows filled this batch (k_serve / k_pull phases)
+  // pvp_unused: PVP-staged rows (stg_nodes, by parity) whose node this batch did not request
+  const uint32_t* stg_nodes;
+  const uint32_t* mark;
+  uint32_t C;
 };
 
 enum { C_HIT, C_VHIT, C_STOR, C_INS, C_BYP, C_EVICT, C_EV0, C_EV1, C_EV2, C_EV3, C_ENR, C_N };
@@ -560,36 +523,35 @@ __global__ void k_set(SetParams p) {
   for (int c = 0; c < C_N; ++c) ctr[c] = 0;
   const uint32_t A = p.A, G = p.G;
 
+  if (p.stg_nodes) {  // pvp_unused (§8(b)): staged rows whose node this batch did not request
+    const uint32_t par = p.it->par;
+    const uint32_t* stg = p.stg_nodes + (size_t)par * p.C;
+    const uint32_t ns = p.scr->staged[par];
+    uint32_t unused = 0;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += gridDim.x * blockDim.x)
+      unused += p.mark[stg[j] / G] != stamp_;
+    unused = __reduce_add_sync(0xffffffffu, unused);
+    if (lane == 0 && unused) atomicAdd(&rec_[F_UNUSED], (unsigned long long)unused);
+  }
+
   for (uint32_t s = blockIdx.x * nwb + wib; s < p.S; s += gridDim.x * nwb) {
-    const uint32_t off = p.set_off[s];
-    const uint32_t m = p.set_off[s + 1] - off;
-    if (m == 0) continue;
-    uint32_t Pm = 32;
-    while (Pm < m) Pm <<= 1;
-    // a bucket larger than the warp's shared-memory capacity works in its own power-of-two
-    // region of global scratch (rare: only when one set receives > P distinct nodes)
-    uint32_t* sv = sv_s;
-    uint32_t* sk = sk_s;
-    uint32_t* sidx = sidx_s;
-    unsigned long long* skey = skey_s;
-    if (m > p.P) {
-      const uint32_t po = p.poff[s];
-      sv = p.g_sv + po;
-      sk = p.g_sk + po;
-      sidx = p.g_sidx + po;
-      skey = p.g_skey + po;
-    }
-    for (uint32_t j = lane; j < Pm; j += 32) sv[j] = j < m ? p.bucket[off + j] : kInvalid;
-    // resident lines of the set: lane w holds way w
+    // one round trip for the set: its node count, its first 32 bucket entries (the bucket array
+    // is padded by 32 entries) and its resident lines (lane w holds way w)
+    const uint32_t* bk = p.bucket + (size_t)s * p.BC;
+    uint32_t m = lane == 0 ? p.set_cnt[s] : 0u;
+    const uint32_t b0 = bk[lane];
     uint32_t tg = kInvalid, lu = 0;
     if (lane < A) {
       tg = p.tags[s * A + lane];
       lu = p.last_use[s * A + lane];
     }
+    m = __shfl_sync(0xffffffffu, m, 0);
+    if (m == 0) continue;
+    if (lane == 0) p.set_cnt[s] = 0;  // ready for the next batch
     stag[lane] = tg;
     __syncwarp();
     if (m <= 32) {  // fast path: every node of the bucket is resident (no miss, no replacement)
-      const uint32_t v = lane < m ? sv[lane] : kInvalid;
+      const uint32_t v = lane < m ? b0 : kInvalid;
       int way = -1;
       if (lane < m)
         for (uint32_t w = 0; w < A; ++w)
@@ -607,6 +569,24 @@ __global__ void k_set(SetParams p) {
         continue;
       }
     }
+    uint32_t Pm = 32;
+    while (Pm < m) Pm <<= 1;
+    // a bucket larger than the warp's shared-memory capacity works in its own power-of-two
+    // region of global scratch (rare: only when one set receives > P distinct nodes)
+    uint32_t* sv = sv_s;
+    uint32_t* sk = sk_s;
+    uint32_t* sidx = sidx_s;
+    unsigned long long* skey = skey_s;
+    if (m > p.P) {
+      const size_t po = (size_t)s * p.BCp;
+      sv = p.g_sv + po;
+      sk = p.g_sk + po;
+      sidx = p.g_sidx + po;
+      skey = p.g_skey + po;
+    }
+    sv[lane] = lane < m ? b0 : kInvalid;
+    for (uint32_t j = 32 + lane; j < Pm; j += 32) sv[j] = j < m ? bk[j] : kInvalid;
+    __syncwarp();
     warp_bitonic_sort(sv, (int)Pm);  // nodes ascending (R10: misses installed in node order)
 
     // ---- probe (S4): tag compare, then the PVP staging directory
@@ -1010,35 +990,105 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
 // the storage read and the delivery overlap, and the row is never re-read from HBM. The
 // remaining warps (1 in 8) start copying the rows not delivered by a fill (hits, staged rows
 // served in place) from HBM into `out`, concurrently with the PCIe-bound fills; fill warps
-// join them once the fills are handed out. Delivery work is taken in chunks of requests from
-// a shared counter, so a hit-dominated batch gets the whole grid and a miss-dominated one
+// join them once the fills are handed out. Delivery work is taken in chunks of 32 requests
+// from a shared counter, so a hit-dominated batch gets the whole grid and a miss-dominated one
 // keeps 7/8 of it on the fills.
-template <int UNROLL, int OUT>
-__global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* __restrict__ pool,
-                        const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
-                        const unsigned long long* __restrict__ head, const uint32_t* __restrict__ nxt,
-                        const IterState* it, uint64_t N,
-                        const uint32_t* __restrict__ node_loc, uint4* __restrict__ out, uint32_t bounce) {
+// TMA = 1 (device `out`): delivery rows move HBM -> shared -> HBM with TMA bulk copies through
+// each warp's ring of `ST` row stages (lane 0 drives it; RowRing), so the bytes in flight are set
+// by shared memory, not registers. TMA = 0: 16-byte vector loads/stores (pinned host `out`).
+// The last CTA to finish closes the iteration's record (S9, end_record).
+struct ServeArgs {
+  const FillEnt* fills;
+  Scratch* scr;
+  uint4* pool;
+  const uint4* table;
+  uint4* hostq;
+  uint32_t nvec;
+  const unsigned long long* head;
+  const uint32_t* nxt;
+  IterState* it;
+  uint64_t N;
+  const uint32_t* node_loc;
+  uint4* out;
+  uint32_t bounce;
+  uint32_t ST;  // TMA ring stages per warp
+  // S9, closed by the last CTA
+  unsigned long long* hist;
+  unsigned long long* cum;
+  volatile uint32_t* bad_mirror;
+};
+
+// S9: close iteration t's record — algorithmic bytes per tier, cumulative sums; the staging
+// count of the next parity is reset so that a missing PVP call stages nothing; the ERANGE
+// counter is mirrored to pinned host memory; it->t_next = t + 1. One warp (lane = field).
+__device__ __forceinline__ void end_record(IterState* it, unsigned long long* hist, unsigned long long* cum,
+                                           Scratch* scr, uint32_t R, volatile uint32_t* bad_mirror) {
+  const uint32_t f = lane_id();
+  const uint64_t t = it->t;
+  unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
+  if (f == 0) {
+    rec[F_UNIQUE] = scr->nuniq;
+    rec[F_REQ] = scr->nreq;
+    rec[F_BOUT] = (unsigned long long)scr->nreq * R;
+    rec[F_BNVL] = rec[F_PEER] * R;
+    rec[F_BH2D] = rec[F_STOR] * R;
+    rec[F_BPVP] = rec[F_PREF] * R;
+    rec[F_BD2H] = rec[F_VADM] * R;
+  }
+  __syncwarp();
+  __threadfence_block();
+  unsigned long long v = 0;
+  if (f < F_NFIELDS) v = rec[f];
+  __syncwarp();
+  if (f > 0 && f < F_NFIELDS) cum[f] += v;
+  if (f == 0) {
+    cum[F_ITER] = t;
+    scr->staged[(t + 1) & 1] = 0;
+    *bad_mirror = scr->bad_ids;
+    it->t_next = t + 1;  // direct calls and graph replays may be mixed
+  }
+}
+
+template <int UNROLL, int OUT, int TMA>
+__global__ void k_serve(ServeArgs a) {
   pdl_prologue();
-  constexpr uint32_t kChunk = 16;
-  const uint32_t stamp = it->stamp;
-  const int64_t* __restrict__ ids = it->ids;
-  const int64_t n = it->n;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar[8][kMaxStages];
+  __shared__ uint32_t s_pend[8][kMaxStages];
+  __shared__ const void* s_src[8][32];
+  __shared__ void* s_dst[8][32];
+  __shared__ uint32_t s_last;
+  constexpr uint32_t kChunk = 32;
+  const uint32_t stamp = a.it->stamp;
+  const int64_t* __restrict__ ids = a.it->ids;
+  const int64_t n = a.it->n;
+  const uint32_t nvec = a.nvec;
+  const uint32_t wib = threadIdx.x >> 5;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t npull = nw >= 8 ? nw / 8 : 1;
   const int lane = (int)lane_id();
+  RowRing ring{};
+  if (TMA) {
+    ring.buf = smem + (size_t)wib * a.ST * nvec * 16;
+    ring.bar = s_bar[wib];
+    ring.pend = s_pend[wib];
+    ring.ST = a.ST;
+    ring.R = nvec * 16;
+    if (lane == 0) ring_init(ring);
+    __syncwarp();
+  }
   if (gw >= npull) {  // ---- fill warps
-    const uint32_t nf = scr->nfill;
+    const uint32_t nf = a.scr->nfill;
     for (uint32_t e = gw - npull; e < nf; e += nw - npull) {
-      const FillEnt f = fills[e];
-      uint4* slot = pool + (size_t)f.dst * nvec;
-      if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, slot, nvec);
+      const FillEnt f = a.fills[e];
+      uint4* slot = a.pool + (size_t)f.dst * nvec;
+      if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(a.hostq + (size_t)f.victim * nvec, slot, nvec);
       const bool from_host = (f.src & kHostBit) != 0;
       // host row: the backing table's row q, or (file tier) bounce-buffer row e
-      const uint4* src = from_host ? table + (size_t)(bounce ? e : (f.src & ~kHostBit)) * nvec
-                                   : pool + (size_t)f.src * nvec;
-      const unsigned long long h = head[f.node];
+      const uint4* src = from_host ? a.table + (size_t)(a.bounce ? e : (f.src & ~kHostBit)) * nvec
+                                   : a.pool + (size_t)f.src * nvec;
+      const unsigned long long h = a.head[f.node];
       const uint32_t first = (uint32_t)(h >> 32) == stamp ? (uint32_t)h : kInvalid;
       for (uint32_t base = 0; base < nvec; base += 32 * UNROLL) {
         uint4 v[UNROLL];
@@ -1052,8 +1102,8 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
           const uint32_t k = base + lane + 32 * u;
           if (k < nvec) st16<kDev>(slot + k, v[u]);
         }
-        for (uint32_t pos = first; pos != kInvalid; pos = nxt[pos]) {
-          uint4* dst = out + (size_t)pos * nvec;  // list positions are request indices
+        for (uint32_t pos = first; pos != kInvalid; pos = a.nxt[pos]) {
+          uint4* dst = a.out + (size_t)pos * nvec;  // list positions are request indices
 #pragma unroll
           for (int u = 0; u < UNROLL; ++u) {
             const uint32_t k = base + lane + 32 * u;
@@ -1065,54 +1115,61 @@ __global__ void k_serve(const FillEnt* __restrict__ fills, Scratch* scr, uint4* 
   }
   // ---- delivery of the rows no fill delivers, in chunks from the shared counter. The
   // chunk's IDs and locations are looked up by its lanes at once (one dependent round trip
-  // per chunk instead of two per row), then its rows are copied one after the other.
+  // per chunk instead of two per row), then its rows are copied.
   for (;;) {
     uint32_t c0 = 0;
-    if (lane == 0) c0 = atomicAdd(&scr->pull_next, kChunk);
+    if (lane == 0) c0 = atomicAdd(&a.scr->pull_next, kChunk);
     c0 = __shfl_sync(0xffffffffu, c0, 0);
     if ((int64_t)c0 >= n) break;
     const uint32_t m = (uint32_t)min((int64_t)kChunk, n - (int64_t)c0);
-    uint32_t loc_l = kDelivered;  // lanes >= m: nothing to copy
+    uint32_t loc = kDelivered;  // lanes >= m: nothing to copy
     if ((uint32_t)lane < m) {
       const int64_t x = ids[c0 + lane];
-      loc_l = (x < 0 || (uint64_t)x >= N) ? kInvalid : node_loc[(uint32_t)x];
+      loc = (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
     }
-    for (uint32_t j = 0; j < m; ++j) {
-      const uint32_t loc = __shfl_sync(0xffffffffu, loc_l, (int)j);
-      uint4* dst = out + (size_t)(c0 + j) * nvec;
-      if (loc == kInvalid) {  // ERANGE: zero-filled row
-        for (uint32_t k = lane; k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
-        continue;
+    uint32_t zero = __ballot_sync(0xffffffffu, loc == kInvalid);
+    while (zero) {  // ERANGE: zero-filled rows (rare)
+      const uint32_t j = __ffs(zero) - 1;
+      zero &= zero - 1;
+      uint4* dst = a.out + (size_t)(c0 + j) * nvec;
+      for (uint32_t k = lane; k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
+    }
+    const uint32_t need = __ballot_sync(0xffffffffu, loc != kInvalid && !(loc & kDelivered));
+    if (TMA) {
+      s_src[wib][lane] = a.pool + (size_t)(loc & ~kDelivered) * nvec;
+      s_dst[wib][lane] = a.out + (size_t)(c0 + lane) * nvec;
+      __syncwarp();
+      if (lane == 0 && need) ring_copy(ring, s_src[wib], s_dst[wib], need);
+      __syncwarp();
+    } else {
+      uint32_t mk = need;
+      while (mk) {
+        const uint32_t j = __ffs(mk) - 1;
+        mk &= mk - 1;
+        const uint32_t lj = __shfl_sync(0xffffffffu, loc, (int)j);
+        warp_copy_row<UNROLL, kDev, OUT>(a.out + (size_t)(c0 + j) * nvec, a.pool + (size_t)lj * nvec, nvec);
       }
-      if (loc & kDelivered) continue;
-      warp_copy_row<UNROLL, kDev, OUT>(dst, pool + (size_t)loc * nvec, nvec);
     }
   }
-}
-
-// ------------------------------------------------------------------------------ S10
-// Window feed. Bit (k mod (W+1)) of mask[q] is set when node q*G+me is in B_k. The ring slot
-// and bit of the batch being fed is it->wslot. k_mask_clear drops the bits of the iteration
-// that last used the slot (its stored list) and then — last CTA out — empties the slot;
-// k_route_local / k_win_gather store the new batch and set its bits.
-__global__ void k_mask_clear(const uint32_t* __restrict__ ring, uint64_t stride, uint32_t* ring_len, IterState* it,
-                             uint32_t G, uint32_t MW, uint32_t* __restrict__ mask) {
-  pdl_prologue();
-  const uint32_t bit = it->wslot;
-  const uint32_t* __restrict__ list = ring + (size_t)bit * stride;
-  const uint32_t n = ring_len[bit];
-  const uint32_t m = ~(1u << (bit & 31));
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    atomicAnd(&mask[(size_t)(list[i] / G) * MW + (bit >> 5)], m);
+  if (TMA && lane == 0) ring_drain();
+  // ---- S9: the last CTA to finish closes the record
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&it->done, 1u) == gridDim.x - 1) {
-      ring_len[bit] = 0;
-      it->done = 0;
-    }
+    s_last = atomicAdd(&a.scr->serve_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && wib == 0) {
+    __threadfence();
+    if (lane == 0) a.scr->serve_done = 0;
+    end_record(a.it, a.hist, a.cum, a.scr, nvec * 16, a.bad_mirror);
   }
 }
+
+// ------------------------------------------------------------------------------ S10 (G > 1)
+// Window feed. Bit (k mod (W+1)) of mask[q] is set when node q*G+me is in B_k. The ring slot
+// and bit of the batch being fed is it->wslot; its previous bits were cleared by k_dedup of
+// gather(k - W - 1) (the feed is ordered after that kernel).
 // Copy the inboxes of all sources (window IDs routed to this home) into the ring slot and
 // set each node's reuse bit of the slot.
 __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,

@@ -136,6 +136,7 @@ struct Ctx {
   uint64_t N = 0;
   uint32_t R = 0, nvec = 0, A = 0, W = 0, T = 0, MW = 0, Wp1 = 0;
   uint64_t L = 0, S = 0, Q = 0, C = 0, cap = 0, ucap = 0, bcap = 0;
+  uint64_t BC = 0, BCp = 0;  // per-set bucket capacity (distinct nodes of a set per batch); its pow2
   uint64_t pool_rows = 0, stage_base0 = 0, bypass_base = 0;
   uint32_t P = 32, warp_bytes = 0, set_warps = 8;
   int sms = 148;
@@ -149,12 +150,12 @@ struct Ctx {
 
   // local device state
   uint32_t *tags = nullptr, *last_use = nullptr, *rr = nullptr, *mask = nullptr, *mark = nullptr;
-  uint32_t *vst_stamp = nullptr, *vst_idx = nullptr, *set_cnt = nullptr, *set_off = nullptr;
-  uint32_t *bucket = nullptr, *uniq = nullptr, *ring = nullptr, *ring_len = nullptr;
+  uint32_t *vst_stamp = nullptr, *vst_idx = nullptr, *set_cnt = nullptr;
+  uint32_t *bucket = nullptr, *ring = nullptr, *ring_len = nullptr;  // bucket: [S * BC + 32]
   // global scratch for cache sets whose bucket exceeds k_set's shared-memory capacity
-  uint32_t *poff = nullptr, *g_sv = nullptr, *g_sk = nullptr, *g_sidx = nullptr;
+  uint32_t *g_sv = nullptr, *g_sk = nullptr, *g_sidx = nullptr;  // [S * BCp] when a set can exceed P
   unsigned long long* g_skey = nullptr;
-  uint32_t *scan_set = nullptr, *scan_q = nullptr;  // k_scan look-back words (3 x tiles each)
+  uint32_t* scan_q = nullptr;  // k_scan look-back words of the victim-queue scan (2 x tiles)
   uint32_t *qcnt = nullptr, *qoff = nullptr, *qb = nullptr, *qlen = nullptr, *qnode = nullptr;
   uint32_t *qreuse = nullptr, *stg_nodes = nullptr, *route_cnt = nullptr;
   unsigned long long* head = nullptr;            // G = 1 fused delivery: per-node request list heads
@@ -205,13 +206,20 @@ struct Ctx {
   // peer on its own GPU runs both phases after "served". LSMGNN_SPLIT_PULL=0/1 overrides.
   bool split_pull = true;
   bool pdl = false;  // programmatic dependent launch on the G = 1 chain (launch_pdl)
+  // k_serve geometry: CTAs per SM and TMA row stages per warp (0 = 16-B vector copies);
+  // LSMGNN_SERVE_CPS / LSMGNN_SERVE_ST override (A/B runs)
+  int serve_cps = 2, serve_st = 3;
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
   // gather t is ev_gend[t & 7] (gend_t says which t it holds); the last window feed is ev_feed
   cudaEvent_t ev_gend[8] = {};
   int64_t gend_t[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  cudaStream_t gend_st[8] = {};
+  cudaEvent_t ev_dedup[8] = {};  // G > 1: after k_dedup of gather dedup_t[i] (window feeds wait on it)
+  int64_t dedup_t[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   cudaEvent_t ev_feed = nullptr;
+  cudaStream_t feed_st = nullptr;
   bool feed_recorded = false, feed_since_gather = false;
   cudaStream_t last_stream = nullptr;
   // stream of the last gather: a gather issued on another stream first waits for the end of
@@ -301,7 +309,7 @@ int dalloc(T** p, size_t count) {
 int scan_tiles(uint64_t n) { return (int)std::max<uint64_t>(1, (n + kScanTile - 1) / kScanTile); }
 ScanSync scan_sync(uint32_t* words, uint64_t n) {
   const size_t k = (size_t)scan_tiles(n);
-  return ScanSync{words, words + k, words + 2 * k};
+  return ScanSync{words, words + k};
 }
 
 // arena views (local or peer)
@@ -455,10 +463,10 @@ void prof_end(int ph, cudaStream_t st) {
 void detach_file();  // file tier (below)
 int free_all() {
   cudaDeviceSynchronize();
-  void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.set_off, g.scan_set, g.scan_q,
-                  g.bucket, g.uniq, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
+  void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.scan_q,
+                  g.bucket, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
                   g.stg_nodes, g.route_cnt, g.head, g.nxt, g.line_info, g.score, g.fills, g.cands,
-                  g.scr, g.it, g.hist, g.poff, g.g_sv, g.g_sk, g.g_sidx, g.g_skey,
+                  g.scr, g.it, g.hist, g.g_sv, g.g_sk, g.g_sidx, g.g_skey,
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -486,6 +494,8 @@ int free_all() {
   if (g.ev_pull0) cudaEventDestroy(g.ev_pull0);
   if (g.ev_main) cudaEventDestroy(g.ev_main);
   for (auto e : g.ev_gend)
+    if (e) cudaEventDestroy(e);
+  for (auto e : g.ev_dedup)
     if (e) cudaEventDestroy(e);
   if (g.ev_feed) cudaEventDestroy(g.ev_feed);
   if (g.ev_pvp) cudaEventDestroy(g.ev_pvp);
@@ -569,7 +579,7 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
 // gather kernels; n_bound = host bound of this rank's request count (grid sizing only);
 // stamp_host = t + 1 for the G > 1 flag protocol (direct calls only).
 int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host, bool graph, uint32_t stamp_host,
-                  cudaStream_t st) {
+                  cudaStream_t st, cudaEvent_t ev_dedup = nullptr) {
   const int G = g.world;
   KLAUNCH(k_begin, 1, 32, 0, st, g.it, g.hist, g.scr, ba);
   LAUNCHED();
@@ -587,24 +597,45 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   // ---- S3 dedup + set grouping
   prof_begin(1, st);
   const int64_t maxreq = (int64_t)g.cap * G;
-  KLAUNCH(k_dedup, grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st, 
-      inbox, inbox_cnt, (uint32_t)G, (uint32_t)g.cap, (uint32_t)g.rank, (uint32_t)G, (uint32_t)g.S, g.it, g.mark,
-      g.uniq, g.set_cnt, g.scr, g.hist, G == 1 ? g.head : nullptr, g.nxt, G == 1 ? 1u : 0u, g.N);
-  LAUNCHED();
-  KLAUNCH(k_scan, scan_tiles(g.S), 1024, 0, st, g.set_cnt, g.set_off, (uint32_t)g.S, g.C ? g.stg_nodes : nullptr,
-                                           (uint32_t)g.C, g.scr, g.mark, g.it, (uint32_t)G, g.hist, g.poff, g.P,
-                                           scan_sync(g.scan_set, g.S), 0u);
-  LAUNCHED();
-  KLAUNCH(k_bucket, grid_for(std::max<int64_t>(n_bound, 1) * G, 256, 4), 256, 0, st, g.uniq, g.scr, (uint32_t)G,
-                                                                                 (uint32_t)g.S, g.set_off, g.set_cnt,
-                                                                                 g.bucket);
-  LAUNCHED();
+  {
+    DedupArgs da{};
+    da.inbox = inbox;
+    da.inbox_cnt = inbox_cnt;
+    da.nsrc = (uint32_t)G;
+    da.cap = (uint32_t)g.cap;
+    da.me = (uint32_t)g.rank;
+    da.G = (uint32_t)G;
+    da.S = (uint32_t)g.S;
+    da.BC = (uint32_t)g.BC;
+    da.mark = g.mark;
+    da.bucket = g.bucket;
+    da.set_cnt = g.set_cnt;
+    da.head = G == 1 ? g.head : nullptr;
+    da.nxt = g.nxt;
+    da.direct = G == 1 ? 1u : 0u;
+    da.N = g.N;
+    da.ring = g.ring;
+    da.ring_stride = g.cap * G;
+    da.ring_len = g.ring_len;
+    da.mask = g.mask;
+    da.MW = g.MW;
+    da.Wp1 = g.Wp1;
+    KLAUNCH(k_dedup, grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st, da,
+            (const IterState*)g.it, g.scr, g.hist);
+    LAUNCHED();
+  }
+  if (ev_dedup) CK(cudaEventRecord(ev_dedup, st));  // the window feed of t+1+W may follow from here
   prof_end(1, st);
   // ---- S4/S5 probe + replacement
   prof_begin(2, st);
   SetParams sp{};
-  sp.set_off = g.set_off;
+  sp.set_cnt = g.set_cnt;
   sp.bucket = g.bucket;
+  sp.BC = (uint32_t)g.BC;
+  sp.BCp = (uint32_t)g.BCp;
+  sp.stg_nodes = g.C ? g.stg_nodes : nullptr;
+  sp.mark = g.mark;
+  sp.C = (uint32_t)g.C;
   sp.tags = g.tags;
   sp.last_use = g.last_use;
   sp.rr = g.rr;
@@ -629,7 +660,6 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   sp.pvp = (uint32_t)g.opt.pvp;
   sp.reinsert = (uint32_t)g.opt.reinsert_victims;
   sp.P = g.P;
-  sp.poff = g.poff;
   sp.g_sv = g.g_sv;
   sp.g_sk = g.g_sk;
   sp.g_sidx = g.g_sidx;
@@ -655,8 +685,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   if (g.C) {
     prof_begin(3, st);
     const int qg = grid_for(g.ucap, 256, 2);
-    KLAUNCH(k_scan, scan_tiles(g.W), 1024, 0, st, g.qcnt, g.qoff, g.W, nullptr, 0, g.scr, nullptr, g.it, 1, nullptr,
-                                             nullptr, 0, scan_sync(g.scan_q, g.W), 1u);
+    KLAUNCH(k_scan, scan_tiles(g.W), 1024, 0, st, g.qcnt, g.qoff, g.W, (const IterState*)g.it,
+            scan_sync(g.scan_q, g.W));
     LAUNCHED();
     KLAUNCH(k_qscatter, qg, 256, 0, st, g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
     LAUNCHED();
@@ -674,17 +704,38 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   const bool wide = g.nvec >= 256;
   const uint32_t bounce = g.file_fd >= 0 ? 1u : 0u;  // file tier: storage rows staged per fill entry
   if (G == 1) {
-    // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits
+    // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits; its last
+    // CTA closes the record (S9)
     prof_begin(4, st);
     if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
-    const int blocks = g.sms * std::min(4, g.geom_per_sm);
-#define SERVE(U, O)                                                                                                  \
-  KLAUNCH((k_serve<U, O>), blocks, 256, 0, st, g.fills, g.scr, pool, tab, hq, g.nvec, g.head, g.nxt, g.it, g.N, \
-                                        loc_of(g.arena), o4, bounce)
-    if (wide && !out_host) SERVE(8, kDev);
-    else if (wide) SERVE(8, kHost);
-    else if (!out_host) SERVE(2, kDev);
-    else SERVE(2, kHost);
+    ServeArgs sa{};
+    sa.fills = g.fills;
+    sa.scr = g.scr;
+    sa.pool = pool;
+    sa.table = tab;
+    sa.hostq = hq;
+    sa.nvec = g.nvec;
+    sa.head = g.head;
+    sa.nxt = g.nxt;
+    sa.it = g.it;
+    sa.N = g.N;
+    sa.node_loc = loc_of(g.arena);
+    sa.out = o4;
+    sa.bounce = bounce;
+    sa.hist = g.hist;
+    sa.cum = g.cum;
+    sa.bad_mirror = g.bad_dev;
+    const bool tma = !out_host && g.serve_st > 0;
+    sa.ST = tma ? (uint32_t)g.serve_st : 0u;
+    const size_t smem = tma ? (size_t)8 * g.serve_st * g.R : 0;
+    const int blocks = g.sms * std::min(tma ? g.serve_cps : 4, g.geom_per_sm);
+#define SERVE(U, O, T) KLAUNCH((k_serve<U, O, T>), blocks, 256, smem, st, sa)
+    if (wide && tma) SERVE(8, kDev, 1);
+    else if (wide && !out_host) SERVE(8, kDev, 0);
+    else if (wide) SERVE(8, kHost, 0);
+    else if (tma) SERVE(2, kDev, 1);
+    else if (!out_host) SERVE(2, kDev, 0);
+    else SERVE(2, kHost, 0);
 #undef SERVE
     LAUNCHED();
     prof_end(4, st);
@@ -745,40 +796,52 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
 #undef PULL
   }
   prof_end(5, st);
-  KLAUNCH(k_end, 1, 32, 0, st, g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev);
-  LAUNCHED();
+  if (G > 1) {
+    EndArgs ea{g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev};
+    KLAUNCH(k_end, 1, 32, 0, st, ea);
+    LAUNCHED();
+  }
   return 0;
 }
 
+int wait_dedup(int64_t t, cudaStream_t st);  // (below)
+
 // Window feed of one batch (G = 1 local path, or the G > 1 exchange). k_host >= 0: host
-// values; k_host < 0: graph replay (batch from the ring).
+// values; k_host < 0: graph replay (batch from the ring). The ring slot / mask bit it rewrites,
+// k mod (W+1), was cleared by k_dedup of gather(k - W - 1): feed_begin orders the launch after
+// that gather at G = 1; at G > 1 the exchange runs first and k_win_gather waits for the event
+// recorded after that gather's k_dedup.
 int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* n_dev, const int64_t* const* ids_ring,
                   const int64_t* n_ring, uint32_t ring_len, int64_t n_bound, cudaStream_t st) {
   const int G = g.world;
-  KLAUNCH(k_win_begin, 1, 32, 0, st, g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1,
-                                (int64_t)g.cap, g.bad_dev_overflow);
-  LAUNCHED();
   const uint64_t stride = g.cap * G;
-  // drop the bits of the iteration that last used this slot (k - (W+1)), then empty the slot
-  KLAUNCH(k_mask_clear, grid_for((int64_t)stride, 256, 2), 256, 0, st, g.ring, stride, g.ring_len, g.it, (uint32_t)G, g.MW,
-                                                                   g.mask);
-  LAUNCHED();
   if (G == 1) {
-    if (n_bound > 0) {
-      KLAUNCH(k_route_local, grid_for(n_bound, 256), 256, 0, st, g.it, g.N, g.ring, stride, g.ring_len, g.scr, g.mask,
-                                                            g.MW);
+    if (k_host < 0 || n_dev) {  // graph replay, or a device-resident length: IterState carries the batch
+      KLAUNCH(k_win_begin, 1, 32, 0, st, g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1,
+              (int64_t)g.cap, g.bad_dev_overflow);
+      LAUNCHED();
+      KLAUNCH(k_route_local, grid_for(n_bound, 256), 256, 0, st, g.it, (int64_t)-1, (const int64_t*)nullptr, (int64_t)0,
+              g.Wp1, g.N, g.ring, stride, g.ring_len, g.scr, g.mask, g.MW);
+      LAUNCHED();
+    } else {  // direct: one launch, the batch as kernel arguments
+      KLAUNCH(k_route_local, grid_for(std::max<int64_t>(n, 1), 256), 256, 0, st, g.it, k_host, ids, n, g.Wp1, g.N,
+              g.ring, stride, g.ring_len, g.scr, g.mask, g.MW);
       LAUNCHED();
     }
-  } else {
-    const uint32_t seq = ++g.win_seq;
-    if (int rc = exchange_ids(n_bound, true, seq, st)) return rc;
-    k_win_gather<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(win_of(g.arena), wcnt_of(g.arena), (uint32_t)G,
-                                                                    (uint32_t)g.cap, g.ring, stride, g.ring_len, g.it,
-                                                                    (uint32_t)G, g.MW, g.mask);
-    LAUNCHED();
-    // window inbox consumed
-    if (int rc = flags_write_all(st, (uint32_t)(3 * G + g.rank), seq)) return rc;
+    return 0;
   }
+  KLAUNCH(k_win_begin, 1, 32, 0, st, g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1,
+          (int64_t)g.cap, g.bad_dev_overflow);
+  LAUNCHED();
+  const uint32_t seq = ++g.win_seq;
+  if (int rc = exchange_ids(n_bound, true, seq, st)) return rc;
+  if (int rc = wait_dedup(k_host - (int64_t)g.W - 1, st)) return rc;
+  k_win_gather<<<grid_for((int64_t)g.cap, 256, 2), 256, 0, st>>>(win_of(g.arena), wcnt_of(g.arena), (uint32_t)G,
+                                                                  (uint32_t)g.cap, g.ring, stride, g.ring_len, g.it,
+                                                                  (uint32_t)G, g.MW, g.mask);
+  LAUNCHED();
+  // window inbox consumed
+  if (int rc = flags_write_all(st, (uint32_t)(3 * G + g.rank), seq)) return rc;
   return 0;
 }
 
@@ -788,31 +851,51 @@ int note_gather_end(int64_t t, cudaStream_t st) {
   if (!g.ev_gend[i]) CK(cudaEventCreateWithFlags(&g.ev_gend[i], cudaEventDisableTiming));
   CK(cudaEventRecord(g.ev_gend[i], st));
   g.gend_t[i] = t;
+  g.gend_st[i] = st;
   return 0;
 }
-// `st` waits for the end of gather t (t < 0: nothing to wait for). If that record was
-// overwritten, wait for every recorded gather (conservative, still correct).
+// `st` waits for the end of gather t (t < 0: nothing to wait for). A record on `st` itself is
+// already ordered (and an event wait there would only cut the programmatic launch chain). If
+// that record was overwritten, wait for every recorded gather (conservative, still correct).
 int wait_gather_end(int64_t t, cudaStream_t st) {
   if (t < 0) return 0;
   const int i = (int)(t & 7);
   if (g.gend_t[i] == t) {
-    CK(cudaStreamWaitEvent(st, g.ev_gend[i], 0));
+    if (g.gend_st[i] != st) CK(cudaStreamWaitEvent(st, g.ev_gend[i], 0));
     return 0;
   }
   for (int j = 0; j < 8; ++j)
-    if (g.gend_t[j] >= 0) CK(cudaStreamWaitEvent(st, g.ev_gend[j], 0));
+    if (g.gend_t[j] >= 0 && g.gend_st[j] != st) CK(cudaStreamWaitEvent(st, g.ev_gend[j], 0));
   return 0;
 }
-// Before feeding iteration k: the previous feed (IterState window fields, ring order) and
-// gather(k - W - 2), the last gather that reads mask bit / ring slot k mod (W+1).
+// G > 1: the event recorded after k_dedup of gather t (the clear of ring slot t mod (W+1)).
+cudaEvent_t dedup_event(int64_t t) {
+  const int i = (int)(t & 7);
+  if (!g.ev_dedup[i]) cudaEventCreateWithFlags(&g.ev_dedup[i], cudaEventDisableTiming);
+  g.dedup_t[i] = t;
+  return g.ev_dedup[i];
+}
+int wait_dedup(int64_t t, cudaStream_t st) {
+  if (t < 0) return 0;
+  const int i = (int)(t & 7);
+  if (g.dedup_t[i] == t) {
+    CK(cudaStreamWaitEvent(st, g.ev_dedup[i], 0));
+    return 0;
+  }
+  return wait_gather_end(t, st);  // not recorded (cannot happen through the C-ABI): the whole gather
+}
+// Before feeding iteration k: the previous feed (IterState window fields, ring order) and, at
+// G = 1, gather(k - W - 1), whose k_dedup clears mask bit / ring slot k mod (W+1) (at G > 1 the
+// feed's exchange runs first and only k_win_gather waits, for that k_dedup).
 int feed_begin(int64_t k, cudaStream_t st) {
-  if (g.feed_recorded) CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
-  return wait_gather_end(k - (int64_t)g.W - 2, st);
+  if (g.feed_recorded && g.feed_st != st) CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+  return g.world == 1 ? wait_gather_end(k - (int64_t)g.W - 1, st) : 0;
 }
 int feed_end(cudaStream_t st) {
   if (!g.ev_feed) CK(cudaEventCreateWithFlags(&g.ev_feed, cudaEventDisableTiming));
   CK(cudaEventRecord(g.ev_feed, st));
   g.feed_recorded = g.feed_since_gather = true;
+  g.feed_st = st;
   return 0;
 }
 
@@ -983,8 +1066,12 @@ int plan_layout(Ctx& c, int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype,
   c.bypass_base = c.L + 2 * c.C;
   c.pool_rows = c.L + 2 * c.C + c.bcap;
   if (c.pool_rows >= (uint64_t)kHostBit) return set_err(LSMGNN_EINVAL, "pool too large for 31-bit rows");
-  // k_set per-warp shared memory: the largest possible bucket of one set
+  // k_set per-warp shared memory: the largest possible bucket of one set (set s holds the home
+  // rows q = s, s + S, ...: at most ceil(Q / S) distinct nodes, and at most the batch's)
   const uint64_t maxm = std::min<uint64_t>((c.Q + c.S - 1) / c.S, c.ucap);
+  c.BC = maxm;
+  c.BCp = 32;
+  while (c.BCp < maxm) c.BCp <<= 1;
   c.P = 32;
   while (c.P < maxm && c.P < 1024) c.P <<= 1;  // larger buckets fall back to global scratch
   c.warp_bytes = (uint32_t)align_up(20ull * c.P + 4 * 32 * 4, 16);
@@ -1095,18 +1182,14 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.vst_stamp, g.Q);
   DA(g.vst_idx, g.Q);
   DA(g.set_cnt, g.S);
-  DA(g.set_off, g.S + 1);
-  DA(g.scan_set, 3 * (size_t)scan_tiles(g.S));
-  DA(g.scan_q, 3 * (size_t)scan_tiles(g.W));
-  if (big_sets) {  // power-of-two regions per oversized set: at most 2x the unique count
-    DA(g.poff, g.S);
-    DA(g.g_sv, 2 * g.ucap + 64);
-    DA(g.g_sk, 2 * g.ucap + 64);
-    DA(g.g_sidx, 2 * g.ucap + 64);
-    DA(g.g_skey, 2 * g.ucap + 64);
+  DA(g.scan_q, 2 * (size_t)scan_tiles(g.W));
+  if (big_sets) {  // a power-of-two region of global scratch per set that can exceed P
+    DA(g.g_sv, g.S * g.BCp + 64);
+    DA(g.g_sk, g.S * g.BCp + 64);
+    DA(g.g_sidx, g.S * g.BCp + 64);
+    DA(g.g_skey, g.S * g.BCp + 64);
   }
-  DA(g.bucket, g.ucap);
-  DA(g.uniq, g.ucap);
+  DA(g.bucket, g.S * g.BC + 32);  // + 32: k_set reads a set's first 32 entries unconditionally
   DA(g.ring, (size_t)g.Wp1 * g.cap * G);
   DA(g.ring_len, g.Wp1);
   DA(g.qcnt, g.W);
@@ -1158,6 +1241,26 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   CK(cudaEventCreateWithFlags(&g.ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_pvp, cudaEventDisableTiming));
   CK(cudaFuncSetAttribute(k_set, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(g.warp_bytes * g.set_warps)));
+  {  // k_serve: the most row stages per SM within ~192 KB of shared memory, 2..8 per warp
+    const uint64_t budget = 192 * 1024;
+    g.serve_cps = 1;
+    g.serve_st = 0;
+    for (int cps = 3; cps >= 1 && !g.serve_st; --cps) {
+      const uint64_t st = std::min<uint64_t>(kMaxStages, budget / ((uint64_t)cps * 8 * g.R));
+      if (st >= 2 && (uint64_t)cps * st >= 6) {
+        g.serve_cps = cps;
+        g.serve_st = (int)st;
+      }
+    }
+    if (!g.serve_st && (uint64_t)8 * 2 * g.R <= budget) g.serve_st = 2;
+    if (const char* e = std::getenv("LSMGNN_SERVE_CPS")) g.serve_cps = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("LSMGNN_SERVE_ST")) g.serve_st = std::max(0, std::min((int)kMaxStages, std::atoi(e)));
+    if (g.serve_st) {
+      const int smem = (int)((size_t)8 * g.serve_st * g.R);
+      CK(cudaFuncSetAttribute(k_serve<8, kDev, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_serve<2, kDev, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+  }
   g.pdl = G == 1 && !std::getenv("LSMGNN_NO_PDL");
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
@@ -1299,13 +1402,14 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     g.pvp_pending = false;
   }
   if (g.feed_since_gather) {  // the window fed through t+W (possibly on another stream)
-    CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+    if (g.feed_st != st) CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
     g.feed_since_gather = false;
   }
   if (t > 0 && st != g.gather_st)  // same stream: already ordered (and PDL keeps chaining)
     if (int rc = wait_gather_end(t - 1, st)) return rc;
   const BeginArgs ba = begin_args(t, node_ids, n, nullptr, nullptr, 0);
-  if (int rc = launch_gather(ba, n, out, out_host, false, (uint32_t)(t + 1), st)) return rc;
+  if (int rc = launch_gather(ba, n, out, out_host, false, (uint32_t)(t + 1), st, g.world > 1 ? dedup_event(t) : nullptr))
+    return rc;
   if (int rc = note_gather_end(t, st)) return rc;
   g.t_next = t + 1;
   g.gather_st = st;
@@ -1328,6 +1432,7 @@ int lsmgnn_prefetch(const int64_t* ids, const int64_t* offsets, int32_t num_batc
     const int64_t n = offsets[b + 1] - offsets[b];
     if (n < 0 || (uint64_t)n > g.cap) return set_err(LSMGNN_EINVAL, "window batch of %lld ids", (long long)n);
     if (k > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
+    if (k < g.t_next) return set_err(LSMGNN_ESTATE, "window iteration %lld was already gathered", (long long)k);
     if (int rc = feed_begin(k, st)) return rc;
     if (int rc = launch_window(k, n > 0 ? ids + offsets[b] : nullptr, n, nullptr, nullptr, nullptr, 0, n, st))
       return rc;
@@ -1555,6 +1660,7 @@ int lsmgnn_prefetch_dev(const int64_t* ids, const int64_t* count_dev, int64_t fi
   if (!count_dev) return set_err(LSMGNN_EINVAL, "null count");
   if (first_iter != g.feed_next) return set_err(LSMGNN_ESTATE, "window iteration out of order");
   if (first_iter > g.t_next + (int64_t)g.W) return set_err(LSMGNN_ESTATE, "window fed beyond t+W");
+  if (first_iter < g.t_next) return set_err(LSMGNN_ESTATE, "window iteration already gathered");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   prof_begin(6, st);
   if (int rc = feed_begin(first_iter, st)) return rc;
@@ -1597,16 +1703,17 @@ int lsmgnn_graph_capture(const int64_t* const* ids_ring, const int64_t* n_ring, 
   const bool prof = g.prof;
   g.prof = false;  // no host-side event spans inside a graph
   const int64_t l0 = g.launches;
-  // Two branches: gather(t) and the window feed of t+1+W. They touch disjoint data — the
-  // feed rewrites ring slot / mask bit t mod (W+1), which gather(t) never reads (it looks
-  // at t+1..t+W) — so they run concurrently; the feed only has to follow gather(t-1),
-  // which the previous replay on the same stream guarantees.
+  // Two branches: gather(t) and, forked after its k_dedup (which clears ring slot / mask bit
+  // t mod (W+1)), the window feed of t+1+W. The feed rewrites only that slot and bit, which
+  // the rest of gather(t) never reads (it looks at t+1..t+W), so the two run concurrently.
   CK(cudaStreamBeginCapture(g.cap_stream, cudaStreamCaptureModeThreadLocal));
-  cudaError_t fe = cudaEventRecord(g.ev_fork, g.cap_stream);
-  if (fe == cudaSuccess) fe = cudaStreamWaitEvent(g.cap_stream2, g.ev_fork, 0);
   const BeginArgs ba = begin_args(-1, nullptr, 0, ids_ring, n_ring, (uint32_t)ring_len);
-  int rc = fe == cudaSuccess ? launch_gather(ba, (int64_t)g.cap, out, out_host, true, 0, g.cap_stream)
-                             : set_err(LSMGNN_ECUDA, "graph fork: %s", cudaGetErrorString(fe));
+  int rc = launch_gather(ba, (int64_t)g.cap, out, out_host, true, 0, g.cap_stream, g.ev_fork);
+  cudaError_t fe = cudaSuccess;
+  if (!rc) {
+    fe = cudaStreamWaitEvent(g.cap_stream2, g.ev_fork, 0);
+    if (fe != cudaSuccess) rc = set_err(LSMGNN_ECUDA, "graph fork: %s", cudaGetErrorString(fe));
+  }
   if (!rc) rc = launch_window(-1, nullptr, 0, nullptr, ids_ring, n_ring, (uint32_t)ring_len, (int64_t)g.cap, g.cap_stream2);
   if (!rc) {
     fe = cudaEventRecord(g.ev_join, g.cap_stream2);
