@@ -266,6 +266,8 @@ def main():
     lines = args.lines or wl.lines_per_gpu
     GK = args.graph_steps if (G == 1 and not args.graph) else 0
     iters = Wu + K + 2 * E + GK + W + 1  # E strict e2e steps + E device-result e2e steps
+    if G == 1 and not args.no_ablation and "hbm_regime" in args.extras:
+        iters = max(iters, W + 1 + 100)  # hbm_regime: 40 warm-up + 30 timed + 15 two-stream + 15 graph steps
     g_, trace, scores = build_inputs(wl, G, rank, iters, only_mine=G > 1)
 
     import torch
@@ -840,10 +842,12 @@ def step_roofline(tb, K, T, pcie_peak, hbm_peak, G):
                              "nvlink": "B200_PROFILING.md measured peer copy per direction"}}
 
 
-def epoch_storage(wl, g, scores, lines, dev, policies=("hybrid", "static", "lru"), pvp_row=True):
+def epoch_storage(wl, g, scores, lines, dev, policies=("hybrid", "static", "lru", "dynamic"), pvp_row=True):
     """The metric's second half: storage-tier bytes per epoch for the
     bench workload — epoch 0 warms the cache, epoch 1 is measured; hybrid vs static-only vs
-    LRU at equal lines (+ hybrid with PVP). Counts-only runs of the CUDA path with 16-B rows
+    LRU vs dynamic-only at equal lines (+ hybrid with PVP), with exact dynamic information
+    (update period P = 1, this build's default) and with the paper's periodic update (P = 4,
+    P:607) for the two policies that use it. Counts-only runs of the CUDA path with 16-B rows
     (counters do not depend on the payload); bytes reported for the workload's rows."""
     import torch
     import synth
@@ -863,10 +867,11 @@ def epoch_storage(wl, g, scores, lines, dev, policies=("hybrid", "static", "lru"
     F = {n: i for i, n in enumerate(STATS_FIELDS)}
     res = {"iterations_per_epoch": ipe, "epochs": "0 warm-up, 1 measured", "lines": lines,
            "row_bytes_reported": wl.R, "trace_gen_s": round(gen_s, 1)}
-    runs = [(p, 0) for p in policies] + ([("hybrid", 1)] if pvp_row else [])
-    for pol, pvp in runs:
+    runs = [(p, 0, 1) for p in policies] + [("hybrid", 0, 4), ("dynamic", 0, 4)] + \
+        ([("hybrid", 1, 1)] if pvp_row else [])
+    for pol, pvp, per in runs:
         c = LsmGnn(wl.N, 4, lines, wl.ways, wl.victim_lines if pvp else 0, scores, policy=pol, pvp=pvp, window=W,
-                   max_batch_ids=mb, device=dev.index)
+                   max_batch_ids=mb, device=dev.index, period=per)
         c.attach_storage(table)
         c.prefetch([ids[k] if k < K else empty for k in range(1, W + 1)], first_iter=1)
         t1 = time.time()
@@ -878,13 +883,18 @@ def epoch_storage(wl, g, scores, lines, dev, policies=("hybrid", "static", "lru"
         c.close()
         e1 = h.sum(axis=0)
         u = max(int(e1[F["unique"]]), 1)
-        key = pol + ("+pvp" if pvp else "")
+        key = pol + ("+pvp" if pvp else "") + (f"@P{per}" if per > 1 else "")
         res[key] = {"storage_GB_per_epoch": round(int(e1[F["storage_reads"]]) * wl.R / 1e9, 3),
                     "hit_ratio": round(int(e1[F["hits"]] + e1[F["victim_hits"]]) / u, 4),
                     "run_s": round(time.time() - t1, 2)}
     h = res["hybrid"]["storage_GB_per_epoch"]
     res["hybrid_vs_static"] = round(h / res["static"]["storage_GB_per_epoch"], 4)
     res["hybrid_vs_lru"] = round(h / res["lru"]["storage_GB_per_epoch"], 4)
+    res["hybrid_vs_dynamic"] = round(h / res["dynamic"]["storage_GB_per_epoch"], 4)
+    res["hybrid_vs_dynamic_at_P4"] = round(res["hybrid@P4"]["storage_GB_per_epoch"] /
+                                           res["dynamic@P4"]["storage_GB_per_epoch"], 4)
+    res["note"] = ("P = update period of the dynamic information (R6): 1 = exact every iteration (default), "
+                   "4 = the paper's periodic window scan (P:607)")
     return res
 
 

@@ -943,44 +943,82 @@ struct PullArgs {
   const uint4* pool[8];
   const uint32_t* node_loc[8];
   uint32_t G;
+  uint32_t ST;  // TMA ring stages per warp (TMA = 1)
 };
-template <int UNROLL, int OUT, int PHASE>
+// TMA = 1: rows move (local or peer) HBM -> shared -> `out` with TMA bulk copies through each
+// warp's ring of ST stages (the source of a peer row is its IPC mapping: over NVLink on
+// distinct GPUs); TMA = 0: 16-byte vector loads/stores (pinned host `out`).
+template <int UNROLL, int OUT, int PHASE, int TMA>
 __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __restrict__ out, uint32_t nvec) {
   pdl_prologue();
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar[8][kMaxStages];
+  __shared__ uint32_t s_pend[8][kMaxStages];
+  __shared__ const void* s_src[8][32];
+  __shared__ void* s_dst[8][32];
   const int64_t* __restrict__ ids = it->ids;
   const int64_t n = it->n;
   const int lane = (int)lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  RowRing ring{};
+  if (TMA) {
+    ring.buf = smem + (size_t)wib * a.ST * nvec * 16;
+    ring.bar = s_bar[wib];
+    ring.pend = s_pend[wib];
+    ring.ST = a.ST;
+    ring.R = nvec * 16;
+    if (lane == 0) ring_init(ring);
+    __syncwarp();
+  }
   // A warp takes kChunk consecutive requests: its lanes read the IDs and the (local or
   // peer) node_loc words at once — one dependent round trip per chunk instead of two per
   // row, which matters most when node_loc is a peer's (NVLink latency) — then the warp
-  // copies the rows of this phase one by one.
-  constexpr uint32_t kChunk = 16;
+  // copies the rows of this phase.
+  constexpr uint32_t kChunk = 32;
   for (int64_t c0 = warp * kChunk; c0 < n; c0 += nwarps * kChunk) {
     const uint32_t m = (uint32_t)min((int64_t)kChunk, n - c0);
-    uint32_t loc_l = kInvalid, g_l = 0;
+    uint32_t loc = kInvalid, g = 0;
+    bool valid = false;
     if ((uint32_t)lane < m) {
       const int64_t x = ids[c0 + lane];
       if (x >= 0 && (uint64_t)x < N) {
         const uint32_t v = (uint32_t)x;
-        g_l = v % a.G;
-        loc_l = a.node_loc[g_l][v / a.G];
+        g = v % a.G;
+        loc = a.node_loc[g][v / a.G];
+        valid = true;
       }
     }
-    for (uint32_t j = 0; j < m; ++j) {
-      const uint32_t loc = __shfl_sync(0xffffffffu, loc_l, (int)j);
-      const uint32_t g = __shfl_sync(0xffffffffu, g_l, (int)j);
-      uint4* dst = out + (size_t)(c0 + j) * nvec;
-      if (loc == kInvalid) {  // ERANGE: zero-filled row
-        if (PHASE == 0)
-          for (uint32_t k = lane; k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
-        continue;
+    if (PHASE == 0) {  // ERANGE: zero-filled rows
+      uint32_t zero = __ballot_sync(0xffffffffu, (uint32_t)lane < m && !valid);
+      while (zero) {
+        const uint32_t j = __ffs(zero) - 1;
+        zero &= zero - 1;
+        uint4* dst = out + (size_t)(c0 + j) * nvec;
+        for (uint32_t k = lane; k < nvec; k += 32) st16<OUT>(dst + k, make_uint4(0, 0, 0, 0));
       }
-      if (((loc & kDelivered) != 0) != (PHASE == 1)) continue;
-      warp_copy_row<UNROLL, kDev, OUT>(dst, a.pool[g] + (size_t)(loc & ~kDelivered) * nvec, nvec);
+    }
+    const uint32_t need = __ballot_sync(0xffffffffu, valid && (((loc & kDelivered) != 0) == (PHASE == 1)));
+    if (TMA) {
+      s_src[wib][lane] = a.pool[g] + (size_t)(loc & ~kDelivered) * nvec;
+      s_dst[wib][lane] = out + (size_t)(c0 + lane) * nvec;
+      __syncwarp();
+      if (lane == 0 && need) ring_copy(ring, s_src[wib], s_dst[wib], need);
+      __syncwarp();
+    } else {
+      uint32_t mk = need;
+      while (mk) {
+        const uint32_t j = __ffs(mk) - 1;
+        mk &= mk - 1;
+        const uint32_t lj = __shfl_sync(0xffffffffu, loc, (int)j);
+        const uint32_t gj = __shfl_sync(0xffffffffu, g, (int)j);
+        warp_copy_row<UNROLL, kDev, OUT>(out + (size_t)(c0 + j) * nvec, a.pool[gj] + (size_t)(lj & ~kDelivered) * nvec,
+                                         nvec);
+      }
     }
   }
+  if (TMA && lane == 0) ring_drain();
 }
 
 // ------------------------------------------------------------------------------ S6+S8 fused (G = 1)

@@ -751,13 +751,19 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       pa.node_loc[h] = loc_of(g.peer_arena[h]);
     }
     pa.G = (uint32_t)G;
-    const int pblocks = grid_for(n_bound * 2, 256, 8);  // a warp per 16 requests
-#define PULL(PH, S)                                                                        \
-  do {                                                                                     \
-    if (wide && !out_host) k_pull<8, kDev, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec); \
-    else if (wide) k_pull<8, kHost, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);        \
-    else if (!out_host) k_pull<2, kDev, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);    \
-    else k_pull<2, kHost, PH><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);                 \
+    const bool tma = !out_host && g.serve_st > 0;
+    pa.ST = tma ? (uint32_t)g.serve_st : 0u;
+    const size_t psmem = tma ? (size_t)8 * g.serve_st * g.R : 0;
+    // a warp per 32 requests; with TMA rings, at most serve_cps CTAs per SM fit
+    const int pblocks = grid_for(n_bound, 256, tma ? g.serve_cps : 8);
+#define PULL(PH, S)                                                                                          \
+  do {                                                                                                       \
+    if (wide && tma) k_pull<8, kDev, PH, 1><<<pblocks, 256, psmem, S>>>(g.it, g.N, pa, o4, g.nvec);           \
+    else if (wide && !out_host) k_pull<8, kDev, PH, 0><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);  \
+    else if (wide) k_pull<8, kHost, PH, 0><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);               \
+    else if (tma) k_pull<2, kDev, PH, 1><<<pblocks, 256, psmem, S>>>(g.it, g.N, pa, o4, g.nvec);              \
+    else if (!out_host) k_pull<2, kDev, PH, 0><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);          \
+    else k_pull<2, kHost, PH, 0><<<pblocks, 256, 0, S>>>(g.it, g.N, pa, o4, g.nvec);                         \
   } while (0)
     if (n_bound > 0 && g.split_pull) {
       CK(cudaEventRecord(g.ev_set, st));
@@ -1259,6 +1265,10 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
       const int smem = (int)((size_t)8 * g.serve_st * g.R);
       CK(cudaFuncSetAttribute(k_serve<8, kDev, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       CK(cudaFuncSetAttribute(k_serve<2, kDev, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_pull<8, kDev, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_pull<8, kDev, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_pull<2, kDev, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_pull<2, kDev, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
   }
   g.pdl = G == 1 && !std::getenv("LSMGNN_NO_PDL");
