@@ -267,7 +267,7 @@ def main():
     GK = args.graph_steps if (G == 1 and not args.graph) else 0
     iters = Wu + K + 2 * E + GK + W + 1  # E strict e2e steps + E device-result e2e steps
     if G == 1 and not args.no_ablation and "hbm_regime" in args.extras:
-        iters = max(iters, W + 1 + 100)  # hbm_regime: 40 warm-up + 30 timed + 15 two-stream + 15 graph steps
+        iters = max(iters, W + 1 + 115)  # hbm_regime: 40 warm-up + 30 timed + 15 profiled + 15 two-stream + 15 graph
     g_, trace, scores = build_inputs(wl, G, rank, iters, only_mine=G > 1)
 
     import torch
@@ -666,7 +666,7 @@ def _file_tier_runs(wl, scores, ids_d, lines, args, max_ids, dev, warm, steps, p
 
 
 def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, warm=40, steps=30, s2steps=15,
-               gsteps=15):
+               gsteps=15, psteps=15):
     """The same workload with a cache that holds the whole table (lines_per_gpu = N): after
     warm-up nearly every request hits, the storage tier drops out, and the step is bound by
     HBM — k_serve reads each requested row from its slot and writes it to `out`. Reports the
@@ -686,22 +686,32 @@ def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, 
     c.prefetch(ids_d[1:W + 1], first_iter=1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0 = None
+    # timed steps: no phase events between the kernels (they would cut the programmatic launch chain)
     for t in range(warm + steps):
         if t == warm:
             torch.cuda.synchronize()
             s0 = c.stats(1)
-            c.profile(True)
-            c.profile_read()
             e0.record(st)
         c.gather(ids_d[t], out)
         c.prefetch([ids_d[t + 1 + W]], first_iter=t + 1 + W)
     e1.record(st)
     torch.cuda.synchronize()
+    s1 = c.stats(1)
+    # then psteps more with phase events: the per-phase split and k_serve's duration for its roofline
+    t0 = warm + steps
+    psteps = max(1, min(psteps, len(ids_d) - W - 1 - t0))
+    c.profile(True)
+    c.profile_read()
+    p0 = c.stats(1)
+    for t in range(t0, t0 + psteps):
+        c.gather(ids_d[t], out)
+        c.prefetch([ids_d[t + 1 + W]], first_iter=t + 1 + W)
+    torch.cuda.synchronize()
     prof = c.profile_read()
     c.profile(False)
-    s1 = c.stats(1)
+    p1 = c.stats(1)
+    t0 += psteps
     # the window feed on a second stream: it only waits for gather(t-1), so it overlaps gather(t)
-    t0 = warm + steps
     s2steps = max(0, min(s2steps, len(ids_d) - W - 1 - t0))
     two = None
     if s2steps:
@@ -739,19 +749,23 @@ def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, 
     c.close()
     T = e0.elapsed_time(e1) / 1e3
     d = {k: s1[k] - s0[k] for k in s1 if k != "iter"}
+    dp = {k: p1[k] - p0[k] for k in p1 if k != "iter"}
     R = wl.R
     serve_ms = prof.get("fill", (0.0, 0))[0]
-    alg = (2 * d["requests"] + 2 * d["storage_reads"]) * R
+    alg = (2 * dp["requests"] + 2 * dp["storage_reads"]) * R
     ach = alg / (serve_ms / 1e3) / 1e9 if serve_ms > 0 else 0.0
     return {"lines_per_gpu": lines, "warmup": warm, "steps": steps,
             "value": round(d["requests"] * R / T / 1e9, 2), "unit": "GB/s", "ms_per_step": round(T / steps * 1e3, 4),
             "hit_ratio": round(d["hits"] / max(d["unique"], 1), 4), "two_streams": two, "graph_replay": graph,
-            "phases_ms_per_step": {k: round(v[0] / steps, 4) for k, v in prof.items()},
+            "profiled_steps": psteps,
+            "phases_ms_per_step": {k: round(v[0] / psteps, 4) for k, v in prof.items()},
             "roofline": {"bound": "hbm", "kernel": "k_serve", "achieved": round(ach, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "peak_source": hbm_src,
-                         "per_launch": {"algorithmic_bytes": int(alg / steps), "avg_ms": round(serve_ms / steps, 4),
+                         "per_launch": {"algorithmic_bytes": int(alg / psteps), "avg_ms": round(serve_ms / psteps, 4),
                                         "units": "2R per request + 2R per fill row"}},
-            "what": "cache holds the whole table: the hit path alone (HBM-bound), same trace as the headline"}
+            "what": "cache holds the whole table: the hit path alone (HBM-bound), same trace as the headline; "
+                    "value/ms_per_step from steps without phase events, phases and k_serve's roofline from "
+                    "profiled_steps more steps with events around each phase"}
 
 
 def pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev, train_ms=10.0, warm=10, steps=20):

@@ -36,6 +36,10 @@
  *   LSMGNN_STORAGE_BUFFERED=1 file tier through the page cache instead of O_DIRECT
  *   LSMGNN_IO_THREADS=n       file-tier pread workers per batch (default 64)
  *   LSMGNN_GEOMETRY=small     one CTA per SM for every grid (launch-geometry tests)
+ *   LSMGNN_SERVE_CPS=c, LSMGNN_SERVE_ST=s  serve/pull geometry: c CTAs per SM, s TMA row stages
+ *                             per warp (s = 0: 16-B vector copies instead of TMA bulk copies)
+ *   LSMGNN_G1_PULL=1          G = 1 profiling aid: the G > 1 serve path (k_fill, k_pull phases,
+ *                             k_end) instead of the fused k_serve; results are identical
  */
 #ifndef LSMGNN_H
 #define LSMGNN_H
@@ -145,9 +149,12 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
  * O_DIRECT when R is a multiple of 512 (the page cache is bypassed: every storage read is
  * a device read), buffered otherwise; LSMGNN_STORAGE_BUFFERED=1 forces buffered. Each
  * gather then reads the rows its fills need (known once replacement has run) with
- * parallel pread into a pinned bounce buffer that the fill kernel reads over PCIe — a host
- * step in the middle of the gather (it synchronises `stream` once); graph capture is
- * refused in this mode. Open/read failures return LSMGNN_EIO (a read failure is sticky:
+ * parallel pread into a pinned bounce buffer that the fill kernel reads over PCIe: the device
+ * publishes the fill list to pinned host memory, the fill kernel is launched at once and waits
+ * per chunk of 64 entries for a host-written ready flag, and the calling thread reads the rows
+ * chunk by chunk, releasing each as it lands — reads and fills overlap and `stream` is never
+ * synchronised, but lsmgnn_gather returns only after this batch's reads are done (the host
+ * waits for the device to publish the list). Graph capture is refused in this mode. Open/read failures return LSMGNN_EIO (a read failure is sticky:
  * the cache already recorded the rows). Exactly one of the two
  * arguments must be non-NULL. */
 int lsmgnn_attach_storage(const void* host_rows_for_my_home, const char* nvme_path);

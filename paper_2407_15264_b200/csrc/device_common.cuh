@@ -52,7 +52,8 @@ struct Scratch {
   uint32_t pvp_done;   // grid-completion counter of the PVP kernel
   uint32_t pull_next;  // k_serve: next request index handed to a delivering warp
   uint32_t serve_done; // k_serve: CTAs finished (the last one closes the record)
-  uint32_t pad[5];
+  uint32_t io_done;    // k_io_export: CTAs finished (the last one publishes the list)
+  uint32_t pad[4];
 };
 
 // Per-iteration values, resident on the device. k_begin / k_win_begin write them (from host

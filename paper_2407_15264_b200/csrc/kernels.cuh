@@ -907,6 +907,62 @@ __global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, c
   (void)adm;
 }
 
+// ------------------------------------------------------------------------------ S6 file tier (N2)
+// The fills of this batch are decided on the device (k_set); the host reads their storage rows
+// from the file. k_io_export publishes the list to pinned host memory — io->src[e] = backing
+// row of fill entry e (kInvalid: a PVP staging row, nothing to read), io->n, then io->list =
+// stamp (system-scope release) — and the host, which polls io->list, reads the rows into the
+// bounce buffer (row e = entry e) chunk by chunk, setting io->ready[c] = stamp after chunk c's
+// kIoChunk entries. The fill kernel, launched right behind, waits per entry for its chunk's flag
+// (io_wait), so the storage reads and the fills overlap and the stream is never synchronised.
+constexpr uint32_t kIoChunk = 64;
+struct IoShared {     // pinned, mapped host memory (device pointer)
+  uint32_t list;      // stamp of the batch whose list is published
+  uint32_t n;         // fill entries of that batch
+  uint32_t pad[30];
+  // followed by: ready[ceil(ucap / kIoChunk)], then src[ucap]
+};
+__device__ __forceinline__ uint32_t ld_acquire_sys(const volatile uint32_t* p) {
+  uint32_t r;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_release_sys(volatile uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__global__ void k_io_export(const FillEnt* __restrict__ fills, Scratch* scr, const IterState* it,
+                            IoShared* io, uint32_t* io_src) {
+  pdl_prologue();
+  const uint32_t n = scr->nfill;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const uint32_t src = fills[e].src;
+    io_src[e] = (src & kHostBit) ? (src & ~kHostBit) : kInvalid;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(&scr->io_done, 1u) == gridDim.x - 1) {  // last CTA: the whole list is out
+      scr->io_done = 0;
+      __threadfence_system();
+      *(volatile uint32_t*)&io->n = n;
+      st_release_sys(&io->list, it->stamp);
+    }
+  }
+}
+// Lane 0 spins until chunk e / kIoChunk of this batch is in the bounce buffer (acquire: the
+// row's bytes are visible after it), then the warp proceeds.
+__device__ __forceinline__ void io_wait(const uint32_t* ready, uint32_t e, uint32_t stamp) {
+  if (lane_id() == 0) {
+    const volatile uint32_t* f = ready + e / kIoChunk;
+    uint32_t ns = 64;
+    while (ld_acquire_sys(f) != stamp) {
+      __nanosleep(ns);
+      if (ns < 2048) ns <<= 1;
+    }
+  }
+  __syncwarp();
+}
+
 // ------------------------------------------------------------------------------ S6
 // Warp per fill entry: first the victim row (old slot content) to the pinned host queue
 // (eviction D2H), then the new row from the backing table (zero-copy over PCIe,
@@ -914,15 +970,17 @@ __global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, c
 template <int UNROLL>
 __global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
                        const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
-                       uint32_t bounce) {
+                       uint32_t bounce, const uint32_t* io_ready, const IterState* it) {
   pdl_prologue();
   const uint32_t n = scr->nfill;
+  const uint32_t stamp = it->stamp;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t e = warp; e < n; e += nwarps) {
     const FillEnt f = fills[e];
     uint4* dst = pool + (size_t)f.dst * nvec;
     if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(hostq + (size_t)f.victim * nvec, dst, nvec);
+    if ((f.src & kHostBit) && bounce) io_wait(io_ready, e, stamp);  // file tier: row e read yet?
     if (f.src & kHostBit)
       warp_copy_row<UNROLL, kHost, kDev>(dst, table + (size_t)(bounce ? e : (f.src & ~kHostBit)) * nvec, nvec);
     else
@@ -1049,6 +1107,7 @@ struct ServeArgs {
   const uint32_t* node_loc;
   uint4* out;
   uint32_t bounce;
+  const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
   // S9, closed by the last CTA
   unsigned long long* hist;
@@ -1123,6 +1182,7 @@ __global__ void k_serve(ServeArgs a) {
       uint4* slot = a.pool + (size_t)f.dst * nvec;
       if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(a.hostq + (size_t)f.victim * nvec, slot, nvec);
       const bool from_host = (f.src & kHostBit) != 0;
+      if (from_host && a.bounce) io_wait(a.io_ready, e, stamp);  // file tier: row e read yet?
       // host row: the backing table's row q, or (file tier) bounce-buffer row e
       const uint4* src = from_host ? a.table + (size_t)(a.bounce ? e : (f.src & ~kHostBit)) * nvec
                                    : a.pool + (size_t)f.src * nvec;

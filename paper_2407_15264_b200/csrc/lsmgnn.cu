@@ -48,9 +48,11 @@ struct Handle {  // exported per rank for lsmgnn_connect
 };
 
 // Persistent worker threads of the file tier (N2): started when a storage file is attached,
-// parked on a condition variable between batches. run(n, fn) hands entries 0..n-1 out in
-// chunks of 64 through an atomic cursor to the workers and the calling thread; it returns
-// the first nonzero fn result (an errno), after which the remaining entries are skipped.
+// parked on a condition variable between batches. run(n, fn, done) hands entries 0..n-1 out in
+// chunks of kIoChunk through an atomic cursor to the workers and the calling thread and calls
+// done(chunk) once a chunk's entries are processed (the device waits on those per-chunk flags);
+// it returns the first nonzero fn result (an errno), after which the remaining entries are
+// skipped — but every chunk is still marked done, so no device wait is left hanging.
 class IoPool {
  public:
   void start(int nthreads) {
@@ -65,11 +67,12 @@ class IoPool {
     for (auto& t : th_) t.join();
     th_.clear();
   }
-  int run(uint32_t n, const std::function<int(uint32_t)>& fn) {
+  int run(uint32_t n, const std::function<int(uint32_t)>& fn, const std::function<void(uint32_t)>& done) {
     {
       std::lock_guard<std::mutex> lk(mu_);
       n_ = n;
       fn_ = &fn;
+      done_ = &done;
       next_.store(0);
       err_.store(0);
       active_ = (int)th_.size();
@@ -86,15 +89,15 @@ class IoPool {
  private:
   void drain() {
     for (;;) {
-      const uint32_t e0 = next_.fetch_add(64);
-      if (e0 >= n_ || err_.load()) return;
-      const uint32_t e1 = std::min(n_, e0 + 64);
-      for (uint32_t e = e0; e < e1; ++e)
+      const uint32_t e0 = next_.fetch_add(kIoChunk);
+      if (e0 >= n_) return;
+      const uint32_t e1 = std::min(n_, e0 + kIoChunk);
+      for (uint32_t e = e0; e < e1 && !err_.load(); ++e)
         if (int rc = (*fn_)(e)) {
           int zero = 0;
           err_.compare_exchange_strong(zero, rc);
-          return;
         }
+      (*done_)(e0 / kIoChunk);
     }
   }
   void worker() {
@@ -119,6 +122,7 @@ class IoPool {
   int active_ = 0;
   uint32_t n_ = 0;
   const std::function<int(uint32_t)>* fn_ = nullptr;
+  const std::function<void(uint32_t)>* done_ = nullptr;
   std::atomic<uint32_t> next_{0};
   std::atomic<int> err_{0};
 };
@@ -187,8 +191,12 @@ struct Ctx {
   int file_fd = -1;
   bool file_direct = false;
   uint8_t* bounce_host = nullptr;
-  FillEnt* fills_host = nullptr;  // pinned copy of the fill list
-  uint32_t* nfill_host = nullptr;
+  IoShared* io_host = nullptr;     // pinned, mapped: the published fill list and per-chunk ready flags
+  IoShared* io_dev = nullptr;      // its device mapping
+  uint32_t* io_ready_host = nullptr;
+  uint32_t* io_ready_dev = nullptr;
+  uint32_t* io_src_host = nullptr;
+  uint32_t* io_src_dev = nullptr;
   IoPool* io = nullptr;  // persistent pread workers (io_threads - 1; the caller is one more)
   int io_threads = 64;  // pread workers per batch (LSMGNN_IO_THREADS); deeper queues help NVMe
   volatile uint32_t* bad_host = nullptr;  // pinned mirror: [0] scr->bad_ids, [1] batch-length overflow
@@ -206,6 +214,10 @@ struct Ctx {
   // peer on its own GPU runs both phases after "served". LSMGNN_SPLIT_PULL=0/1 overrides.
   bool split_pull = true;
   bool pdl = false;  // programmatic dependent launch on the G = 1 chain (launch_pdl)
+  // LSMGNN_G1_PULL=1 (G = 1, profiling aid): the G > 1 serve path — k_fill, then k_pull phase 0
+  // (rows in place) and phase 1 (rows filled this batch), then k_end — instead of the fused
+  // k_serve; the pull kernels can then be profiled on one process (local HBM instead of peers)
+  bool g1_pull = false;
   // k_serve geometry: CTAs per SM and TMA row stages per warp (0 = 16-B vector copies);
   // LSMGNN_SERVE_CPS / LSMGNN_SERVE_ST override (A/B runs)
   int serve_cps = 2, serve_st = 3;
@@ -549,7 +561,8 @@ BeginArgs begin_args(int64_t t_host, const int64_t* ids, int64_t n, const int64_
   return a;
 }
 
-int read_storage_rows(cudaStream_t st);  // file tier (below)
+int io_export(cudaStream_t st);                     // file tier (below)
+int read_storage_rows(uint32_t stamp, cudaStream_t st);
 
 // Kernel launch with programmatic dependent launch (PDL) on the single-home step chain: the
 // next kernel is scheduled while its predecessor drains and waits in pdl_prologue() for its
@@ -703,11 +716,11 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   uint4* o4 = reinterpret_cast<uint4*>(out);
   const bool wide = g.nvec >= 256;
   const uint32_t bounce = g.file_fd >= 0 ? 1u : 0u;  // file tier: storage rows staged per fill entry
-  if (G == 1) {
+  if (G == 1 && !g.g1_pull) {
     // one fused launch: fills deliver their rows to `out`, 1 warp in 8 copies the hits; its last
     // CTA closes the record (S9)
     prof_begin(4, st);
-    if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
+    if (bounce && (rc_io = io_export(st))) return rc_io;
     ServeArgs sa{};
     sa.fills = g.fills;
     sa.scr = g.scr;
@@ -722,6 +735,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.node_loc = loc_of(g.arena);
     sa.out = o4;
     sa.bounce = bounce;
+    sa.io_ready = g.io_ready_dev;
     sa.hist = g.hist;
     sa.cum = g.cum;
     sa.bad_mirror = g.bad_dev;
@@ -738,13 +752,15 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     else SERVE(2, kHost, 0);
 #undef SERVE
     LAUNCHED();
+    if (bounce && (rc_io = read_storage_rows(stamp_host, st))) return rc_io;
     prof_end(4, st);
     prof_begin(5, st);
   } else {
     // Pull phase 0 (S7/S8 for the rows already in place): once every home has run k_set
     // ("located"), copy hit and staged rows from local / peer HBM on pull_st while this
     // home's k_fill streams the misses over PCIe.
-    if (int rc = flags_write_all(st, (uint32_t)(4 * G + g.rank), stamp_host)) return rc;
+    if (G > 1)
+      if (int rc = flags_write_all(st, (uint32_t)(4 * G + g.rank), stamp_host)) return rc;
     PullArgs pa{};
     for (int h = 0; h < G; ++h) {
       pa.pool[h] = reinterpret_cast<const uint4*>(pool_of(g.peer_arena[h]));
@@ -774,21 +790,24 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       CK(cudaEventRecord(g.ev_pull0, g.pull_st));
     }
     prof_begin(4, st);
-    if (bounce && (rc_io = read_storage_rows(st))) return rc_io;
+    if (bounce && (rc_io = io_export(st))) return rc_io;
     // 2 CTAs per SM: the PCIe-bound fill saturates the link from 1 CTA/SM
     // (profiles/r01_pcie_microbench.txt) and leaves room on every SM for pull phase 0
     const int blocks = g.sms * std::min(2, g.geom_per_sm);
     if (wide)
-      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce);
+      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce, g.io_ready_dev, g.it);
     else
-      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce);
+      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce, g.io_ready_dev, g.it);
     LAUNCHED();
+    if (bounce && (rc_io = read_storage_rows(stamp_host, st))) return rc_io;
     prof_end(4, st);
     // homes signal "served", requesters wait for every home, then pull the filled rows
     // (phase 1); the gather ends after both phases
     prof_begin(5, st);
-    if (int rc = flags_write_all(st, (uint32_t)(G + g.rank), stamp_host)) return rc;
-    if (int rc = flags_wait_all(st, &flags_of(g.arena)[G], stamp_host)) return rc;
+    if (G > 1) {
+      if (int rc = flags_write_all(st, (uint32_t)(G + g.rank), stamp_host)) return rc;
+      if (int rc = flags_wait_all(st, &flags_of(g.arena)[G], stamp_host)) return rc;
+    }
     if (n_bound > 0) {
       if (g.split_pull) {
         CK(cudaStreamWaitEvent(st, g.ev_pull0, 0));
@@ -802,7 +821,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
 #undef PULL
   }
   prof_end(5, st);
-  if (G > 1) {
+  if (G > 1 || g.g1_pull) {
     EndArgs ea{g.it, g.hist, g.cum, g.scr, g.R, g.bad_dev};
     KLAUNCH(k_end, 1, 32, 0, st, ea);
     LAUNCHED();
@@ -952,11 +971,10 @@ void detach_file() {
   if (g.file_fd >= 0) close(g.file_fd);
   g.file_fd = -1;
   if (g.bounce_host) cudaFreeHost(g.bounce_host);
-  if (g.fills_host) cudaFreeHost(g.fills_host);
-  if (g.nfill_host) cudaFreeHost(g.nfill_host);
+  if (g.io_host) cudaFreeHost(g.io_host);
   g.bounce_host = nullptr;
-  g.fills_host = nullptr;
-  g.nfill_host = nullptr;
+  g.io_host = nullptr;
+  g.io_dev = nullptr;
   g.table_dev = nullptr;
 }
 int attach_file(const char* path, uint64_t rows) {
@@ -975,9 +993,19 @@ int attach_file(const char* path, uint64_t rows) {
   // fills per batch <= unique nodes per batch at this home (installs + bypassed misses)
   CK(cudaHostAlloc(reinterpret_cast<void**>(&g.bounce_host), std::max<uint64_t>(1, g.ucap) * g.R,
                    cudaHostAllocMapped | cudaHostAllocPortable));
-  CK(cudaHostAlloc(reinterpret_cast<void**>(&g.fills_host), std::max<uint64_t>(1, g.ucap) * sizeof(FillEnt),
-                   cudaHostAllocDefault));
-  CK(cudaHostAlloc(reinterpret_cast<void**>(&g.nfill_host), sizeof(uint32_t), cudaHostAllocDefault));
+  {  // [IoShared | ready[chunks] | src[ucap]], zeroed (stamps start at 1)
+    const uint64_t chunks = (std::max<uint64_t>(1, g.ucap) + kIoChunk - 1) / kIoChunk;
+    const size_t bytes = sizeof(IoShared) + 4 * chunks + 4 * std::max<uint64_t>(1, g.ucap);
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&g.io_host), bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    std::memset(g.io_host, 0, bytes);
+    void* d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, g.io_host, 0));
+    g.io_dev = reinterpret_cast<IoShared*>(d);
+    g.io_ready_host = reinterpret_cast<uint32_t*>(g.io_host + 1);
+    g.io_ready_dev = reinterpret_cast<uint32_t*>(g.io_dev + 1);
+    g.io_src_host = g.io_ready_host + chunks;
+    g.io_src_dev = g.io_ready_dev + chunks;
+  }
   void* dp = nullptr;
   CK(cudaHostGetDevicePointer(&dp, g.bounce_host, 0));
   g.table_dev = reinterpret_cast<const uint8_t*>(dp);
@@ -987,21 +1015,38 @@ int attach_file(const char* path, uint64_t rows) {
   g.io->start(g.io_threads - 1);
   return 0;
 }
-// Read the storage rows of this batch's fills into the bounce buffer (row e = fill e).
-// Synchronises `st` (the fill list is decided on the device by k_set).
-int read_storage_rows(cudaStream_t st) {
-  CK(cudaMemcpyAsync(g.nfill_host, &g.scr->nfill, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  const uint32_t n = *g.nfill_host;
+// File tier, step 1 (stream-ordered, before the fill kernel): publish this batch's fill list to
+// pinned host memory (k_io_export).
+int io_export(cudaStream_t st) {
+  KLAUNCH(k_io_export, grid_for((int64_t)g.ucap, 256, 2), 256, 0, st, (const FillEnt*)g.fills, g.scr,
+          (const IterState*)g.it, g.io_dev, g.io_src_dev);
+  LAUNCHED();
+  return 0;
+}
+// File tier, step 2 (host, after the fill kernel was launched): wait until the list of batch
+// `stamp` is published, then read its storage rows into the bounce buffer (row e = entry e) with
+// the pread workers, releasing each chunk of kIoChunk entries to the waiting fill kernel as soon
+// as it is read. Every chunk is released even after a read error (the rows are then garbage and
+// the error is sticky), so the device never waits forever. No stream synchronisation.
+int read_storage_rows(uint32_t stamp, cudaStream_t st) {
+  volatile uint32_t* list = &g.io_host->list;
+  for (uint64_t spin = 0; *list != stamp; ++spin) {
+    if ((spin & 1023) == 1023) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q != cudaErrorNotReady && q != cudaSuccess)
+        return set_err(LSMGNN_ECUDA, "stream failed before the fill list was published: %s", cudaGetErrorString(q));
+      std::this_thread::yield();
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  const uint32_t n = *(volatile uint32_t*)&g.io_host->n;
   if (n == 0) return 0;
-  CK(cudaMemcpyAsync(g.fills_host, g.fills, (size_t)n * sizeof(FillEnt), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
   const uint64_t R = g.R;
   const std::function<int(uint32_t)> read_one = [R](uint32_t e) -> int {
-    const FillEnt f = g.fills_host[e];
-    if (!(f.src & kHostBit)) return 0;  // PVP staging row: already in HBM
+    const uint32_t q = g.io_src_host[e];
+    if (q == kInvalid) return 0;  // PVP staging row: already in HBM
     uint8_t* dst = g.bounce_host + (size_t)e * R;
-    const off_t off = (off_t)(f.src & ~kHostBit) * (off_t)R;
+    const off_t off = (off_t)q * (off_t)R;
     size_t done = 0;
     while (done < R) {
       const ssize_t r = pread(g.file_fd, dst + done, R - done, off + (off_t)done);
@@ -1011,7 +1056,11 @@ int read_storage_rows(cudaStream_t st) {
     }
     return 0;
   };
-  const int err = g.io->run(n, read_one);
+  const std::function<void(uint32_t)> release = [stamp](uint32_t c) {
+    std::atomic_thread_fence(std::memory_order_release);  // the chunk's rows before its flag
+    reinterpret_cast<std::atomic<uint32_t>*>(&g.io_ready_host[c])->store(stamp, std::memory_order_release);
+  };
+  const int err = g.io->run(n, read_one, release);
   if (err) {  // the cache already holds tags for rows that never arrived: sticky
     g.sticky = LSMGNN_EIO;
     return set_err(LSMGNN_EIO, "storage read failed: %s", std::strerror(err));
@@ -1272,6 +1321,8 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     }
   }
   g.pdl = G == 1 && !std::getenv("LSMGNN_NO_PDL");
+  g.g1_pull = G == 1 && std::getenv("LSMGNN_G1_PULL") && std::atoi(std::getenv("LSMGNN_G1_PULL")) != 0;
+  if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g.ev_set, cudaEventDisableTiming));

@@ -470,3 +470,33 @@ def test_full_row_width_pvp_unused():
     compare(hg, ho, "pvp_unused 4KiB")
     assert ho[:, F["pvp_unused"]].sum() > 0 and ho[:, F["victim_hits"]].sum() > 0
 
+
+@pytest.mark.parametrize("D", [128, 1024])
+@pytest.mark.parametrize("st", ["0", "3"])
+def test_g1_pull_path(cfg1_g1, monkeypatch, D, st):
+    """LSMGNN_G1_PULL=1 (the profiling aid) runs the G > 1 serve path on one home — k_fill, then
+    k_pull phase 0 (rows in place) and phase 1 (rows filled this batch), k_end — with TMA rings
+    (st = 3) or 16-B vector copies (st = 0): same rows and counters as the oracle."""
+    monkeypatch.setenv("LSMGNN_G1_PULL", "1")
+    monkeypatch.setenv("LSMGNN_SERVE_ST", st)
+    g, tr, sc = cfg1_g1
+    kw = dict(N=16384, D=D, L=1024, A=8, scores=sc, policy="hybrid", pvp=1, W=8, V=512)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"g1 pull D{D} st{st}")
+
+
+@pytest.mark.parametrize("st", ["0", "2", "8"])
+def test_serve_geometry(cfg1_g1, monkeypatch, st):
+    """k_serve's delivery with TMA rings of 2 or 8 stages per warp and with 16-B vector copies
+    (LSMGNN_SERVE_ST) at 4 KiB rows: identical rows and counters (I9 for the serve geometry)."""
+    monkeypatch.setenv("LSMGNN_SERVE_ST", st)
+    monkeypatch.setenv("LSMGNN_SERVE_CPS", "1")
+    g, tr, sc = cfg1_g1
+    kw = dict(N=16384, D=1024, L=1024, A=8, scores=sc, policy="lru", pvp=0, W=8)
+    hg, _, bad = run_gpu(tr, **kw)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"serve st{st}")
+
