@@ -72,6 +72,7 @@ __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, B
     scr->nbypass = 0;
     scr->nreq = 0;
     scr->pull_next = 0;
+    scr->nslow = 0;
   }
 }
 
@@ -224,22 +225,9 @@ __global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
 // S10 (window): the same launch drops the reuse bits of iteration t (ring slot t mod (W+1)):
 // gather(t) reads iterations t+1..t+W only, and gather(t-1), the last reader of those bits,
 // has completed; the feed of t+1+W (which rewrites the slot) is ordered after this kernel.
-__device__ __forceinline__ bool dedup_one(uint32_t v, uint32_t pos, uint32_t G, uint32_t S, uint32_t BC, uint32_t stamp,
-                                          uint32_t* __restrict__ mark, uint32_t* __restrict__ set_cnt,
-                                          uint32_t* __restrict__ bucket, unsigned long long* __restrict__ head,
-                                          uint32_t* __restrict__ nxt) {
-  const uint32_t q = v / G;
-  const bool first = atomicExch(&mark[q], stamp) != stamp;
-  if (first) {
-    const uint32_t s = q % S;
-    bucket[(size_t)s * BC + atomicAdd(&set_cnt[s], 1u)] = v;
-  }
-  if (head) {
-    const unsigned long long old = atomicExch(&head[q], ((unsigned long long)stamp << 32) | pos);
-    nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
-  }
-  return first;
-}
+struct DedupArgs;
+__device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, uint32_t stamp,
+                                              uint32_t t, uint32_t* nhit);
 struct DedupArgs {
   const uint32_t* inbox;
   const uint32_t* inbox_cnt;
@@ -257,7 +245,57 @@ struct DedupArgs {
   const uint32_t* ring_len;
   uint32_t* mask;
   uint32_t MW, Wp1;
+  // S4 hit probe of every distinct node (the cache state is final: the previous k_serve is done):
+  // a hit writes node_loc and the way's last use (hits are protected, R10) and is counted here;
+  // a node that is not resident marks its set for k_set (slow_stamp[s] = stamp)
+  const uint32_t* tags;
+  uint32_t* last_use;
+  uint32_t* node_loc;
+  uint32_t* slow_stamp;
+  uint32_t* slow_list;  // the sets with a miss this batch (count scr->nslow)
+  Scratch* scr;
+  uint32_t A;
 };
+// One request: first occurrence of its node (returns 1) -> into the set's bucket, probed.
+__device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, uint32_t stamp,
+                                              uint32_t t, uint32_t* nhit) {
+  const uint32_t q = v / a.G;
+  const bool first = atomicExch(&a.mark[q], stamp) != stamp;
+  if (a.head) {
+    const unsigned long long old = atomicExch(&a.head[q], ((unsigned long long)stamp << 32) | pos);
+    a.nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
+  }
+  if (!first) return 0;
+  const uint32_t s = q % a.S;
+  a.bucket[(size_t)s * a.BC + atomicAdd(&a.set_cnt[s], 1u)] = v;
+  // probe the set's A ways (one round trip: independent loads)
+  const uint32_t* tg = a.tags + (size_t)s * a.A;
+  int way = -1;
+  if (a.A == 32) {
+    const uint4* t4 = reinterpret_cast<const uint4*>(tg);
+    uint4 w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = t4[i];
+#pragma unroll
+    for (int i = 7; i >= 0; --i) {
+      if (w[i].w == v) way = 4 * i + 3;
+      if (w[i].z == v) way = 4 * i + 2;
+      if (w[i].y == v) way = 4 * i + 1;
+      if (w[i].x == v) way = 4 * i;
+    }
+  } else {
+    for (uint32_t k = 0; k < a.A; ++k)
+      if (tg[k] == v) way = (int)k;
+  }
+  if (way >= 0) {
+    a.node_loc[q] = s * a.A + (uint32_t)way;
+    a.last_use[s * a.A + (uint32_t)way] = t;
+    ++*nhit;
+  } else if (a.slow_stamp[s] != stamp && atomicExch(&a.slow_stamp[s], stamp) != stamp) {
+    a.slow_list[atomicAdd(&a.scr->nslow, 1u)] = s;  // first miss of the set: k_set processes it
+  }
+  return 1;
+}
 __global__ void k_dedup(DedupArgs a, const IterState* it, Scratch* scr, unsigned long long* hist) {
   pdl_prologue();
   const uint32_t stamp = it->stamp;
@@ -273,15 +311,15 @@ __global__ void k_dedup(DedupArgs a, const IterState* it, Scratch* scr, unsigned
       if (v != kInvalid) atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
     }
   }
-  uint32_t nreq = 0, npeer = 0, nfirst = 0;
+  uint32_t nreq = 0, npeer = 0, nfirst = 0, nhit = 0;
+  const uint32_t t = (uint32_t)it->t;
   if (a.direct) {
     const int64_t* __restrict__ ids = it->ids;
     const int64_t n = it->n;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
       const int64_t x = ids[i];
       if (x >= 0 && (uint64_t)x < a.N) {
-        nfirst += dedup_one((uint32_t)x, (uint32_t)i, a.G, a.S, a.BC, stamp, a.mark, a.set_cnt, a.bucket, a.head,
-                            a.nxt);
+        nfirst += dedup_one((uint32_t)x, (uint32_t)i, a, stamp, t, &nhit);
         ++nreq;
       } else {
         atomicAdd(&scr->bad_ids, 1u);
@@ -292,7 +330,7 @@ __global__ void k_dedup(DedupArgs a, const IterState* it, Scratch* scr, unsigned
       const uint32_t n = a.inbox_cnt[r];
       const uint32_t* in = a.inbox + (size_t)r * a.cap;
       for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        nfirst += dedup_one(in[i], i, a.G, a.S, a.BC, stamp, a.mark, a.set_cnt, a.bucket, a.head, a.nxt);
+        nfirst += dedup_one(in[i], i, a, stamp, t, &nhit);
         ++nreq;
         if (r != a.me) ++npeer;
       }
@@ -301,9 +339,11 @@ __global__ void k_dedup(DedupArgs a, const IterState* it, Scratch* scr, unsigned
   nreq = __reduce_add_sync(0xffffffffu, nreq);
   npeer = __reduce_add_sync(0xffffffffu, npeer);
   nfirst = __reduce_add_sync(0xffffffffu, nfirst);
+  nhit = __reduce_add_sync(0xffffffffu, nhit);
   if (lane_id() == 0) {
     if (nreq) atomicAdd(&scr->nreq, nreq);
     if (nfirst) atomicAdd(&scr->nuniq, nfirst);
+    if (nhit) atomicAdd(&rec[F_HIT], (unsigned long long)nhit);
     if (npeer) atomicAdd(&rec[F_PEER], (unsigned long long)npeer);
   }
 }
@@ -421,6 +461,8 @@ __global__ void k_snapshot(const uint32_t* __restrict__ tags, uint32_t L, uint32
 // ------------------------------------------------------------------------------ S4 + S5
 struct SetParams {
   uint32_t* set_cnt;     // distinct nodes per set this batch (k_dedup); k_set resets it to 0
+  const uint32_t* slow_stamp;  // == stamp: a node of the set missed in k_dedup's probe
+  const uint32_t* slow_list;   // those sets (count scr->nslow)
   const uint32_t* bucket;  // set s's nodes at bucket[s * BC, + set_cnt[s])
   uint32_t BC, BCp;      // bucket capacity per set; global-scratch region per oversized set (pow2 >= BC)
   uint32_t* tags;
@@ -495,7 +537,7 @@ __device__ __forceinline__ uint64_t policy_key(const SetParams& p, uint32_t v, u
   }
 }
 
-__global__ void k_set(SetParams p) {
+__global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
   pdl_prologue();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_ctr[C_N];
@@ -534,11 +576,19 @@ __global__ void k_set(SetParams p) {
     if (lane == 0 && unused) atomicAdd(&rec_[F_UNUSED], (unsigned long long)unused);
   }
 
-  for (uint32_t s = blockIdx.x * nwb + wib; s < p.S; s += gridDim.x * nwb) {
-    // one round trip for the set: its node count, its first 32 bucket entries (the bucket array
-    // is padded by 32 entries) and its resident lines (lane w holds way w)
-    const uint32_t* bk = p.bucket + (size_t)s * p.BC;
+  // A set whose nodes all hit was fully handled by k_dedup's probe (node_loc, last use, hit
+  // count): its counter is only reset here (sets scanned 32 per warp iteration, lane = set).
+  // The sets with a miss (k_dedup's slow list) are processed by one warp each.
+  const uint32_t gwarp = blockIdx.x * nwb + wib, nwarps = gridDim.x * nwb;
+  for (uint32_t sl = gwarp * 32 + lane; sl < p.S; sl += nwarps * 32)
+    if (p.set_cnt[sl] && p.slow_stamp[sl] != stamp_) p.set_cnt[sl] = 0;  // ready for the next batch
+  const uint32_t nslow = p.scr->nslow;
+  for (uint32_t i = gwarp; i < nslow; i += nwarps) {
+    const uint32_t s = p.slow_list[i];
     uint32_t m = lane == 0 ? p.set_cnt[s] : 0u;
+    // one round trip for the set: its first 32 bucket entries (the bucket array is padded by 32
+    // entries) and its resident lines (lane w holds way w)
+    const uint32_t* bk = p.bucket + (size_t)s * p.BC;
     const uint32_t b0 = bk[lane];
     uint32_t tg = kInvalid, lu = 0;
     if (lane < A) {
@@ -546,29 +596,9 @@ __global__ void k_set(SetParams p) {
       lu = p.last_use[s * A + lane];
     }
     m = __shfl_sync(0xffffffffu, m, 0);
-    if (m == 0) continue;
     if (lane == 0) p.set_cnt[s] = 0;  // ready for the next batch
     stag[lane] = tg;
     __syncwarp();
-    if (m <= 32) {  // fast path: every node of the bucket is resident (no miss, no replacement)
-      const uint32_t v = lane < m ? b0 : kInvalid;
-      int way = -1;
-      if (lane < m)
-        for (uint32_t w = 0; w < A; ++w)
-          if (stag[w] == v) way = (int)w;
-      if (__all_sync(0xffffffffu, lane >= m || way >= 0)) {
-        uint32_t pm = 0;
-        if (lane < m) {
-          p.node_loc[v / G] = s * A + (uint32_t)way;
-          ++ctr[C_HIT];
-          pm = 1u << way;
-        }
-        pm = __reduce_or_sync(0xffffffffu, pm);
-        if ((pm >> lane) & 1u) p.last_use[s * A + lane] = t_;
-        __syncwarp();
-        continue;
-      }
-    }
     uint32_t Pm = 32;
     while (Pm < m) Pm <<= 1;
     // a bucket larger than the warp's shared-memory capacity works in its own power-of-two
@@ -599,11 +629,9 @@ __global__ void k_set(SetParams p) {
         for (uint32_t w = 0; w < A; ++w)
           if (stag[w] == v) way = (int)w;
         uint32_t kind, inM;
-        if (way >= 0) {
+        if (way >= 0) {  // (node_loc and the hit count were written by k_dedup's probe)
           kind = kHit;
           protm |= 1u << way;
-          p.node_loc[q] = s * A + (uint32_t)way;
-          ++ctr[C_HIT];
         } else if (p.vst_stamp[q] == stamp_) {
           kind = kVHit;
           ++ctr[C_VHIT];

@@ -155,6 +155,8 @@ struct Ctx {
   // local device state
   uint32_t *tags = nullptr, *last_use = nullptr, *rr = nullptr, *mask = nullptr, *mark = nullptr;
   uint32_t *vst_stamp = nullptr, *vst_idx = nullptr, *set_cnt = nullptr;
+  uint32_t* slow_stamp = nullptr;  // [S]: == stamp when a node of the set missed k_dedup's probe
+  uint32_t* slow_list = nullptr;   // [S]: those sets, in k_dedup's order
   uint32_t *bucket = nullptr, *ring = nullptr, *ring_len = nullptr;  // bucket: [S * BC + 32]
   // global scratch for cache sets whose bucket exceeds k_set's shared-memory capacity
   uint32_t *g_sv = nullptr, *g_sk = nullptr, *g_sidx = nullptr;  // [S * BCp] when a set can exceed P
@@ -475,7 +477,7 @@ void prof_end(int ph, cudaStream_t st) {
 void detach_file();  // file tier (below)
 int free_all() {
   cudaDeviceSynchronize();
-  void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.scan_q,
+  void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.slow_stamp, g.slow_list, g.scan_q,
                   g.bucket, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
                   g.stg_nodes, g.route_cnt, g.head, g.nxt, g.line_info, g.score, g.fills, g.cands,
                   g.scr, g.it, g.hist, g.g_sv, g.g_sk, g.g_sidx, g.g_skey,
@@ -633,6 +635,13 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.mask = g.mask;
     da.MW = g.MW;
     da.Wp1 = g.Wp1;
+    da.tags = g.tags;
+    da.last_use = g.last_use;
+    da.node_loc = loc_of(g.arena);
+    da.slow_stamp = g.slow_stamp;
+    da.slow_list = g.slow_list;
+    da.scr = g.scr;
+    da.A = g.A;
     KLAUNCH(k_dedup, grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st, da,
             (const IterState*)g.it, g.scr, g.hist);
     LAUNCHED();
@@ -643,6 +652,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   prof_begin(2, st);
   SetParams sp{};
   sp.set_cnt = g.set_cnt;
+  sp.slow_stamp = g.slow_stamp;
+  sp.slow_list = g.slow_list;
   sp.bucket = g.bucket;
   sp.BC = (uint32_t)g.BC;
   sp.BCp = (uint32_t)g.BCp;
@@ -1238,6 +1249,8 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   DA(g.vst_idx, g.Q);
   DA(g.set_cnt, g.S);
   DA(g.scan_q, 2 * (size_t)scan_tiles(g.W));
+  DA(g.slow_stamp, g.S);
+  DA(g.slow_list, g.S);
   if (big_sets) {  // a power-of-two region of global scratch per set that can exceed P
     DA(g.g_sv, g.S * g.BCp + 64);
     DA(g.g_sk, g.S * g.BCp + 64);
@@ -1310,6 +1323,8 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     if (!g.serve_st && (uint64_t)8 * 2 * g.R <= budget) g.serve_st = 2;
     if (const char* e = std::getenv("LSMGNN_SERVE_CPS")) g.serve_cps = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("LSMGNN_SERVE_ST")) g.serve_st = std::max(0, std::min((int)kMaxStages, std::atoi(e)));
+    // the rings of 8 warps must fit one CTA's shared memory (227 KB on sm_100)
+    while (g.serve_st > 0 && (uint64_t)8 * g.serve_st * g.R > 220 * 1024) --g.serve_st;
     if (g.serve_st) {
       const int smem = (int)((size_t)8 * g.serve_st * g.R);
       CK(cudaFuncSetAttribute(k_serve<8, kDev, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
