@@ -283,8 +283,12 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 
 // A warp's ring of ST row stages in shared memory, driven by its lane 0: rows are loaded with
 // cp.async.bulk (global -> shared, completion on the stage's mbarrier) and stored with
-// cp.async.bulk (shared -> global, bulk groups), up to ST - 1 loads in flight behind the store
-// being issued. The counters run across calls so that stage phases stay consistent.
+// cp.async.bulk (shared -> global, bulk groups). At most ST - 1 loads are in flight, so the stage
+// a new load reuses is the one stored one step EARLIER: its store has (almost always) finished
+// reading shared memory, and the store just issued may still be reading (wait_group.read 1).
+// (Reloading the stage just stored would wait for every store to drain: measured as the top
+// stall of the first version, profiles/r02_ncu_hit.md.) Counters run across calls so that the
+// stage phases stay consistent.
 constexpr uint32_t kMaxStages = 8;
 struct RowRing {
   uint8_t* buf;    // ST * R bytes of this warp's shared memory
@@ -305,7 +309,7 @@ __device__ __forceinline__ void ring_copy(RowRing& r, const void* const* src, vo
   const uint32_t total = __popc(mask);
   uint32_t issued = 0, stored = 0;
   while (stored < total) {
-    while (issued < total && r.nl - r.ns < r.ST) {
+    while (issued < total && r.nl - r.ns < r.ST - 1) {
       const uint32_t j = __ffs(mask) - 1;
       mask &= mask - 1;
       const uint32_t s = r.nl % r.ST;

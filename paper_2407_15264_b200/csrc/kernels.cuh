@@ -37,43 +37,55 @@ struct BeginArgs {
   int64_t cap;                     // max_batch_ids: a longer device-resident batch is clamped ...
   volatile uint32_t* overflow;     // ... and flagged here (pinned host word, sticky EINVAL)
 };
+// The per-iteration values of gather t, from the host arguments (direct calls) or from the
+// device's own iteration counter and the caller's ring of batches (graph replay). `clamped` is
+// set when a device-resident length exceeded max_batch_ids.
+struct IterVals {
+  uint64_t t;
+  const int64_t* ids;
+  int64_t n;
+  bool clamped;
+};
+__device__ __forceinline__ IterVals begin_values(const BeginArgs& a, const IterState* it) {
+  IterVals v;
+  v.t = a.t_host >= 0 ? (uint64_t)a.t_host : it->t_next;
+  v.clamped = false;
+  if (a.t_host >= 0) {
+    v.ids = a.ids_host;
+    v.n = a.n_host;
+  } else {
+    const uint32_t k = (uint32_t)(v.t % a.ring_len);
+    v.ids = a.ids_ring[k];
+    v.n = a.n_ring[k];
+    if (v.n > a.cap || v.n < 0) {
+      v.n = v.n < 0 ? 0 : a.cap;
+      v.clamped = true;
+    }
+  }
+  return v;
+}
+// Publish them in IterState for the kernels that follow (one thread).
+__device__ __forceinline__ void begin_publish(const BeginArgs& a, const IterVals& v, IterState* it,
+                                              unsigned long long* hist) {
+  const uint64_t t = v.t;
+  it->t = t;
+  it->ids = v.ids;
+  it->n = v.n;
+  if (v.clamped) *a.overflow = 1u;
+  it->stamp = (uint32_t)(t + 1);
+  it->p0 = (uint32_t)((t + 1) % a.Wp1);
+  it->par = (uint32_t)(t & 1);
+  it->upd = a.period <= 1 || t % a.period == 0;
+  it->rec_idx = (uint32_t)(t % kHist);
+  it->stage_base = a.L + (uint32_t)(t & 1) * a.C;
+  hist[(size_t)(t % kHist) * F_NFIELDS + F_ITER] = t;
+}
+// G > 1 (the route kernels read the batch before k_dedup runs): publish the iteration's values.
+// The record of t and the per-batch scratch counters were zeroed by end_record of t - 1 (and
+// by allocation before the first gather); at G = 1 k_dedup publishes them itself.
 __global__ void k_begin(IterState* it, unsigned long long* hist, Scratch* scr, BeginArgs a) {
   pdl_prologue();
-  const uint64_t t = a.t_host >= 0 ? (uint64_t)a.t_host : it->t_next;
-  unsigned long long* rec = hist + (size_t)(t % kHist) * F_NFIELDS;
-  const int i = threadIdx.x;
-  if (i < F_NFIELDS) rec[i] = 0;
-  __syncthreads();
-  if (i == 0) {
-    it->t = t;
-    if (a.t_host >= 0) {
-      it->ids = a.ids_host;
-      it->n = a.n_host;
-    } else {
-      const uint32_t k = (uint32_t)(t % a.ring_len);
-      it->ids = a.ids_ring[k];
-      it->n = a.n_ring[k];
-      if (it->n > a.cap || it->n < 0) {
-        it->n = it->n < 0 ? 0 : a.cap;
-        *a.overflow = 1u;
-      }
-    }
-    it->stamp = (uint32_t)(t + 1);
-    it->p0 = (uint32_t)((t + 1) % a.Wp1);
-    it->par = (uint32_t)(t & 1);
-    it->upd = a.period <= 1 || t % a.period == 0;
-    it->rec_idx = (uint32_t)(t % kHist);
-    it->stage_base = a.L + (uint32_t)(t & 1) * a.C;
-    rec[F_ITER] = t;
-    rec[F_PREF] = scr->staged[t & 1];
-    scr->nuniq = 0;
-    scr->nfill = 0;
-    scr->ncand = 0;
-    scr->nbypass = 0;
-    scr->nreq = 0;
-    scr->pull_next = 0;
-    scr->nslow = 0;
-  }
+  if (threadIdx.x == 0) begin_publish(a, begin_values(a, it), it, hist);
 }
 
 // Close the record (G > 1, after the pulls; at G = 1 the last CTA of k_serve does it):
@@ -296,13 +308,30 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
   }
   return 1;
 }
-__global__ void k_dedup(DedupArgs a, const IterState* it, Scratch* scr, unsigned long long* hist) {
+// fused_begin (G = 1): the iteration's values come from `ba` (k_begin's job: no separate launch)
+// and block 0 publishes them; otherwise k_begin published them in IterState.
+__global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long long* hist, BeginArgs ba,
+                        uint32_t fused_begin) {
   pdl_prologue();
-  const uint32_t stamp = it->stamp;
-  unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
+  uint64_t t64;
+  const int64_t* ids_b;
+  int64_t n_b;
+  if (fused_begin) {
+    const IterVals v = begin_values(ba, it);
+    t64 = v.t;
+    ids_b = v.ids;
+    n_b = v.n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) begin_publish(ba, v, it, hist);
+  } else {
+    t64 = it->t;
+    ids_b = it->ids;
+    n_b = it->n;
+  }
+  const uint32_t stamp = (uint32_t)(t64 + 1);
+  unsigned long long* rec = hist + (size_t)(t64 % kHist) * F_NFIELDS;
   const uint32_t stride = gridDim.x * blockDim.x;
   {  // S10: clear the bits of iteration t (its window list is in ring slot t mod (W+1))
-    const uint32_t slot = (uint32_t)(it->t % a.Wp1);
+    const uint32_t slot = (uint32_t)(t64 % a.Wp1);
     const uint32_t* __restrict__ list = a.ring + (size_t)slot * a.ring_stride;
     const uint32_t nl = a.ring_len[slot];
     const uint32_t m = ~(1u << (slot & 31));
@@ -312,10 +341,10 @@ __global__ void k_dedup(DedupArgs a, const IterState* it, Scratch* scr, unsigned
     }
   }
   uint32_t nreq = 0, npeer = 0, nfirst = 0, nhit = 0;
-  const uint32_t t = (uint32_t)it->t;
+  const uint32_t t = (uint32_t)t64;
   if (a.direct) {
-    const int64_t* __restrict__ ids = it->ids;
-    const int64_t n = it->n;
+    const int64_t* __restrict__ ids = ids_b;
+    const int64_t n = n_b;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
       const int64_t x = ids[i];
       if (x >= 0 && (uint64_t)x < a.N) {
@@ -1152,6 +1181,7 @@ __device__ __forceinline__ void end_record(IterState* it, unsigned long long* hi
   const uint64_t t = it->t;
   unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
   if (f == 0) {
+    rec[F_PREF] = scr->staged[t & 1];  // rows the PVP staged for t (its copy completed before gather t)
     rec[F_UNIQUE] = scr->nuniq;
     rec[F_REQ] = scr->nreq;
     rec[F_BOUT] = (unsigned long long)scr->nreq * R;
@@ -1171,6 +1201,19 @@ __device__ __forceinline__ void end_record(IterState* it, unsigned long long* hi
     scr->staged[(t + 1) & 1] = 0;
     *bad_mirror = scr->bad_ids;
     it->t_next = t + 1;  // direct calls and graph replays may be mixed
+  }
+  __syncwarp();
+  // prepare gather t + 1: its record and the per-batch scratch counters start at zero
+  unsigned long long* nrec = hist + (size_t)((t + 1) % kHist) * F_NFIELDS;
+  if (f < F_NFIELDS) nrec[f] = 0;
+  if (f == 0) {
+    scr->nuniq = 0;
+    scr->nfill = 0;
+    scr->ncand = 0;
+    scr->nbypass = 0;
+    scr->nreq = 0;
+    scr->pull_next = 0;
+    scr->nslow = 0;
   }
 }
 

@@ -596,8 +596,10 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
 int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host, bool graph, uint32_t stamp_host,
                   cudaStream_t st, cudaEvent_t ev_dedup = nullptr) {
   const int G = g.world;
-  KLAUNCH(k_begin, 1, 32, 0, st, g.it, g.hist, g.scr, ba);
-  LAUNCHED();
+  if (G > 1) {  // (at G = 1 k_dedup publishes the iteration's values itself)
+    KLAUNCH(k_begin, 1, 32, 0, st, g.it, g.hist, g.scr, ba);
+    LAUNCHED();
+  }
   // ---- S1/S2 route + exchange
   prof_begin(0, st);
   const uint32_t* inbox = inbox_of(g.arena);
@@ -643,7 +645,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.scr = g.scr;
     da.A = g.A;
     KLAUNCH(k_dedup, grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st, da,
-            (const IterState*)g.it, g.scr, g.hist);
+            g.it, g.scr, g.hist, ba, G == 1 ? 1u : 0u);
     LAUNCHED();
   }
   if (ev_dedup) CK(cudaEventRecord(ev_dedup, st));  // the window feed of t+1+W may follow from here
@@ -1309,18 +1311,20 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   CK(cudaEventCreateWithFlags(&g.ev_main, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&g.ev_pvp, cudaEventDisableTiming));
   CK(cudaFuncSetAttribute(k_set, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(g.warp_bytes * g.set_warps)));
-  {  // k_serve: the most row stages per SM within ~192 KB of shared memory, 2..8 per warp
+  {  // k_serve / k_pull: the most row loads in flight per SM — (ST - 1) per warp, 8 warps per
+     // CTA, up to 3 CTAs (registers) — within ~192 KB of shared memory per SM
     const uint64_t budget = 192 * 1024;
     g.serve_cps = 1;
     g.serve_st = 0;
-    for (int cps = 3; cps >= 1 && !g.serve_st; --cps) {
+    uint64_t best = 0;
+    for (int cps = 1; cps <= 3; ++cps) {
       const uint64_t st = std::min<uint64_t>(kMaxStages, budget / ((uint64_t)cps * 8 * g.R));
-      if (st >= 2 && (uint64_t)cps * st >= 6) {
+      if (st >= 2 && (st - 1) * cps > best) {
+        best = (st - 1) * cps;
         g.serve_cps = cps;
         g.serve_st = (int)st;
       }
     }
-    if (!g.serve_st && (uint64_t)8 * 2 * g.R <= budget) g.serve_st = 2;
     if (const char* e = std::getenv("LSMGNN_SERVE_CPS")) g.serve_cps = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("LSMGNN_SERVE_ST")) g.serve_st = std::max(0, std::min((int)kMaxStages, std::atoi(e)));
     // the rings of 8 warps must fit one CTA's shared memory (227 KB on sm_100)
@@ -1563,7 +1567,8 @@ int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope) {
 
 int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
-  if (count < 0 || first < 0 || first + count > g.t_next || (g.t_next - first) > kHist)
+  // the last kHist - 1 iterations (the slot of the next one is already zeroed)
+  if (count < 0 || first < 0 || first + count > g.t_next || (g.t_next - first) > (int64_t)kHist - 1)
     return set_err(LSMGNN_EINVAL, "history range [%lld,+%lld) unavailable", (long long)first, (long long)count);
   CK(cudaDeviceSynchronize());
   // the ring [first, first+count) is at most two contiguous pieces

@@ -280,8 +280,8 @@ def test_bf16_rows():
 
 
 def test_long_run_history_wrap():
-    """6,000 iterations (the on-device history keeps the last 4,096): the cumulative counters
-    and the last 4,096 per-iteration records still equal the oracle's (stamps, rings, wraps)."""
+    """6,000 iterations (the on-device history keeps the last 4,095): the cumulative counters
+    and the last 4,095 per-iteration records still equal the oracle's (stamps, rings, wraps)."""
     import torch
     from paper_2407_15264_b200 import LsmGnn
     from .harness import table_for
@@ -301,7 +301,7 @@ def test_long_run_history_wrap():
         c.gather(ids[t], out)
         c.prefetch([ids[t + 1 + W]], first_iter=t + 1 + W)
     torch.cuda.synchronize()
-    compare(c.history(K - 4096, 4096), ho[K - 4096:], "history tail")
+    compare(c.history(K - 4095, 4095), ho[K - 4095:], "history tail")
     cum = c.stats(1)
     from paper_2407_15264_b200 import STATS_FIELDS
     for i, f in enumerate(STATS_FIELDS[1:], 1):
@@ -368,9 +368,9 @@ def test_gather_host_end_to_end(cfg1_g1, out_kind, D):
 
 def test_launch_count_and_profile(cfg1_g1):
     """lsmgnn_kernel_launches and lsmgnn_profile/_read (what bench.py's gpu_launches and phases
-    come from): a G = 1 step without PVP or periodic update is 5 kernels (begin, dedup (+ the clear
-    of the leaving window slot), set, serve (its last CTA closes the record) + the window feed's
-    route_local), and the profiled
+    come from): a G = 1 step without PVP or periodic update is 4 kernels (dedup (+ the iteration's
+    values, the clear of the leaving window slot and the hit probe), set (the sets with a miss),
+    serve (its last CTA closes the record) + the window feed's route_local), and the profiled
     phase spans cover the step's phases with non-negative times."""
     import torch
     from paper_2407_15264_b200 import LsmGnn
@@ -396,7 +396,7 @@ def test_launch_count_and_profile(cfg1_g1):
     prof = c.profile_read()
     c.profile(False)
     c.close()
-    assert n1 - n0 == 5 * steps, (n1 - n0, steps)
+    assert n1 - n0 == 4 * steps, (n1 - n0, steps)
     for ph in ("route", "dedup", "probe_replace", "fill", "window"):
         ms, cnt = prof[ph]
         assert cnt == steps and ms >= 0.0, (ph, prof[ph])
