@@ -312,20 +312,29 @@ class LsmGnn:
 class Sampler:
     """NEXT N3: GPU GraphSAGE sampler over a host-pinned CSR (lsmgnn_sampler_attach/_sample)."""
 
-    def __init__(self, indptr: np.ndarray, indices: np.ndarray):
+    def __init__(self, indptr: np.ndarray, indices: np.ndarray, pin: bool = True):
+        """pin=True copies the CSR into pinned torch tensors; pin=False hands the caller's arrays
+        (e.g. memory-mapped shared memory) to the library, which page-locks them in place."""
         import torch
         if not torch.cuda.is_available():
             raise LsmGnnError("CUDA device required")
-        L = load_library()
-        self.indptr = torch.from_numpy(np.ascontiguousarray(indptr, np.int64)).pin_memory()
-        self.indices = torch.from_numpy(np.ascontiguousarray(indices, np.int32)).pin_memory()
+        load_library()
+        if pin:
+            self.indptr = torch.from_numpy(np.ascontiguousarray(indptr, np.int64)).pin_memory()
+            self.indices = torch.from_numpy(np.ascontiguousarray(indices, np.int32)).pin_memory()
+            self._ptrs = (self.indptr.data_ptr(), self.indices.data_ptr(), self.indptr.numel() - 1,
+                          self.indices.numel())
+        else:
+            assert indptr.dtype == np.int64 and indices.dtype == np.int32
+            assert indptr.flags["C_CONTIGUOUS"] and indices.flags["C_CONTIGUOUS"]
+            self.indptr, self.indices = indptr, indices
+            self._ptrs = (indptr.ctypes.data, indices.ctypes.data, indptr.size - 1, indices.size)
         self.reattach()
 
     def reattach(self) -> None:
-        """(Re)register the pinned CSR with the library (lsmgnn_finalize forgets it)."""
-        _check(load_library().lsmgnn_sampler_attach(ctypes.c_void_p(self.indptr.data_ptr()),
-                                                    ctypes.c_void_p(self.indices.data_ptr()),
-                                                    self.indptr.numel() - 1, self.indices.numel()))
+        """(Re)register the CSR with the library (lsmgnn_finalize forgets it)."""
+        ip, ix, n, nnz = self._ptrs
+        _check(load_library().lsmgnn_sampler_attach(ctypes.c_void_p(ip), ctypes.c_void_p(ix), n, nnz))
 
     def place(self, in_hbm: bool) -> None:
         """Read the CSR from HBM (a library-owned copy) or from pinned host memory (UVA)."""

@@ -139,10 +139,18 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
 // also advances it->wk_next so that graph replays can follow); k_host < 0 (graph replay):
 // k_win_begin published them in IterState. (The gather side of S1 at G = 1 is fused into
 // k_dedup.)
+// wait_prev = 0 (the host sets it only when the library's previous launch on this stream was
+// the k_serve of gather t): no griddepcontrol.wait — the feed of iteration k = t+1+W depends on
+// nothing gather t writes (k_dedup(t) cleared its slot, and k_dedup/k_set completed before
+// k_serve(t) could trigger this launch), and the caller's IDs were produced before gather(t) (a
+// kernel or copy of the caller's in between is not a programmatic predecessor: no early start).
+// So it runs alongside k_serve(t) on the SMs k_serve leaves free; k_dedup(t+1) waits for
+// k_serve(t) itself (it->t_next).
 __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host, uint32_t Wp1,
                               uint64_t N, uint32_t* __restrict__ ring, uint64_t stride, uint32_t* __restrict__ ring_len,
-                              Scratch* scr, uint32_t* __restrict__ mask, uint32_t MW) {
-  pdl_prologue();
+                              Scratch* scr, uint32_t* __restrict__ mask, uint32_t MW, uint32_t wait_prev) {
+  if (wait_prev || k_host < 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t* __restrict__ ids;
   int64_t n;
   uint32_t slot;
@@ -168,7 +176,8 @@ __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ring_len[slot] = (uint32_t)n;
-    if (k_host >= 0) it->wk_next = (uint64_t)k_host + 1;
+    // (feeds of consecutive iterations may overlap: the latest one wins)
+    if (k_host >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&it->wk_next), (unsigned long long)k_host + 1);
   }
 }
 
@@ -312,11 +321,19 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
 // and block 0 publishes them; otherwise k_begin published them in IterState.
 __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long long* hist, BeginArgs ba,
                         uint32_t fused_begin) {
+  // (every thread reaches the __syncthreads below: no early exit before it)
   pdl_prologue();
   uint64_t t64;
   const int64_t* ids_b;
   int64_t n_b;
   if (fused_begin) {
+    // The window feed between gather t-1 and this one starts without waiting for k_serve(t-1)
+    // (k_route_local), so the programmatic wait above may only cover the feed: wait until
+    // k_serve(t-1) closed its record (end_record publishes t_next last, after a fence).
+    if (ba.t_host >= 0 && threadIdx.x == 0)
+      while (*(volatile const uint64_t*)&it->t_next < (uint64_t)ba.t_host) __nanosleep(100);
+    __syncthreads();
+    __threadfence();
     const IterVals v = begin_values(ba, it);
     t64 = v.t;
     ids_b = v.ids;
@@ -365,15 +382,27 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
       }
     }
   }
+  // counters: warp -> CTA (shared memory) -> one atomic per CTA and counter (a warp-level atomic
+  // on these four hot addresses serialised thousands of atomics per batch at L2)
+  __shared__ uint32_t s_cnt[4];
+  if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
   nreq = __reduce_add_sync(0xffffffffu, nreq);
   npeer = __reduce_add_sync(0xffffffffu, npeer);
   nfirst = __reduce_add_sync(0xffffffffu, nfirst);
   nhit = __reduce_add_sync(0xffffffffu, nhit);
   if (lane_id() == 0) {
-    if (nreq) atomicAdd(&scr->nreq, nreq);
-    if (nfirst) atomicAdd(&scr->nuniq, nfirst);
-    if (nhit) atomicAdd(&rec[F_HIT], (unsigned long long)nhit);
-    if (npeer) atomicAdd(&rec[F_PEER], (unsigned long long)npeer);
+    if (nreq) atomicAdd(&s_cnt[0], nreq);
+    if (nfirst) atomicAdd(&s_cnt[1], nfirst);
+    if (nhit) atomicAdd(&s_cnt[2], nhit);
+    if (npeer) atomicAdd(&s_cnt[3], npeer);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_cnt[0]) atomicAdd(&scr->nreq, s_cnt[0]);
+    if (s_cnt[1]) atomicAdd(&scr->nuniq, s_cnt[1]);
+    if (s_cnt[2]) atomicAdd(&rec[F_HIT], (unsigned long long)s_cnt[2]);
+    if (s_cnt[3]) atomicAdd(&rec[F_PEER], (unsigned long long)s_cnt[3]);
   }
 }
 
@@ -1200,7 +1229,6 @@ __device__ __forceinline__ void end_record(IterState* it, unsigned long long* hi
     cum[F_ITER] = t;
     scr->staged[(t + 1) & 1] = 0;
     *bad_mirror = scr->bad_ids;
-    it->t_next = t + 1;  // direct calls and graph replays may be mixed
   }
   __syncwarp();
   // prepare gather t + 1: its record and the per-batch scratch counters start at zero
@@ -1214,6 +1242,11 @@ __device__ __forceinline__ void end_record(IterState* it, unsigned long long* hi
     scr->nreq = 0;
     scr->pull_next = 0;
     scr->nslow = 0;
+  }
+  __syncwarp();
+  if (f == 0) {  // last: gather t is complete (k_dedup of t + 1 may be waiting for this, below)
+    __threadfence();
+    *(volatile uint64_t*)&it->t_next = t + 1;  // direct calls and graph replays may be mixed
   }
 }
 

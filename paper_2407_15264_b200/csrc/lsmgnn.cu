@@ -216,6 +216,10 @@ struct Ctx {
   // peer on its own GPU runs both phases after "served". LSMGNN_SPLIT_PULL=0/1 overrides.
   bool split_pull = true;
   bool pdl = false;  // programmatic dependent launch on the G = 1 chain (launch_pdl)
+  // the library's last launch on tail_st ended a G = 1 gather (k_serve / k_end): a window feed
+  // right behind it may start early (k_route_local, wait_prev = 0)
+  bool tail_gather = false;
+  cudaStream_t tail_st = nullptr;
   // LSMGNN_G1_PULL=1 (G = 1, profiling aid): the G > 1 serve path — k_fill, then k_pull phase 0
   // (rows in place) and phase 1 (rows filled this batch), then k_end — instead of the fused
   // k_serve; the pull kernels can then be profiled on one process (local HBM instead of peers)
@@ -230,11 +234,13 @@ struct Ctx {
   cudaEvent_t ev_gend[8] = {};
   int64_t gend_t[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   cudaStream_t gend_st[8] = {};
+  bool gend_rec[8] = {};  // lazily recorded: only when another stream has to wait for it
   cudaEvent_t ev_dedup[8] = {};  // G > 1: after k_dedup of gather dedup_t[i] (window feeds wait on it)
   int64_t dedup_t[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   cudaEvent_t ev_feed = nullptr;
   cudaStream_t feed_st = nullptr;
   bool feed_recorded = false, feed_since_gather = false;
+  bool feed_ev_rec = false;  // lazily recorded like gend_rec
   cudaStream_t last_stream = nullptr;
   // stream of the last gather: a gather issued on another stream first waits for the end of
   // the previous one (k_begin resets the per-iteration state and scratch it still uses; at
@@ -582,6 +588,7 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = g.pdl ? 1 : 0;
+  g.tail_gather = false;  // (launch_gather sets it again after its last kernel)
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) return set_err(LSMGNN_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
   return 0;
@@ -839,6 +846,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     KLAUNCH(k_end, 1, 32, 0, st, ea);
     LAUNCHED();
   }
+  g.tail_gather = G == 1 && !graph;
+  g.tail_st = st;
   return 0;
 }
 
@@ -859,11 +868,12 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
               (int64_t)g.cap, g.bad_dev_overflow);
       LAUNCHED();
       KLAUNCH(k_route_local, grid_for(n_bound, 256), 256, 0, st, g.it, (int64_t)-1, (const int64_t*)nullptr, (int64_t)0,
-              g.Wp1, g.N, g.ring, stride, g.ring_len, g.scr, g.mask, g.MW);
+              g.Wp1, g.N, g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, 1u);
       LAUNCHED();
     } else {  // direct: one launch, the batch as kernel arguments
+      const uint32_t wait_prev = (g.tail_gather && g.tail_st == st) ? 0u : 1u;
       KLAUNCH(k_route_local, grid_for(std::max<int64_t>(n, 1), 256), 256, 0, st, g.it, k_host, ids, n, g.Wp1, g.N,
-              g.ring, stride, g.ring_len, g.scr, g.mask, g.MW);
+              g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, wait_prev);
       LAUNCHED();
     }
     return 0;
@@ -884,26 +894,53 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
 }
 
 // ---- cross-stream order of gathers, window feeds and the PVP copy
+// The end-of-gather and end-of-feed events are recorded LAZILY: note_* only remembers the
+// stream; the event is recorded on it when another stream first has to wait (then it also
+// covers the work issued on that stream since — conservative, never early). A single-stream
+// caller therefore gets no event record between the kernels of consecutive calls, which would
+// cut the programmatic-dependent-launch chain (k_serve(t) -> feed -> k_dedup(t+1)).
 int note_gather_end(int64_t t, cudaStream_t st) {
   const int i = (int)(t & 7);
   if (!g.ev_gend[i]) CK(cudaEventCreateWithFlags(&g.ev_gend[i], cudaEventDisableTiming));
-  CK(cudaEventRecord(g.ev_gend[i], st));
   g.gend_t[i] = t;
   g.gend_st[i] = st;
+  g.gend_rec[i] = false;
   return 0;
 }
-// `st` waits for the end of gather t (t < 0: nothing to wait for). A record on `st` itself is
-// already ordered (and an event wait there would only cut the programmatic launch chain). If
-// that record was overwritten, wait for every recorded gather (conservative, still correct).
+int gend_event(int i) {  // record slot i's event now if it was not recorded yet
+  if (!g.gend_rec[i]) {
+    CK(cudaEventRecord(g.ev_gend[i], g.gend_st[i]));
+    g.gend_rec[i] = true;
+  }
+  return 0;
+}
+// `st` waits for the end of gather t (t < 0: nothing to wait for). A gather issued on `st` itself
+// is already ordered. If that slot was reused, wait for every remembered gather (conservative).
 int wait_gather_end(int64_t t, cudaStream_t st) {
   if (t < 0) return 0;
   const int i = (int)(t & 7);
   if (g.gend_t[i] == t) {
-    if (g.gend_st[i] != st) CK(cudaStreamWaitEvent(st, g.ev_gend[i], 0));
+    if (g.gend_st[i] != st) {
+      if (int rc = gend_event(i)) return rc;
+      CK(cudaStreamWaitEvent(st, g.ev_gend[i], 0));
+    }
     return 0;
   }
   for (int j = 0; j < 8; ++j)
-    if (g.gend_t[j] >= 0 && g.gend_st[j] != st) CK(cudaStreamWaitEvent(st, g.ev_gend[j], 0));
+    if (g.gend_t[j] >= 0 && g.gend_st[j] != st) {
+      if (int rc = gend_event(j)) return rc;
+      CK(cudaStreamWaitEvent(st, g.ev_gend[j], 0));
+    }
+  return 0;
+}
+// `st` waits for the last window feed (issued on feed_st)
+int wait_feed(cudaStream_t st) {
+  if (!g.feed_recorded || g.feed_st == st) return 0;
+  if (!g.feed_ev_rec) {
+    CK(cudaEventRecord(g.ev_feed, g.feed_st));
+    g.feed_ev_rec = true;
+  }
+  CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
   return 0;
 }
 // G > 1: the event recorded after k_dedup of gather t (the clear of ring slot t mod (W+1)).
@@ -926,14 +963,14 @@ int wait_dedup(int64_t t, cudaStream_t st) {
 // G = 1, gather(k - W - 1), whose k_dedup clears mask bit / ring slot k mod (W+1) (at G > 1 the
 // feed's exchange runs first and only k_win_gather waits, for that k_dedup).
 int feed_begin(int64_t k, cudaStream_t st) {
-  if (g.feed_recorded && g.feed_st != st) CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+  if (int rc = wait_feed(st)) return rc;
   return g.world == 1 ? wait_gather_end(k - (int64_t)g.W - 1, st) : 0;
 }
 int feed_end(cudaStream_t st) {
   if (!g.ev_feed) CK(cudaEventCreateWithFlags(&g.ev_feed, cudaEventDisableTiming));
-  CK(cudaEventRecord(g.ev_feed, st));
   g.feed_recorded = g.feed_since_gather = true;
   g.feed_st = st;
+  g.feed_ev_rec = false;
   return 0;
 }
 
@@ -955,7 +992,8 @@ int launch_pvp(cudaStream_t st) {
   // (profiles/r01_pvp_overlap.md); after the feed it overlaps the caller's next work instead
   // At G > 1 the feed event completes only after every rank's window exchange, which would
   // gate this copy on the slowest rank; there the copy keeps its gather-only dependencies.
-  if (g.feed_recorded && g.world == 1) CK(cudaStreamWaitEvent(g.side, g.ev_feed, 0));
+  if (g.world == 1)
+    if (int rc = wait_feed(g.side)) return rc;
   uint4* pool = reinterpret_cast<uint4*>(pool_of(g.arena));
   const int blocks = g.sms * std::min(2, g.geom_per_sm);
   prof_begin(7, g.side);
@@ -1482,7 +1520,7 @@ int lsmgnn_gather(const int64_t* node_ids, int64_t n, void* out, void* stream) {
     g.pvp_pending = false;
   }
   if (g.feed_since_gather) {  // the window fed through t+W (possibly on another stream)
-    if (g.feed_st != st) CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+    if (int rc = wait_feed(st)) return rc;
     g.feed_since_gather = false;
   }
   if (t > 0 && st != g.gather_st)  // same stream: already ordered (and PDL keeps chaining)
@@ -1827,7 +1865,7 @@ int lsmgnn_graph_replay(void* stream) {
     g.pvp_pending = false;
   }
   if (g.feed_since_gather) {
-    CK(cudaStreamWaitEvent(st, g.ev_feed, 0));
+    if (int rc = wait_feed(st)) return rc;
     g.feed_since_gather = false;
   }
   if (int rc = wait_gather_end(g.t_next - 1, st)) return rc;  // the replay's feed follows gather(t-1)
