@@ -144,8 +144,9 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
 // nothing gather t writes (k_dedup(t) cleared its slot, and k_dedup/k_set completed before
 // k_serve(t) could trigger this launch), and the caller's IDs were produced before gather(t) (a
 // kernel or copy of the caller's in between is not a programmatic predecessor: no early start).
-// So it runs alongside k_serve(t) on the SMs k_serve leaves free; k_dedup(t+1) waits for
-// k_serve(t) itself (it->t_next).
+// So it runs alongside k_serve(t) on the SMs k_serve leaves free, and waits for k_serve(t) only
+// at its END: the launch completes after k_serve(t) did, so the programmatic wait of k_dedup(t+1)
+// still covers gather t.
 __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host, uint32_t Wp1,
                               uint64_t N, uint32_t* __restrict__ ring, uint64_t stride, uint32_t* __restrict__ ring_len,
                               Scratch* scr, uint32_t* __restrict__ mask, uint32_t MW, uint32_t wait_prev) {
@@ -179,6 +180,7 @@ __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_
     // (feeds of consecutive iterations may overlap: the latest one wins)
     if (k_host >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&it->wk_next), (unsigned long long)k_host + 1);
   }
+  if (!wait_prev && k_host >= 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // complete after k_serve(t)
 }
 
 // ------------------------------------------------------------------------------ S1 (G > 1)
@@ -327,13 +329,6 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
   const int64_t* ids_b;
   int64_t n_b;
   if (fused_begin) {
-    // The window feed between gather t-1 and this one starts without waiting for k_serve(t-1)
-    // (k_route_local), so the programmatic wait above may only cover the feed: wait until
-    // k_serve(t-1) closed its record (end_record publishes t_next last, after a fence).
-    if (ba.t_host >= 0 && threadIdx.x == 0)
-      while (*(volatile const uint64_t*)&it->t_next < (uint64_t)ba.t_host) __nanosleep(100);
-    __syncthreads();
-    __threadfence();
     const IterVals v = begin_values(ba, it);
     t64 = v.t;
     ids_b = v.ids;

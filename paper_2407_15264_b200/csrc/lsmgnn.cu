@@ -220,6 +220,7 @@ struct Ctx {
   // right behind it may start early (k_route_local, wait_prev = 0)
   bool tail_gather = false;
   cudaStream_t tail_st = nullptr;
+  bool feed_early = true;  // LSMGNN_FEED_EARLY=0 turns the early feed start off (A/B)
   // LSMGNN_G1_PULL=1 (G = 1, profiling aid): the G > 1 serve path — k_fill, then k_pull phase 0
   // (rows in place) and phase 1 (rows filled this batch), then k_end — instead of the fused
   // k_serve; the pull kernels can then be profiled on one process (local HBM instead of peers)
@@ -871,7 +872,7 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
               g.Wp1, g.N, g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, 1u);
       LAUNCHED();
     } else {  // direct: one launch, the batch as kernel arguments
-      const uint32_t wait_prev = (g.tail_gather && g.tail_st == st) ? 0u : 1u;
+      const uint32_t wait_prev = (g.feed_early && g.tail_gather && g.tail_st == st) ? 0u : 1u;
       KLAUNCH(k_route_local, grid_for(std::max<int64_t>(n, 1), 256), 256, 0, st, g.it, k_host, ids, n, g.Wp1, g.N,
               g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, wait_prev);
       LAUNCHED();
@@ -1379,6 +1380,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   }
   g.pdl = G == 1 && !std::getenv("LSMGNN_NO_PDL");
   g.g1_pull = G == 1 && std::getenv("LSMGNN_G1_PULL") && std::atoi(std::getenv("LSMGNN_G1_PULL")) != 0;
+  g.feed_early = !(std::getenv("LSMGNN_FEED_EARLY") && std::atoi(std::getenv("LSMGNN_FEED_EARLY")) == 0);
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
