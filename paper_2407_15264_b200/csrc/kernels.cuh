@@ -280,18 +280,25 @@ struct DedupArgs {
   uint32_t A;
 };
 // One request: first occurrence of its node (returns 1) -> into the set's bucket, probed.
+// G = 1: request position pos joins node q's list (head[q] = stamp<<32 | pos, nxt[pos] = previous)
+// — the positions a fill of q delivers its row to (k_serve). A hit is delivered through node_loc,
+// so the FIRST occurrence of a hit node never needs to be on the list (the common case skips the
+// atomic); later occurrences join it before they know whether the node hit (harmless).
+__device__ __forceinline__ void list_join(const DedupArgs& a, uint32_t q, uint32_t pos, uint32_t stamp) {
+  const unsigned long long old = atomicExch(&a.head[q], ((unsigned long long)stamp << 32) | pos);
+  a.nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
+}
 __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, uint32_t stamp,
                                               uint32_t t, uint32_t* nhit) {
   const uint32_t q = v / a.G;
   const bool first = atomicExch(&a.mark[q], stamp) != stamp;
-  if (a.head) {
-    const unsigned long long old = atomicExch(&a.head[q], ((unsigned long long)stamp << 32) | pos);
-    a.nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
+  if (!first) {
+    if (a.head) list_join(a, q, pos, stamp);
+    return 0;
   }
-  if (!first) return 0;
   const uint32_t s = q % a.S;
-  a.bucket[(size_t)s * a.BC + atomicAdd(&a.set_cnt[s], 1u)] = v;
-  // probe the set's A ways (one round trip: independent loads)
+  // the bucket slot and the probe of the set's A ways are independent: one round trip
+  const uint32_t slot = atomicAdd(&a.set_cnt[s], 1u);
   const uint32_t* tg = a.tags + (size_t)s * a.A;
   int way = -1;
   if (a.A == 32) {
@@ -310,17 +317,18 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
     for (uint32_t k = 0; k < a.A; ++k)
       if (tg[k] == v) way = (int)k;
   }
+  a.bucket[(size_t)s * a.BC + slot] = v;
   if (way >= 0) {
     a.node_loc[q] = s * a.A + (uint32_t)way;
     a.last_use[s * a.A + (uint32_t)way] = t;
     ++*nhit;
-  } else if (a.slow_stamp[s] != stamp && atomicExch(&a.slow_stamp[s], stamp) != stamp) {
-    a.slow_list[atomicAdd(&a.scr->nslow, 1u)] = s;  // first miss of the set: k_set processes it
+  } else {
+    if (a.head) list_join(a, q, pos, stamp);  // a fill will deliver this row
+    if (a.slow_stamp[s] != stamp && atomicExch(&a.slow_stamp[s], stamp) != stamp)
+      a.slow_list[atomicAdd(&a.scr->nslow, 1u)] = s;  // first miss of the set: k_set processes it
   }
   return 1;
 }
-// fused_begin (G = 1): the iteration's values come from `ba` (k_begin's job: no separate launch)
-// and block 0 publishes them; otherwise k_begin published them in IterState.
 __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long long* hist, BeginArgs ba,
                         uint32_t fused_begin) {
   // (every thread reaches the __syncthreads below: no early exit before it)
@@ -1111,24 +1119,36 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
     if (lane == 0) ring_init(ring);
     __syncwarp();
   }
-  // A warp takes kChunk consecutive requests: its lanes read the IDs and the (local or
-  // peer) node_loc words at once — one dependent round trip per chunk instead of two per
-  // row, which matters most when node_loc is a peer's (NVLink latency) — then the warp
-  // copies the rows of this phase.
+  // A warp takes kChunk consecutive requests (chunks w, w + nw, ...): its lanes read the IDs and
+  // the (local or peer) node_loc words at once — one dependent round trip per chunk instead of
+  // two per row, which matters most when node_loc is a peer's (NVLink latency) — and the next
+  // chunk's locations / the one after's IDs are loaded while this chunk's rows are copied.
   constexpr uint32_t kChunk = 32;
-  for (int64_t c0 = warp * kChunk; c0 < n; c0 += nwarps * kChunk) {
-    const uint32_t m = (uint32_t)min((int64_t)kChunk, n - c0);
-    uint32_t loc = kInvalid, g = 0;
-    bool valid = false;
-    if ((uint32_t)lane < m) {
-      const int64_t x = ids[c0 + lane];
-      if (x >= 0 && (uint64_t)x < N) {
-        const uint32_t v = (uint32_t)x;
-        g = v % a.G;
-        loc = a.node_loc[g][v / a.G];
-        valid = true;
-      }
+  const int64_t step = nwarps * kChunk;
+  auto id_at = [&](int64_t c) -> int64_t { return c + lane < n ? ids[c + lane] : -2; };
+  struct Loc {
+    uint32_t loc, g;
+    bool valid;
+  };
+  auto loc_of = [&](int64_t x) -> Loc {  // -2: past the batch
+    Loc l{kInvalid, 0, false};
+    if (x >= 0 && (uint64_t)x < N) {
+      const uint32_t v = (uint32_t)x;
+      l.g = v % a.G;
+      l.loc = a.node_loc[l.g][v / a.G];
+      l.valid = true;
     }
+    return l;
+  };
+  int64_t c0 = warp * kChunk;
+  Loc cur = c0 < n ? loc_of(id_at(c0)) : Loc{kInvalid, 0, false};
+  int64_t x_next = c0 + step < n ? id_at(c0 + step) : -2;
+  for (; c0 < n; c0 += step) {
+    const Loc nxt = loc_of(x_next);
+    const int64_t x_nn = c0 + 2 * step < n ? id_at(c0 + 2 * step) : -2;
+    const uint32_t m = (uint32_t)min((int64_t)kChunk, n - c0);
+    const uint32_t loc = cur.loc, g = cur.g;
+    const bool valid = cur.valid;
     if (PHASE == 0) {  // ERANGE: zero-filled rows
       uint32_t zero = __ballot_sync(0xffffffffu, (uint32_t)lane < m && !valid);
       while (zero) {
@@ -1156,6 +1176,8 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
                                          nvec);
       }
     }
+    cur = nxt;
+    x_next = x_nn;
   }
   if (TMA && lane == 0) ring_drain();
 }
@@ -1310,20 +1332,22 @@ __global__ void k_serve(ServeArgs a) {
       }
     }
   }
-  // ---- delivery of the rows no fill delivers, in chunks from the shared counter. The
-  // chunk's IDs and locations are looked up by its lanes at once (one dependent round trip
-  // per chunk instead of two per row), then its rows are copied.
-  for (;;) {
-    uint32_t c0 = 0;
-    if (lane == 0) c0 = atomicAdd(&a.scr->pull_next, kChunk);
-    c0 = __shfl_sync(0xffffffffu, c0, 0);
-    if ((int64_t)c0 >= n) break;
-    const uint32_t m = (uint32_t)min((int64_t)kChunk, n - (int64_t)c0);
-    uint32_t loc = kDelivered;  // lanes >= m: nothing to copy
-    if ((uint32_t)lane < m) {
-      const int64_t x = ids[c0 + lane];
-      loc = (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
-    }
+  // ---- delivery of the rows no fill delivers: warp w takes the chunks of 32 requests
+  // w, w + nw, w + 2 nw, ... (a static order: the next chunk is known, so its IDs and locations
+  // are loaded while the current chunk's rows are copied — one chunk of IDs and one of
+  // locations in flight ahead of the copy). Fill warps join with their chunks once their fills
+  // are done; in a storage-bound batch that only moves the hits' share of the copy to the end.
+  const int64_t step = (int64_t)nw * kChunk;
+  int64_t c0 = (int64_t)gw * kChunk;
+  auto id_at = [&](int64_t c) -> int64_t { return c + lane < n ? ids[c + lane] : -2; };
+  auto loc_of = [&](int64_t x) -> uint32_t {  // -2: past the batch (nothing to copy)
+    return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
+  };
+  uint32_t loc = c0 < n ? loc_of(id_at(c0)) : kDelivered;
+  int64_t x_next = c0 + step < n ? id_at(c0 + step) : -2;
+  for (; c0 < n; c0 += step) {
+    const uint32_t loc_next = loc_of(x_next);                        // chunk c0 + step: locations
+    const int64_t x_nn = c0 + 2 * step < n ? id_at(c0 + 2 * step) : -2;  // chunk c0 + 2 step: IDs
     uint32_t zero = __ballot_sync(0xffffffffu, loc == kInvalid);
     while (zero) {  // ERANGE: zero-filled rows (rare)
       const uint32_t j = __ffs(zero) - 1;
@@ -1347,6 +1371,8 @@ __global__ void k_serve(ServeArgs a) {
         warp_copy_row<UNROLL, kDev, OUT>(a.out + (size_t)(c0 + j) * nvec, a.pool + (size_t)lj * nvec, nvec);
       }
     }
+    loc = loc_next;
+    x_next = x_nn;
   }
   if (TMA && lane == 0) ring_drain();
   // ---- S9: the last CTA to finish closes the record
