@@ -1140,7 +1140,7 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
     }
     return l;
   };
-  int64_t c0 = warp * kChunk;
+  int64_t c0 = ((int64_t)wib * gridDim.x + blockIdx.x) * kChunk;  // SM-major warp order (see k_serve)
   Loc cur = c0 < n ? loc_of(id_at(c0)) : Loc{kInvalid, 0, false};
   int64_t x_next = c0 + step < n ? id_at(c0 + step) : -2;
   for (; c0 < n; c0 += step) {
@@ -1210,6 +1210,7 @@ struct ServeArgs {
   const uint32_t* node_loc;
   uint4* out;
   uint32_t bounce;
+  uint32_t dynamic;  // delivery chunks from a counter instead of the static order
   const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
   // S9, closed by the last CTA
@@ -1332,22 +1333,10 @@ __global__ void k_serve(ServeArgs a) {
       }
     }
   }
-  // ---- delivery of the rows no fill delivers: warp w takes the chunks of 32 requests
-  // w, w + nw, w + 2 nw, ... (a static order: the next chunk is known, so its IDs and locations
-  // are loaded while the current chunk's rows are copied — one chunk of IDs and one of
-  // locations in flight ahead of the copy). Fill warps join with their chunks once their fills
-  // are done; in a storage-bound batch that only moves the hits' share of the copy to the end.
-  const int64_t step = (int64_t)nw * kChunk;
-  int64_t c0 = (int64_t)gw * kChunk;
-  auto id_at = [&](int64_t c) -> int64_t { return c + lane < n ? ids[c + lane] : -2; };
-  auto loc_of = [&](int64_t x) -> uint32_t {  // -2: past the batch (nothing to copy)
-    return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
-  };
-  uint32_t loc = c0 < n ? loc_of(id_at(c0)) : kDelivered;
-  int64_t x_next = c0 + step < n ? id_at(c0 + step) : -2;
-  for (; c0 < n; c0 += step) {
-    const uint32_t loc_next = loc_of(x_next);                        // chunk c0 + step: locations
-    const int64_t x_nn = c0 + 2 * step < n ? id_at(c0 + 2 * step) : -2;  // chunk c0 + 2 step: IDs
+  // ---- delivery of the rows no fill delivers, in chunks of 32 requests. The chunk's IDs and
+  // locations are looked up by its lanes at once (one dependent round trip per chunk instead of
+  // two per row), then its rows are copied.
+  auto copy_chunk = [&](int64_t c0, uint32_t loc) {
     uint32_t zero = __ballot_sync(0xffffffffu, loc == kInvalid);
     while (zero) {  // ERANGE: zero-filled rows (rare)
       const uint32_t j = __ffs(zero) - 1;
@@ -1371,8 +1360,35 @@ __global__ void k_serve(ServeArgs a) {
         warp_copy_row<UNROLL, kDev, OUT>(a.out + (size_t)(c0 + j) * nvec, a.pool + (size_t)lj * nvec, nvec);
       }
     }
-    loc = loc_next;
-    x_next = x_nn;
+  };
+  auto id_at = [&](int64_t c) -> int64_t { return c + lane < n ? ids[c + lane] : -2; };
+  auto loc_of = [&](int64_t x) -> uint32_t {  // -2: past the batch (nothing to copy)
+    return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
+  };
+  if (a.dynamic) {  // chunks handed out by a counter (LSMGNN_SERVE_DYNAMIC=1)
+    for (;;) {
+      uint32_t c0 = 0;
+      if (lane == 0) c0 = atomicAdd(&a.scr->pull_next, kChunk);
+      c0 = __shfl_sync(0xffffffffu, c0, 0);
+      if ((int64_t)c0 >= n) break;
+      copy_chunk(c0, loc_of(id_at(c0)));
+    }
+  } else {
+    // Static order, warps numbered SM-major (warp slot w of CTA b is warp w * gridDim + b) so
+    // that the warps holding one chunk more than the others are spread over every SM; the next
+    // chunk's locations and the one after's IDs are loaded during the current chunk's copy.
+    const uint32_t sw = wib * gridDim.x + blockIdx.x;
+    const int64_t step = (int64_t)nw * kChunk;
+    int64_t c0 = (int64_t)sw * kChunk;
+    uint32_t loc = c0 < n ? loc_of(id_at(c0)) : kDelivered;
+    int64_t x_next = c0 + step < n ? id_at(c0 + step) : -2;
+    for (; c0 < n; c0 += step) {
+      const uint32_t loc_next = loc_of(x_next);
+      const int64_t x_nn = c0 + 2 * step < n ? id_at(c0 + 2 * step) : -2;
+      copy_chunk(c0, loc);
+      loc = loc_next;
+      x_next = x_nn;
+    }
   }
   if (TMA && lane == 0) ring_drain();
   // ---- S9: the last CTA to finish closes the record
