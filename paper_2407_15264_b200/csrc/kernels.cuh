@@ -1210,7 +1210,7 @@ struct ServeArgs {
   const uint32_t* node_loc;
   uint4* out;
   uint32_t bounce;
-  uint32_t dynamic;  // delivery chunks from a counter instead of the static order
+  uint32_t ahead;    // delivery chunks reserved ahead of the one being copied (0, 1, 2)
   const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
   // S9, closed by the last CTA
@@ -1365,29 +1365,40 @@ __global__ void k_serve(ServeArgs a) {
   auto loc_of = [&](int64_t x) -> uint32_t {  // -2: past the batch (nothing to copy)
     return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
   };
-  if (a.dynamic) {  // chunks handed out by a counter (LSMGNN_SERVE_DYNAMIC=1)
+  // Chunks are handed out by a counter (load balance: the hit rows finish together, and a
+  // storage-bound batch keeps the delivery-only warps busy while the fills run). ahead = 1: the
+  // next chunk's counter atomic is issued before the current chunk's copy (its latency hidden);
+  // ahead = 2: also the following chunk's IDs are loaded during the copy (a warp then holds up to
+  // two chunks in reserve). A static chunk order measured slower (0.85 vs 0.89 of HBM peak:
+  // per-warp imbalance at the tail; profiles/r02_hit_path.md).
+  auto grab = [&]() -> uint32_t { return lane == 0 ? atomicAdd(&a.scr->pull_next, kChunk) : 0u; };
+  if (a.ahead == 0) {
     for (;;) {
-      uint32_t c0 = 0;
-      if (lane == 0) c0 = atomicAdd(&a.scr->pull_next, kChunk);
-      c0 = __shfl_sync(0xffffffffu, c0, 0);
+      const uint32_t c0 = __shfl_sync(0xffffffffu, grab(), 0);
       if ((int64_t)c0 >= n) break;
       copy_chunk(c0, loc_of(id_at(c0)));
     }
+  } else if (a.ahead == 1) {
+    uint32_t c0 = __shfl_sync(0xffffffffu, grab(), 0);
+    while ((int64_t)c0 < n) {
+      const uint32_t raw = grab();  // next chunk, in flight during the copy
+      copy_chunk(c0, loc_of(id_at(c0)));
+      c0 = __shfl_sync(0xffffffffu, raw, 0);
+    }
   } else {
-    // Static order, warps numbered SM-major (warp slot w of CTA b is warp w * gridDim + b) so
-    // that the warps holding one chunk more than the others are spread over every SM; the next
-    // chunk's locations and the one after's IDs are loaded during the current chunk's copy.
-    const uint32_t sw = wib * gridDim.x + blockIdx.x;
-    const int64_t step = (int64_t)nw * kChunk;
-    int64_t c0 = (int64_t)sw * kChunk;
-    uint32_t loc = c0 < n ? loc_of(id_at(c0)) : kDelivered;
-    int64_t x_next = c0 + step < n ? id_at(c0 + step) : -2;
-    for (; c0 < n; c0 += step) {
-      const uint32_t loc_next = loc_of(x_next);
-      const int64_t x_nn = c0 + 2 * step < n ? id_at(c0 + 2 * step) : -2;
+    uint32_t c0 = __shfl_sync(0xffffffffu, grab(), 0);
+    uint32_t c1 = __shfl_sync(0xffffffffu, grab(), 0);
+    uint32_t loc = (int64_t)c0 < n ? loc_of(id_at(c0)) : kDelivered;
+    int64_t x1 = (int64_t)c1 < n ? id_at(c1) : -2;
+    while ((int64_t)c0 < n) {
+      const uint32_t loc1 = loc_of(x1);  // chunk c1's locations, in flight during the copy
+      const uint32_t raw = (int64_t)c1 < n ? grab() : (uint32_t)n;  // chunk c2, likewise
       copy_chunk(c0, loc);
-      loc = loc_next;
-      x_next = x_nn;
+      const uint32_t c2 = __shfl_sync(0xffffffffu, raw, 0);
+      x1 = (int64_t)c2 < n ? id_at(c2) : -2;
+      c0 = c1;
+      loc = loc1;
+      c1 = c2;
     }
   }
   if (TMA && lane == 0) ring_drain();

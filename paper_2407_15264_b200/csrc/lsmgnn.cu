@@ -228,7 +228,7 @@ struct Ctx {
   // k_serve geometry: CTAs per SM and TMA row stages per warp (0 = 16-B vector copies);
   // LSMGNN_SERVE_CPS / LSMGNN_SERVE_ST override (A/B runs)
   int serve_cps = 2, serve_st = 3;
-  bool serve_dynamic = false;  // LSMGNN_SERVE_DYNAMIC=1: k_serve hands delivery chunks out by a counter
+  int serve_ahead = 1;  // LSMGNN_SERVE_AHEAD=0/1/2: delivery chunks k_serve reserves ahead (A/B)
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
@@ -758,7 +758,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.out = o4;
     sa.bounce = bounce;
     sa.io_ready = g.io_ready_dev;
-    sa.dynamic = g.serve_dynamic ? 1u : 0u;
+    sa.ahead = (uint32_t)g.serve_ahead;
     sa.hist = g.hist;
     sa.cum = g.cum;
     sa.bad_mirror = g.bad_dev;
@@ -1383,7 +1383,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   g.pdl = G == 1 && !std::getenv("LSMGNN_NO_PDL");
   g.g1_pull = G == 1 && std::getenv("LSMGNN_G1_PULL") && std::atoi(std::getenv("LSMGNN_G1_PULL")) != 0;
   g.feed_early = !(std::getenv("LSMGNN_FEED_EARLY") && std::atoi(std::getenv("LSMGNN_FEED_EARLY")) == 0);
-  g.serve_dynamic = std::getenv("LSMGNN_SERVE_DYNAMIC") && std::atoi(std::getenv("LSMGNN_SERVE_DYNAMIC")) != 0;
+  if (const char* e = std::getenv("LSMGNN_SERVE_AHEAD")) g.serve_ahead = std::max(0, std::min(2, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
