@@ -54,7 +54,8 @@ struct Scratch {
   uint32_t serve_done; // k_serve: CTAs finished (the last one closes the record)
   uint32_t io_done;    // k_io_export: CTAs finished (the last one publishes the list)
   uint32_t nslow;      // sets with a miss this batch (k_dedup's slow list)
-  uint32_t pad[3];
+  uint32_t pull_phase_next[2];  // k_pull: next request index per phase
+  uint32_t pad[1];
 };
 
 // Per-iteration values, resident on the device. k_begin / k_win_begin write them (from host

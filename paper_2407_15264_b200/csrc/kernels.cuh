@@ -1089,8 +1089,10 @@ __global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, ui
 struct PullArgs {
   const uint4* pool[8];
   const uint32_t* node_loc[8];
+  Scratch* scr;  // per-phase chunk counters
   uint32_t G;
   uint32_t ST;  // TMA ring stages per warp (TMA = 1)
+  uint32_t tail_chunk;
 };
 // TMA = 1: rows move (local or peer) HBM -> shared -> `out` with TMA bulk copies through each
 // warp's ring of ST stages (the source of a peer row is its IPC mapping: over NVLink on
@@ -1119,36 +1121,31 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
     if (lane == 0) ring_init(ring);
     __syncwarp();
   }
-  // A warp takes kChunk consecutive requests (chunks w, w + nw, ...): its lanes read the IDs and
-  // the (local or peer) node_loc words at once — one dependent round trip per chunk instead of
-  // two per row, which matters most when node_loc is a peer's (NVLink latency) — and the next
-  // chunk's locations / the one after's IDs are loaded while this chunk's rows are copied.
+  // A warp takes chunks of consecutive requests from a per-phase counter (guided sizes: 32,
+  // then a.tail_chunk near the end; see k_serve): its lanes read the IDs and the (local or peer)
+  // node_loc words at once — one dependent round trip per chunk instead of two per row, which
+  // matters most when node_loc is a peer's (NVLink latency) — then its rows are copied.
   constexpr uint32_t kChunk = 32;
-  const int64_t step = nwarps * kChunk;
-  auto id_at = [&](int64_t c) -> int64_t { return c + lane < n ? ids[c + lane] : -2; };
-  struct Loc {
-    uint32_t loc, g;
-    bool valid;
-  };
-  auto loc_of = [&](int64_t x) -> Loc {  // -2: past the batch
-    Loc l{kInvalid, 0, false};
-    if (x >= 0 && (uint64_t)x < N) {
-      const uint32_t v = (uint32_t)x;
-      l.g = v % a.G;
-      l.loc = a.node_loc[l.g][v / a.G];
-      l.valid = true;
+  uint32_t* counter = &a.scr->pull_phase_next[PHASE];
+  uint32_t size = kChunk;
+  for (;;) {
+    uint32_t c0u = 0;
+    if (lane == 0) c0u = atomicAdd(counter, size);
+    const int64_t c0 = __shfl_sync(0xffffffffu, c0u, 0);
+    if (c0 >= n) break;
+    const int64_t end = min(c0 + (int64_t)size, n);
+    const uint32_t m = (uint32_t)(end - c0);
+    uint32_t loc = kInvalid, g = 0;
+    bool valid = false;
+    if ((uint32_t)lane < m) {
+      const int64_t x = ids[c0 + lane];
+      if (x >= 0 && (uint64_t)x < N) {
+        const uint32_t v = (uint32_t)x;
+        g = v % a.G;
+        loc = a.node_loc[g][v / a.G];
+        valid = true;
+      }
     }
-    return l;
-  };
-  int64_t c0 = ((int64_t)wib * gridDim.x + blockIdx.x) * kChunk;  // SM-major warp order (see k_serve)
-  Loc cur = c0 < n ? loc_of(id_at(c0)) : Loc{kInvalid, 0, false};
-  int64_t x_next = c0 + step < n ? id_at(c0 + step) : -2;
-  for (; c0 < n; c0 += step) {
-    const Loc nxt = loc_of(x_next);
-    const int64_t x_nn = c0 + 2 * step < n ? id_at(c0 + 2 * step) : -2;
-    const uint32_t m = (uint32_t)min((int64_t)kChunk, n - c0);
-    const uint32_t loc = cur.loc, g = cur.g;
-    const bool valid = cur.valid;
     if (PHASE == 0) {  // ERANGE: zero-filled rows
       uint32_t zero = __ballot_sync(0xffffffffu, (uint32_t)lane < m && !valid);
       while (zero) {
@@ -1176,8 +1173,7 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
                                          nvec);
       }
     }
-    cur = nxt;
-    x_next = x_nn;
+    if (c0 + 2ll * nwarps * kChunk >= n) size = a.tail_chunk;
   }
   if (TMA && lane == 0) ring_drain();
 }
@@ -1210,7 +1206,7 @@ struct ServeArgs {
   const uint32_t* node_loc;
   uint4* out;
   uint32_t bounce;
-  uint32_t ahead;    // delivery chunks reserved ahead of the one being copied (0, 1, 2)
+  uint32_t tail_chunk;  // delivery chunk size near the end of the batch (guided; 32 = fixed)
   const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
   // S9, closed by the last CTA
@@ -1259,6 +1255,8 @@ __device__ __forceinline__ void end_record(IterState* it, unsigned long long* hi
     scr->nbypass = 0;
     scr->nreq = 0;
     scr->pull_next = 0;
+    scr->pull_phase_next[0] = 0;
+    scr->pull_phase_next[1] = 0;
     scr->nslow = 0;
   }
   __syncwarp();
@@ -1361,45 +1359,26 @@ __global__ void k_serve(ServeArgs a) {
       }
     }
   };
-  auto id_at = [&](int64_t c) -> int64_t { return c + lane < n ? ids[c + lane] : -2; };
   auto loc_of = [&](int64_t x) -> uint32_t {  // -2: past the batch (nothing to copy)
     return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
   };
   // Chunks are handed out by a counter (load balance: the hit rows finish together, and a
-  // storage-bound batch keeps the delivery-only warps busy while the fills run). ahead = 1: the
-  // next chunk's counter atomic is issued before the current chunk's copy (its latency hidden);
-  // ahead = 2: also the following chunk's IDs are loaded during the copy (a warp then holds up to
-  // two chunks in reserve). A static chunk order measured slower (0.85 vs 0.89 of HBM peak:
-  // per-warp imbalance at the tail; profiles/r02_hit_path.md).
-  auto grab = [&]() -> uint32_t { return lane == 0 ? atomicAdd(&a.scr->pull_next, kChunk) : 0u; };
-  if (a.ahead == 0) {
-    for (;;) {
-      const uint32_t c0 = __shfl_sync(0xffffffffu, grab(), 0);
-      if ((int64_t)c0 >= n) break;
-      copy_chunk(c0, loc_of(id_at(c0)));
-    }
-  } else if (a.ahead == 1) {
-    uint32_t c0 = __shfl_sync(0xffffffffu, grab(), 0);
-    while ((int64_t)c0 < n) {
-      const uint32_t raw = grab();  // next chunk, in flight during the copy
-      copy_chunk(c0, loc_of(id_at(c0)));
-      c0 = __shfl_sync(0xffffffffu, raw, 0);
-    }
-  } else {
-    uint32_t c0 = __shfl_sync(0xffffffffu, grab(), 0);
-    uint32_t c1 = __shfl_sync(0xffffffffu, grab(), 0);
-    uint32_t loc = (int64_t)c0 < n ? loc_of(id_at(c0)) : kDelivered;
-    int64_t x1 = (int64_t)c1 < n ? id_at(c1) : -2;
-    while ((int64_t)c0 < n) {
-      const uint32_t loc1 = loc_of(x1);  // chunk c1's locations, in flight during the copy
-      const uint32_t raw = (int64_t)c1 < n ? grab() : (uint32_t)n;  // chunk c2, likewise
-      copy_chunk(c0, loc);
-      const uint32_t c2 = __shfl_sync(0xffffffffu, raw, 0);
-      x1 = (int64_t)c2 < n ? id_at(c2) : -2;
-      c0 = c1;
-      loc = loc1;
-      c1 = c2;
-    }
+  // storage-bound batch keeps the delivery-only warps busy while the fills run). Guided sizes:
+  // 32 requests while more than two rounds of chunks remain, then `tail` (so the warps finish
+  // within a small chunk of each other). Reserving chunks ahead of the copy to hide the counter
+  // and ID latencies, and a static chunk order, both measured slower: the tail imbalance they
+  // add costs more than the latency they hide (profiles/r02_hit_path.md).
+  const uint32_t tail = a.tail_chunk;
+  uint32_t size = kChunk;
+  for (;;) {
+    uint32_t c0 = 0;
+    if (lane == 0) c0 = atomicAdd(&a.scr->pull_next, size);
+    c0 = __shfl_sync(0xffffffffu, c0, 0);
+    if ((int64_t)c0 >= n) break;
+    const int64_t end = min((int64_t)c0 + size, n);
+    const int64_t x = (int64_t)c0 + lane < end ? ids[c0 + lane] : -2;
+    copy_chunk(c0, loc_of(x));
+    if ((int64_t)c0 + 2ll * nw * kChunk >= n) size = tail;
   }
   if (TMA && lane == 0) ring_drain();
   // ---- S9: the last CTA to finish closes the record

@@ -228,7 +228,7 @@ struct Ctx {
   // k_serve geometry: CTAs per SM and TMA row stages per warp (0 = 16-B vector copies);
   // LSMGNN_SERVE_CPS / LSMGNN_SERVE_ST override (A/B runs)
   int serve_cps = 2, serve_st = 3;
-  int serve_ahead = 1;  // LSMGNN_SERVE_AHEAD=0/1/2: delivery chunks k_serve reserves ahead (A/B)
+  int serve_tail = 8;  // LSMGNN_SERVE_TAIL=n: k_serve's delivery chunk size near the batch end (A/B)
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
@@ -758,7 +758,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.out = o4;
     sa.bounce = bounce;
     sa.io_ready = g.io_ready_dev;
-    sa.ahead = (uint32_t)g.serve_ahead;
+    sa.tail_chunk = (uint32_t)g.serve_tail;
     sa.hist = g.hist;
     sa.cum = g.cum;
     sa.bad_mirror = g.bad_dev;
@@ -790,6 +790,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       pa.node_loc[h] = loc_of(g.peer_arena[h]);
     }
     pa.G = (uint32_t)G;
+    pa.scr = g.scr;
+    pa.tail_chunk = (uint32_t)g.serve_tail;
     const bool tma = !out_host && g.serve_st > 0;
     pa.ST = tma ? (uint32_t)g.serve_st : 0u;
     const size_t psmem = tma ? (size_t)8 * g.serve_st * g.R : 0;
@@ -1383,7 +1385,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   g.pdl = G == 1 && !std::getenv("LSMGNN_NO_PDL");
   g.g1_pull = G == 1 && std::getenv("LSMGNN_G1_PULL") && std::atoi(std::getenv("LSMGNN_G1_PULL")) != 0;
   g.feed_early = !(std::getenv("LSMGNN_FEED_EARLY") && std::atoi(std::getenv("LSMGNN_FEED_EARLY")) == 0);
-  if (const char* e = std::getenv("LSMGNN_SERVE_AHEAD")) g.serve_ahead = std::max(0, std::min(2, std::atoi(e)));
+  if (const char* e = std::getenv("LSMGNN_SERVE_TAIL")) g.serve_tail = std::max(1, std::min(32, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
