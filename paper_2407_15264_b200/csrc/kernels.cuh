@@ -1092,7 +1092,7 @@ struct PullArgs {
   Scratch* scr;  // per-phase chunk counters
   uint32_t G;
   uint32_t ST;  // TMA ring stages per warp (TMA = 1)
-  uint32_t tail_chunk;
+  uint32_t tail_chunk, tail_rounds;
 };
 // TMA = 1: rows move (local or peer) HBM -> shared -> `out` with TMA bulk copies through each
 // warp's ring of ST stages (the source of a peer row is its IPC mapping: over NVLink on
@@ -1173,7 +1173,7 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
                                          nvec);
       }
     }
-    if (c0 + 2ll * nwarps * kChunk >= n) size = a.tail_chunk;
+    if (c0 + (int64_t)a.tail_rounds * nwarps * kChunk >= n) size = a.tail_chunk;
   }
   if (TMA && lane == 0) ring_drain();
 }
@@ -1207,6 +1207,7 @@ struct ServeArgs {
   uint4* out;
   uint32_t bounce;
   uint32_t tail_chunk;  // delivery chunk size near the end of the batch (guided; 32 = fixed)
+  uint32_t tail_rounds; // ... once fewer than tail_rounds rounds of 32-request chunks remain
   const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
   // S9, closed by the last CTA
@@ -1378,7 +1379,7 @@ __global__ void k_serve(ServeArgs a) {
     const int64_t end = min((int64_t)c0 + size, n);
     const int64_t x = (int64_t)c0 + lane < end ? ids[c0 + lane] : -2;
     copy_chunk(c0, loc_of(x));
-    if ((int64_t)c0 + 2ll * nw * kChunk >= n) size = tail;
+    if ((int64_t)c0 + (int64_t)a.tail_rounds * nw * kChunk >= n) size = tail;
   }
   if (TMA && lane == 0) ring_drain();
   // ---- S9: the last CTA to finish closes the record

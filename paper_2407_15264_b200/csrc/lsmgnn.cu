@@ -229,6 +229,7 @@ struct Ctx {
   // LSMGNN_SERVE_CPS / LSMGNN_SERVE_ST override (A/B runs)
   int serve_cps = 2, serve_st = 3;
   int serve_tail = 8;  // LSMGNN_SERVE_TAIL=n: k_serve's delivery chunk size near the batch end (A/B)
+  int serve_tail_rounds = 2;  // LSMGNN_SERVE_TAIL_ROUNDS=r: ... once fewer than r rounds of chunks remain
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
@@ -711,7 +712,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   }
   {
     const int64_t blocks =
-        std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(8, g.geom_per_sm));
+        std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(4, g.geom_per_sm));
     KLAUNCH(k_set, (int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st, sp);
     LAUNCHED();
   }
@@ -759,6 +760,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.bounce = bounce;
     sa.io_ready = g.io_ready_dev;
     sa.tail_chunk = (uint32_t)g.serve_tail;
+    sa.tail_rounds = (uint32_t)g.serve_tail_rounds;
     sa.hist = g.hist;
     sa.cum = g.cum;
     sa.bad_mirror = g.bad_dev;
@@ -792,6 +794,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     pa.G = (uint32_t)G;
     pa.scr = g.scr;
     pa.tail_chunk = (uint32_t)g.serve_tail;
+    pa.tail_rounds = (uint32_t)g.serve_tail_rounds;
     const bool tma = !out_host && g.serve_st > 0;
     pa.ST = tma ? (uint32_t)g.serve_st : 0u;
     const size_t psmem = tma ? (size_t)8 * g.serve_st * g.R : 0;
@@ -1386,6 +1389,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   g.g1_pull = G == 1 && std::getenv("LSMGNN_G1_PULL") && std::atoi(std::getenv("LSMGNN_G1_PULL")) != 0;
   g.feed_early = !(std::getenv("LSMGNN_FEED_EARLY") && std::atoi(std::getenv("LSMGNN_FEED_EARLY")) == 0);
   if (const char* e = std::getenv("LSMGNN_SERVE_TAIL")) g.serve_tail = std::max(1, std::min(32, std::atoi(e)));
+  if (const char* e = std::getenv("LSMGNN_SERVE_TAIL_ROUNDS")) g.serve_tail_rounds = std::max(0, std::min(64, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
