@@ -38,6 +38,10 @@
  *   LSMGNN_GEOMETRY=small     one CTA per SM for every grid (launch-geometry tests)
  *   LSMGNN_SERVE_CPS=c, LSMGNN_SERVE_ST=s  serve/pull geometry: c CTAs per SM, s TMA row stages
  *                             per warp (s = 0: 16-B vector copies instead of TMA bulk copies)
+ *   LSMGNN_SERVE_TAIL=k, LSMGNN_SERVE_TAIL_ROUNDS=r  delivery chunks of 32 requests, k once
+ *                             fewer than r rounds of chunks remain (guided; defaults 4, 2)
+ *   LSMGNN_FEED_EARLY=0       the window feed waits for the gather before it (default: it
+ *                             starts alongside k_serve and waits for it at its end)
  *   LSMGNN_G1_PULL=1          G = 1 profiling aid: the G > 1 serve path (k_fill, k_pull phases,
  *                             k_end) instead of the fused k_serve; results are identical
  */

@@ -228,7 +228,7 @@ struct Ctx {
   // k_serve geometry: CTAs per SM and TMA row stages per warp (0 = 16-B vector copies);
   // LSMGNN_SERVE_CPS / LSMGNN_SERVE_ST override (A/B runs)
   int serve_cps = 2, serve_st = 3;
-  int serve_tail = 8;  // LSMGNN_SERVE_TAIL=n: k_serve's delivery chunk size near the batch end (A/B)
+  int serve_tail = 4;  // LSMGNN_SERVE_TAIL=n: k_serve's delivery chunk size near the batch end (A/B)
   int serve_tail_rounds = 2;  // LSMGNN_SERVE_TAIL_ROUNDS=r: ... once fewer than r rounds of chunks remain
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
