@@ -1208,6 +1208,7 @@ struct ServeArgs {
   uint32_t bounce;
   uint32_t tail_chunk;  // delivery chunk size near the end of the batch (guided; 32 = fixed)
   uint32_t tail_rounds; // ... once fewer than tail_rounds rounds of 32-request chunks remain
+  uint32_t ahead;       // keep one 32-request chunk in reserve before the tail phase
   const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
   // S9, closed by the last CTA
@@ -1364,22 +1365,51 @@ __global__ void k_serve(ServeArgs a) {
     return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
   };
   // Chunks are handed out by a counter (load balance: the hit rows finish together, and a
-  // storage-bound batch keeps the delivery-only warps busy while the fills run). Guided sizes:
-  // 32 requests while more than two rounds of chunks remain, then `tail` (so the warps finish
-  // within a small chunk of each other). Reserving chunks ahead of the copy to hide the counter
-  // and ID latencies, and a static chunk order, both measured slower: the tail imbalance they
-  // add costs more than the latency they hide (profiles/r02_hit_path.md).
+  // storage-bound batch keeps the delivery-only warps busy while the fills run), with guided
+  // sizes: 32 requests, then `tail` once fewer than tail_rounds rounds of 32-request chunks remain,
+  // so the warps finish within a small chunk of each other. In the 32-request phase (a.ahead) a
+  // warp holds the next chunk in reserve: its locations and the counter atomic for the one after
+  // are in flight during the current copy (one ID round trip exposed per chunk instead of three);
+  // the reservation stops in the tail phase, where it would add imbalance. A static chunk order,
+  // and reserving ahead through the tail, measured slower (profiles/r02_hit_path.md).
   const uint32_t tail = a.tail_chunk;
-  uint32_t size = kChunk;
+  const int64_t tail_from = n - (int64_t)a.tail_rounds * nw * kChunk;
+  auto grab = [&](uint32_t sz) -> uint32_t { return lane == 0 ? atomicAdd(&a.scr->pull_next, sz) : 0u; };
+  auto ids_of = [&](int64_t c, uint32_t sz) -> int64_t {
+    return c + lane < min(c + (int64_t)sz, n) ? ids[c + lane] : -2;
+  };
+  if (a.ahead) {
+    int64_t c0 = __shfl_sync(0xffffffffu, grab(kChunk), 0);
+    if (c0 < n) {
+      uint32_t loc0 = loc_of(ids_of(c0, kChunk));
+      int64_t c1 = c0 < tail_from ? (int64_t)__shfl_sync(0xffffffffu, grab(kChunk), 0) : n;
+      int64_t x1 = c1 < n ? ids_of(c1, kChunk) : -2;
+      for (;;) {
+        if (c1 < n && c1 < tail_from) {  // keep one chunk in reserve
+          const uint32_t loc1 = loc_of(x1);
+          const uint32_t raw = grab(kChunk);
+          copy_chunk(c0, loc0);
+          const int64_t c2 = __shfl_sync(0xffffffffu, raw, 0);
+          x1 = c2 < n ? ids_of(c2, kChunk) : -2;
+          c0 = c1;
+          loc0 = loc1;
+          c1 = c2;
+          continue;
+        }
+        copy_chunk(c0, loc0);
+        if (c1 < n) copy_chunk(c1, loc_of(x1));
+        break;
+      }
+    }
+  }
+  // (a.ahead = 0, or the tail after the reserved chunks): chunks grabbed one at a time
+  uint32_t size = a.ahead ? tail : kChunk;
   for (;;) {
-    uint32_t c0 = 0;
-    if (lane == 0) c0 = atomicAdd(&a.scr->pull_next, size);
-    c0 = __shfl_sync(0xffffffffu, c0, 0);
-    if ((int64_t)c0 >= n) break;
-    const int64_t end = min((int64_t)c0 + size, n);
-    const int64_t x = (int64_t)c0 + lane < end ? ids[c0 + lane] : -2;
-    copy_chunk(c0, loc_of(x));
-    if ((int64_t)c0 + (int64_t)a.tail_rounds * nw * kChunk >= n) size = tail;
+    const uint32_t sz = size;
+    const int64_t c0 = __shfl_sync(0xffffffffu, grab(sz), 0);
+    if (c0 >= n) break;
+    copy_chunk(c0, loc_of(ids_of(c0, sz)));
+    if (c0 >= tail_from) size = tail;
   }
   if (TMA && lane == 0) ring_drain();
   // ---- S9: the last CTA to finish closes the record

@@ -230,6 +230,7 @@ struct Ctx {
   int serve_cps = 2, serve_st = 3;
   int serve_tail = 4;  // LSMGNN_SERVE_TAIL=n: k_serve's delivery chunk size near the batch end (A/B)
   int serve_tail_rounds = 2;  // LSMGNN_SERVE_TAIL_ROUNDS=r: ... once fewer than r rounds of chunks remain
+  bool serve_ahead = true;    // LSMGNN_SERVE_AHEAD=0/1: one chunk in reserve before the tail phase
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
@@ -761,6 +762,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.io_ready = g.io_ready_dev;
     sa.tail_chunk = (uint32_t)g.serve_tail;
     sa.tail_rounds = (uint32_t)g.serve_tail_rounds;
+    sa.ahead = g.serve_ahead ? 1u : 0u;
     sa.hist = g.hist;
     sa.cum = g.cum;
     sa.bad_mirror = g.bad_dev;
@@ -1390,6 +1392,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   g.feed_early = !(std::getenv("LSMGNN_FEED_EARLY") && std::atoi(std::getenv("LSMGNN_FEED_EARLY")) == 0);
   if (const char* e = std::getenv("LSMGNN_SERVE_TAIL")) g.serve_tail = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_SERVE_TAIL_ROUNDS")) g.serve_tail_rounds = std::max(0, std::min(64, std::atoi(e)));
+  if (const char* e = std::getenv("LSMGNN_SERVE_AHEAD")) g.serve_ahead = std::atoi(e) != 0;
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));

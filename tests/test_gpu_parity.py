@@ -487,8 +487,9 @@ def test_g1_pull_path(cfg1_g1, monkeypatch, D, st):
     compare(hg, ho, f"g1 pull D{D} st{st}")
 
 
-@pytest.mark.parametrize("st,tail,rounds", [("0", "8", "2"), ("2", "1", "64"), ("8", "32", "2"), ("6", "3", "0")])
-def test_serve_geometry(cfg1_g1, monkeypatch, st, tail, rounds):
+@pytest.mark.parametrize("st,tail,rounds,ahead", [("0", "8", "2", "1"), ("2", "1", "64", "1"), ("8", "32", "2", "0"),
+                                                 ("6", "3", "0", "1"), ("6", "4", "1", "0")])
+def test_serve_geometry(cfg1_g1, monkeypatch, st, tail, rounds, ahead):
     """k_serve's delivery with TMA rings of 2..8 stages per warp (8 is clamped to the shared
     memory) and with 16-B vector copies (LSMGNN_SERVE_ST), and guided chunk sizes down to one
     request (LSMGNN_SERVE_TAIL / _ROUNDS) at 4 KiB rows: identical rows and counters (I9 for the
@@ -497,10 +498,11 @@ def test_serve_geometry(cfg1_g1, monkeypatch, st, tail, rounds):
     monkeypatch.setenv("LSMGNN_SERVE_CPS", "1")
     monkeypatch.setenv("LSMGNN_SERVE_TAIL", tail)
     monkeypatch.setenv("LSMGNN_SERVE_TAIL_ROUNDS", rounds)
+    monkeypatch.setenv("LSMGNN_SERVE_AHEAD", ahead)
     g, tr, sc = cfg1_g1
     kw = dict(N=16384, D=1024, L=1024, A=8, scores=sc, policy="lru", pvp=0, W=8)
     hg, _, bad = run_gpu(tr, **kw)
     ho = run_oracle(tr, G=1, **kw)[:, 0, :]
     assert bad == 0
-    compare(hg, ho, f"serve st{st} tail{tail}/{rounds}")
+    compare(hg, ho, f"serve st{st} tail{tail}/{rounds} ahead{ahead}")
 
