@@ -40,6 +40,7 @@
  *                             per warp (s = 0: 16-B vector copies instead of TMA bulk copies)
  *   LSMGNN_SERVE_TAIL=k, LSMGNN_SERVE_TAIL_ROUNDS=r  delivery chunks of 32 requests, k once
  *                             fewer than r rounds of chunks remain (guided; defaults 4, 2)
+ *   LSMGNN_SERVE_AHEAD=1      keep one delivery chunk in reserve before the tail (A/B; slower)
  *   LSMGNN_FEED_EARLY=0       the window feed waits for the gather before it (default: it
  *                             starts alongside k_serve and waits for it at its end)
  *   LSMGNN_G1_PULL=1          G = 1 profiling aid: the G > 1 serve path (k_fill, k_pull phases,

@@ -1367,11 +1367,12 @@ __global__ void k_serve(ServeArgs a) {
   // Chunks are handed out by a counter (load balance: the hit rows finish together, and a
   // storage-bound batch keeps the delivery-only warps busy while the fills run), with guided
   // sizes: 32 requests, then `tail` once fewer than tail_rounds rounds of 32-request chunks remain,
-  // so the warps finish within a small chunk of each other. In the 32-request phase (a.ahead) a
-  // warp holds the next chunk in reserve: its locations and the counter atomic for the one after
-  // are in flight during the current copy (one ID round trip exposed per chunk instead of three);
-  // the reservation stops in the tail phase, where it would add imbalance. A static chunk order,
-  // and reserving ahead through the tail, measured slower (profiles/r02_hit_path.md).
+  // so the warps finish within a small chunk of each other. a.ahead (off by default) makes a warp
+  // hold the next chunk in reserve in the 32-request phase, its locations and the counter atomic
+  // for the one after in flight during the current copy; like a static chunk order and
+  // reserving through the tail, it measured slower (hit path 0.237 vs 0.227 ms/step; the
+  // reservations unbalance the warps more than the hidden latency gains,
+  // profiles/r02_hit_path.md).
   const uint32_t tail = a.tail_chunk;
   const int64_t tail_from = n - (int64_t)a.tail_rounds * nw * kChunk;
   auto grab = [&](uint32_t sz) -> uint32_t { return lane == 0 ? atomicAdd(&a.scr->pull_next, sz) : 0u; };

@@ -230,7 +230,7 @@ struct Ctx {
   int serve_cps = 2, serve_st = 3;
   int serve_tail = 4;  // LSMGNN_SERVE_TAIL=n: k_serve's delivery chunk size near the batch end (A/B)
   int serve_tail_rounds = 2;  // LSMGNN_SERVE_TAIL_ROUNDS=r: ... once fewer than r rounds of chunks remain
-  bool serve_ahead = true;    // LSMGNN_SERVE_AHEAD=0/1: one chunk in reserve before the tail phase
+  bool serve_ahead = false;   // LSMGNN_SERVE_AHEAD=1: one chunk in reserve before the tail phase (measured slower)
   cudaEvent_t ev_main = nullptr, ev_pvp = nullptr;
   bool pvp_pending = false;
   // cross-stream order (callers may gather and prefetch on different streams): the end of
