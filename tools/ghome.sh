@@ -8,6 +8,9 @@ mkdir -p $CUDA_MPS_PIPE_DIRECTORY $CUDA_MPS_LOG_DIRECTORY
 nvidia-cuda-mps-control -d || echo "(no MPS: ranks time-slice)"
 free -g | head -2
 R="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+timeout 600 $R --nproc-per-node 2 --master-port 29610 tools/ghome_run.py gpurun_out/ghome_smoke.json \
+  --workload igb --nodes 2000000 --lines-per-gpu 65536 --iters 4 --warm 2 > gpurun_out/ghome_smoke.log 2>&1
+echo "smoke rc=$?"; tail -2 gpurun_out/ghome_smoke.log; rm -rf /dev/shm/lsmgnn_ghome
 timeout 1800 $R --nproc-per-node 8 --master-port 29611 tools/ghome_run.py gpurun_out/ghome_igb_16g.json \
   --workload igb --lines-per-gpu 4194304 --policies hybrid,static,lru --max-ids 1600000 > gpurun_out/ghome_igb.log 2>&1
 echo "igb rc=$?"; tail -3 gpurun_out/ghome_igb.log

@@ -49,13 +49,14 @@ def shared_graph(rank, N, dist):
     if rank == 0:
         os.makedirs(SHM, exist_ok=True)
         g = synth.plcite_c(N, 12)
-        np.save(f"{SHM}/indptr.npy", g.indptr)
-        np.save(f"{SHM}/indices.npy", g.indices)
+        g.indptr.tofile(f"{SHM}/indptr.bin")  # raw, so the mapping starts page-aligned
+        g.indices.tofile(f"{SHM}/indices.bin")
         np.save(f"{SHM}/scores.npy", synth.static_scores(g))
         del g
     dist.barrier()
-    indptr = np.load(f"{SHM}/indptr.npy", mmap_mode="r")
-    indices = np.load(f"{SHM}/indices.npy", mmap_mode="r")
+    # shared, writable mappings (cudaHostRegister refuses the read-only mapping np.load gives)
+    indptr = np.memmap(f"{SHM}/indptr.bin", dtype=np.int64, mode="r+")
+    indices = np.memmap(f"{SHM}/indices.bin", dtype=np.int32, mode="r+")
     scores = np.load(f"{SHM}/scores.npy")
     log(f"graph N={N} nnz={indices.size} ready in {time.time() - t0:.0f}s")
     return indptr, indices, scores
