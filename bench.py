@@ -687,14 +687,17 @@ def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0 = None
     # timed steps: no phase events between the kernels (they would cut the programmatic launch chain)
+    h0 = 0.0
     for t in range(warm + steps):
         if t == warm:
             torch.cuda.synchronize()
             s0 = c.stats(1)
             e0.record(st)
+            h0 = time.perf_counter()
         c.gather(ids_d[t], out)
         c.prefetch([ids_d[t + 1 + W]], first_iter=t + 1 + W)
     e1.record(st)
+    host_issue_ms = (time.perf_counter() - h0) * 1e3 / steps  # host time to issue one step
     torch.cuda.synchronize()
     s1 = c.stats(1)
     # then psteps more with phase events: the per-phase split and k_serve's duration for its roofline
@@ -758,6 +761,7 @@ def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, 
             "value": round(d["requests"] * R / T / 1e9, 2), "unit": "GB/s", "ms_per_step": round(T / steps * 1e3, 4),
             "hit_ratio": round(d["hits"] / max(d["unique"], 1), 4), "two_streams": two, "graph_replay": graph,
             "profiled_steps": psteps,
+            "host_issue_ms_per_step": round(host_issue_ms, 4),
             "phases_ms_per_step": {k: round(v[0] / psteps, 4) for k, v in prof.items()},
             "roofline": {"bound": "hbm", "kernel": "k_serve", "achieved": round(ach, 1), "peak": hbm_peak,
                          "unit": "GB/s", "frac": round(ach / hbm_peak, 4), "peak_source": hbm_src,

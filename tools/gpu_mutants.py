@@ -45,7 +45,7 @@ MUTANTS = [
     ("miss_not_listed", "    if (a.head) list_join(a, q, pos, stamp);  // a fill will deliver this row",
      "", "S8 a filled node's first requester receives the row"),
     ("fast_set_cnt_kept", "    if (p.set_cnt[sl] && p.slow_stamp[sl] != stamp_) p.set_cnt[sl] = 0;  // ready for the next batch",
-     "", "S3 the all-hit sets' buckets start empty next batch"),
+     "    ;", "S3 the all-hit sets' buckets start empty next batch"),
     ("hit_counted_twice", "        if (way >= 0) {  // (node_loc and the hit count were written by k_dedup's probe)\n          kind = kHit;",
      "        if (way >= 0) {\n          kind = kHit;\n          ++ctr[C_HIT];", "S9 hits counted once"),
     ("pvp_unused_inverted", "      unused += p.mark[stg[j] / G] != stamp_;", "      unused += p.mark[stg[j] / G] == stamp_;",
@@ -63,6 +63,8 @@ def build():
     out = os.path.join(ROOT, "ab")
     os.makedirs(out, exist_ok=True)
     for name, old, new, _ in MUTANTS:
+        if os.path.exists(os.path.join(out, f"mut_{name}.so")):
+            continue  # (delete ab/ to rebuild everything)
         fname = "device_common.cuh" if name.startswith("dc_") else "kernels.cuh"
         src = open(os.path.join(CSRC, fname)).read()
         assert src.count(old) == 1, name
