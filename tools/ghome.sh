@@ -12,7 +12,7 @@ timeout 600 $R --nproc-per-node 2 --master-port 29610 tools/ghome_run.py gpurun_
   --workload igb --nodes 2000000 --lines-per-gpu 65536 --iters 4 --warm 2 > gpurun_out/ghome_smoke.log 2>&1
 echo "smoke rc=$?"; tail -2 gpurun_out/ghome_smoke.log; rm -rf /dev/shm/lsmgnn_ghome
 timeout 1800 $R --nproc-per-node 8 --master-port 29611 tools/ghome_run.py gpurun_out/ghome_igb_16g.json \
-  --workload igb --lines-per-gpu 4194304 --policies hybrid,static,lru --max-ids 1600000 > gpurun_out/ghome_igb.log 2>&1
+  --workload igb --lines-per-gpu 4194304 --policies ${IGB_POLICIES:-hybrid,static,lru} --max-ids 1600000 > gpurun_out/ghome_igb.log 2>&1
 echo "igb rc=$?"; tail -3 gpurun_out/ghome_igb.log
 timeout 2400 $R --nproc-per-node 4 --master-port 29612 tools/ghome_run.py gpurun_out/ghome_igbh_10pct.json \
   --workload igbh --cache-pct 10 --policies hybrid,static,lru,dynamic > gpurun_out/ghome_igbh.log 2>&1

@@ -126,7 +126,9 @@ def main():
             """this rank's list of iteration k (sampled once, kept compact until its gather)"""
             if k not in bufs:
                 ids = empty
-                if k < K:
+                # igb: every measured iteration sees a full window (batches sampled through K + W,
+                # as tools/cfg4_counts.py did); igbh: the trace ends after two epochs
+                if k < (K + W if not ipe else K):
                     if ipe:
                         ep, te = divmod(k, ipe)
                         lo = (te * G + rank) * B
