@@ -268,6 +268,7 @@ struct DedupArgs {
   const uint32_t* ring_len;
   uint32_t* mask;
   uint32_t MW, Wp1;
+  uint64_t Q;  // home rows (the overflow sweep)
   // S4 hit probe of every distinct node (the cache state is final: the previous k_serve is done):
   // a hit writes node_loc and the way's last use (hits are protected, R10) and is counted here;
   // a node that is not resident marks its set for k_set (slow_stamp[s] = stamp)
@@ -355,9 +356,14 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
     const uint32_t* __restrict__ list = a.ring + (size_t)slot * a.ring_stride;
     const uint32_t nl = a.ring_len[slot];
     const uint32_t m = ~(1u << (slot & 31));
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
-      const uint32_t v = list[i];
-      if (v != kInvalid) atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
+    if (nl == 0xFFFFFFFFu) {  // the slot's list did not fit its ring slot (k_win_gather): sweep
+      for (uint64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < a.Q; q += stride)
+        atomicAnd(&a.mask[q * a.MW + (slot >> 5)], m);
+    } else {
+      for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
+        const uint32_t v = list[i];
+        if (v != kInvalid) atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
+      }
     }
   }
   uint32_t nreq = 0, npeer = 0, nfirst = 0, nhit = 0;
@@ -1433,6 +1439,11 @@ __global__ void k_serve(ServeArgs a) {
 // gather(k - W - 1) (the feed is ordered after that kernel).
 // Copy the inboxes of all sources (window IDs routed to this home) into the ring slot and
 // set each node's reuse bit of the slot.
+// The ring slot holds up to `stride` IDs (the expected per-home share with slack, not the worst
+// case of every rank's whole batch at one home): a longer list is not stored — the slot is marked
+// kRingOverflow and k_dedup then clears the slot's bit for every node of the home (a sweep of one
+// mask word per node) instead of walking the list. The bits themselves are always set.
+constexpr uint32_t kRingOverflow = 0xFFFFFFFFu;
 __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t* __restrict__ inbox_cnt,
                              uint32_t nsrc, uint32_t cap, uint32_t* __restrict__ ring, uint64_t stride,
                              uint32_t* ring_len, const IterState* it, uint32_t G, uint32_t MW,
@@ -1441,17 +1452,20 @@ __global__ void k_win_gather(const uint32_t* __restrict__ inbox, const uint32_t*
   const uint32_t slot_i = it->wslot;
   uint32_t* __restrict__ slot = ring + (size_t)slot_i * stride;
   const uint32_t m = 1u << (slot_i & 31);
+  uint64_t total = 0;
+  for (uint32_t r = 0; r < nsrc; ++r) total += inbox_cnt[r];
+  const bool store = total <= stride;
   uint32_t base = 0;
   for (uint32_t r = 0; r < nsrc; ++r) {
     const uint32_t n = inbox_cnt[r];
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
       const uint32_t v = inbox[(size_t)r * cap + i];
-      slot[base + i] = v;
+      if (store) slot[base + i] = v;
       atomicOr(&mask[(size_t)(v / G) * MW + (slot_i >> 5)], m);
     }
     base += n;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ring_len[slot_i] = base;
+  if (blockIdx.x == 0 && threadIdx.x == 0) ring_len[slot_i] = store ? base : kRingOverflow;
 }
 
 // ------------------------------------------------------------------------------ S11

@@ -141,6 +141,9 @@ struct Ctx {
   uint32_t R = 0, nvec = 0, A = 0, W = 0, T = 0, MW = 0, Wp1 = 0;
   uint64_t L = 0, S = 0, Q = 0, C = 0, cap = 0, ucap = 0, bcap = 0;
   uint64_t BC = 0, BCp = 0;  // per-set bucket capacity (distinct nodes of a set per batch); its pow2
+  // window ring slot capacity: G = 1 cap; G > 1 min(G, 2)·cap — twice a home's expected share of
+  // the G ranks' batches (a fuller slot is swept instead of listed, k_win_gather / k_dedup)
+  uint64_t ring_stride = 0;
   uint64_t pool_rows = 0, stage_base0 = 0, bypass_base = 0;
   uint32_t P = 32, warp_bytes = 0, set_warps = 8;
   int sms = 148;
@@ -643,7 +646,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.direct = G == 1 ? 1u : 0u;
     da.N = g.N;
     da.ring = g.ring;
-    da.ring_stride = g.cap * G;
+    da.ring_stride = g.ring_stride;
+    da.Q = g.Q;
     da.ring_len = g.ring_len;
     da.mask = g.mask;
     da.MW = g.MW;
@@ -871,7 +875,7 @@ int wait_dedup(int64_t t, cudaStream_t st);  // (below)
 int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* n_dev, const int64_t* const* ids_ring,
                   const int64_t* n_ring, uint32_t ring_len, int64_t n_bound, cudaStream_t st) {
   const int G = g.world;
-  const uint64_t stride = g.cap * G;
+  const uint64_t stride = g.ring_stride;
   if (G == 1) {
     if (k_host < 0 || n_dev) {  // graph replay, or a device-resident length: IterState carries the batch
       KLAUNCH(k_win_begin, 1, 32, 0, st, g.it, k_host, ids, n, n_dev, ids_ring, n_ring, ring_len ? ring_len : 1, g.Wp1,
@@ -1186,6 +1190,7 @@ int plan_layout(Ctx& c, int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype,
   // rows q = s, s + S, ...: at most ceil(Q / S) distinct nodes, and at most the batch's)
   const uint64_t maxm = std::min<uint64_t>((c.Q + c.S - 1) / c.S, c.ucap);
   c.BC = maxm;
+  c.ring_stride = c.cap * (uint64_t)std::min(G, 2);
   c.BCp = 32;
   while (c.BCp < maxm) c.BCp <<= 1;
   c.P = 32;
@@ -1308,7 +1313,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     DA(g.g_skey, g.S * g.BCp + 64);
   }
   DA(g.bucket, g.S * g.BC + 32);  // + 32: k_set reads a set's first 32 entries unconditionally
-  DA(g.ring, (size_t)g.Wp1 * g.cap * G);
+  DA(g.ring, (size_t)g.Wp1 * g.ring_stride);
   DA(g.ring_len, g.Wp1);
   DA(g.qcnt, g.W);
   DA(g.qoff, g.W + 1);

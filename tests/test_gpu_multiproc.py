@@ -75,10 +75,12 @@ def test_multiprocess_fuzz(tmp_path, G, split):
 
 
 @pytest.mark.parametrize("G,case,split", [(2, "ragged", 1), (3, "dups", 0), (3, "dups", 1), (2, "period", 1),
-                                          (4, "rr", None), (2, "file", 1), (3, "two_streams", 1)])
+                                          (4, "rr", None), (2, "file", 1), (3, "two_streams", 1), (3, "skew", 1)])
 def test_multiprocess_edge_cases(tmp_path, G, case, split):
     """Ranks with empty batches, cross-rank duplicates, raw lists, victim-queue overflow,
-    reinsert = 0, the periodic update and RR — per-home counters equal the oracle's."""
+    reinsert = 0, the periodic update, RR, and a home whose window slots overflow the ring (every
+    rank's batch homed there: the slot's bits are cleared by a sweep) — per-home counters equal
+    the oracle's."""
     rng = np.random.default_rng(G * 7 + len(case))
     N, D, K = 3000, 4, 18
     sc = rng.integers(0, 256, N).astype(np.uint8)
@@ -88,6 +90,9 @@ def test_multiprocess_edge_cases(tmp_path, G, case, split):
         for r in range(G):
             n = 0 if (case == "ragged" and (t + r) % 3 == 0) else int(rng.integers(1, 400))
             x = rng.zipf(1.2, n) % N if case == "dups" else rng.integers(0, N, n)
+            if case == "skew":  # every ID at home 0 on odd iterations: its window slot overflows the
+                n = 399        # ring (3 ranks x max_batch_ids > 2 x max_batch_ids) and is swept instead
+                x = 3 * rng.integers(0, N // 3, n) if t % 2 else rng.integers(0, N, n)
             row.append(np.asarray(x, np.int64))
         tr.append(row)
     cfg = dict(N=N, D=D, L=64 * 8, A=8, policy="hybrid", pvp=1, W=5, V=5 * 2, reinsert=1, P=1)
