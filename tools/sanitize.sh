@@ -17,6 +17,10 @@ for tool in memcheck racecheck; do
     -k "multi_tile_set_scan and hybrid" > $out/sanitize_${tool}_multitile.log 2>&1
   echo "G=1 multi-tile $tool rc=$? : $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $out/sanitize_${tool}_multitile.log | tail -1) $(grep -Eo '[0-9]+ passed' $out/sanitize_${tool}_multitile.log)" >> $out/sanitize_summary.txt
 done
+# the pipelined file tier (device-published fill list, host preads, per-chunk device waits)
+timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_storage_file.py -q -x \
+  -k "small_rows" > $out/sanitize_memcheck_file.log 2>&1
+echo "G=1 file tier memcheck rc=$? : $(grep -E 'ERROR SUMMARY' $out/sanitize_memcheck_file.log | tail -1) $(grep -Eo '[0-9]+ passed' $out/sanitize_memcheck_file.log)" >> $out/sanitize_summary.txt
 # G = 2: each rank runs under its own compute-sanitizer (torch.distributed env set by hand, so
 # the ranks themselves are instrumented), both pull orders; the ranks' outputs are
 # checked (rows bad = 0)
