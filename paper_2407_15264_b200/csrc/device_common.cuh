@@ -88,7 +88,6 @@ __device__ __forceinline__ void pdl_prologue() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // CTA-wide reservation of one slot per thread with want == true: one atomicAdd per CTA on the
 // shared counter instead of one per warp (a hot single address). Every thread of the CTA must

@@ -351,6 +351,21 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
   const uint32_t stamp = (uint32_t)(t64 + 1);
   unsigned long long* rec = hist + (size_t)(t64 % kHist) * F_NFIELDS;
   const uint32_t stride = gridDim.x * blockDim.x;
+  {  // S10: clear the bits of iteration t (its window list is in ring slot t mod (W+1))
+    const uint32_t slot = (uint32_t)(t64 % a.Wp1);
+    const uint32_t* __restrict__ list = a.ring + (size_t)slot * a.ring_stride;
+    const uint32_t nl = a.ring_len[slot];
+    const uint32_t m = ~(1u << (slot & 31));
+    if (nl == 0xFFFFFFFFu) {  // the slot's list did not fit its ring slot (k_win_gather): sweep
+      for (uint64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < a.Q; q += stride)
+        atomicAnd(&a.mask[q * a.MW + (slot >> 5)], m);
+    } else {
+      for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
+        const uint32_t v = list[i];
+        if (v != kInvalid) atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
+      }
+    }
+  }
   uint32_t nreq = 0, npeer = 0, nfirst = 0, nhit = 0;
   const uint32_t t = (uint32_t)t64;
   if (a.direct) {
@@ -373,22 +388,6 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
         nfirst += dedup_one(in[i], i, a, stamp, t, &nhit);
         ++nreq;
         if (r != a.me) ++npeer;
-      }
-    }
-  }
-  {  // S10: clear the bits of iteration t (its window list is in ring slot t mod (W+1)); after
-     // the dedup work, so that chain starts at once and the clear's loads overlap its tail
-    const uint32_t slot = (uint32_t)(t64 % a.Wp1);
-    const uint32_t* __restrict__ list = a.ring + (size_t)slot * a.ring_stride;
-    const uint32_t nl = a.ring_len[slot];
-    const uint32_t m = ~(1u << (slot & 31));
-    if (nl == 0xFFFFFFFFu) {  // the slot's list did not fit its ring slot (k_win_gather): sweep
-      for (uint64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < a.Q; q += stride)
-        atomicAnd(&a.mask[q * a.MW + (slot >> 5)], m);
-    } else {
-      for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
-        const uint32_t v = list[i];
-        if (v != kInvalid) atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
       }
     }
   }
@@ -665,19 +664,6 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
     }
     m = __shfl_sync(0xffffffffu, m, 0);
     if (lane == 0) p.set_cnt[s] = 0;  // ready for the next batch
-    // bring what the rest of the set's chain reads into L2 while the bucket is sorted: the
-    // staging directory and score of its first 32 nodes (and their mask rows, for bypass keys),
-    // the score and mask row of every resident line (victim keys, reuse classes)
-    if ((uint32_t)lane < m) {
-      const uint32_t qb = b0 / G;
-      prefetch_l2(p.vst_stamp + qb);
-      prefetch_l2(p.score + qb);
-      prefetch_l2(p.mask + (size_t)qb * p.MW);
-    }
-    if (tg != kInvalid) {
-      prefetch_l2(p.score + tg / G);
-      prefetch_l2(p.mask + (size_t)(tg / G) * p.MW);
-    }
     stag[lane] = tg;
     __syncwarp();
     uint32_t Pm = 32;
