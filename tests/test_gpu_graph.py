@@ -74,3 +74,37 @@ def test_gather_and_prefetch_on_different_streams(pvp):
         assert synth.check_rows(rows, tr[t][0], D)[0] == 0, t
     compare(c.history(0, K), ho, f"two streams pvp{pvp}")
     c.close()
+
+
+@pytest.mark.parametrize("pvp", [0, 1])
+def test_gathers_alternate_streams(pvp):
+    """gather(t) on alternating streams (and the feeds on a third): a gather on a new stream
+    first waits for the previous gather (its k_dedup would otherwise reset the per-iteration
+    state and scratch the previous k_serve still uses) — bit-exact rows and counters."""
+    import torch
+    from paper_2407_15264_b200 import LsmGnn
+    N, D, W = 16384, 128, 8
+    g, tr, sc = small_workload(N, 8, G=1, batch=256, fanout=(10, 5), iters=20)
+    K = len(tr)
+    kw = dict(N=N, D=D, L=1024, A=8, scores=sc, policy="hybrid", pvp=pvp, W=W, V=512)
+    ho = run_oracle(tr, G=1, **kw)[:, 0, :]
+    mb = max(len(x[0]) for x in tr)
+    c = LsmGnn(N, D, 1024, 8, 512, sc, policy="hybrid", pvp=pvp, window=W, max_batch_ids=mb)
+    c.attach_storage(table_for(N, D, pinned=True))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    sf = torch.cuda.Stream()
+    ids = [torch.from_numpy(np.asarray(tr[k][0], np.int64)).cuda() if k < K else
+           torch.zeros(0, dtype=torch.int64, device="cuda") for k in range(K + W + 1)]
+    torch.cuda.synchronize()
+    outs = [torch.empty((mb, 4 * D), dtype=torch.uint8, device="cuda") for _ in range(K)]
+    c.prefetch(ids[1:W + 1], first_iter=1, stream=sf)
+    for t in range(K):
+        c.gather(ids[t], outs[t], stream=streams[t % 2])
+        c.prefetch([ids[t + 1 + W]], first_iter=t + 1 + W, stream=sf if t % 3 else streams[t % 2])
+    torch.cuda.synchronize()
+    for t in range(K):
+        n = ids[t].numel()
+        rows = outs[t][:n].cpu().numpy().view(np.uint32).reshape(n, D)
+        assert synth.check_rows(rows, tr[t][0], D)[0] == 0, t
+    compare(c.history(0, K), ho, f"alternating streams pvp{pvp}")
+    c.close()
