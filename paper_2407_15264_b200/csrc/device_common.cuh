@@ -266,6 +266,26 @@ __device__ __forceinline__ void bulk_s2g(void* g, const void* smem, uint32_t byt
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(smem_u32(smem)), "r"(bytes)
                : "memory");
 }
+// The same copies with an L2 eviction-priority policy (createpolicy): the row streams of a step
+// are touched once, so they are loaded and stored evict_first and the metadata the next
+// step's latency-bound kernels walk (tags, stamps, node_loc, reuse masks) stays in L2.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* smem, const void* g, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem)),
+      "l"(g), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* g, const void* smem, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(g),
+               "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most k committed bulk groups still have to READ their shared-memory source
 __device__ __forceinline__ void bulk_wait_read(uint32_t k) {
@@ -297,11 +317,14 @@ struct RowRing {
   uint32_t* pend;  // ST entries: the row index (into dst[]) whose load occupies the stage
   uint32_t ST, R;
   uint32_t nl, ns, phase;  // loads issued, stores issued (lane 0), phase bit per stage
+  uint32_t hint;           // 1: rows moved with the L2 evict_first policy `pol`
+  uint64_t pol;
 };
 __device__ __forceinline__ void ring_init(RowRing& r) {  // lane 0; then __syncwarp
   for (uint32_t s = 0; s < r.ST; ++s) mbar_init(&r.bar[s], 1);
   mbar_fence_init();
   r.nl = r.ns = r.phase = 0;
+  r.pol = r.hint ? l2_policy_evict_first() : 0;
 }
 // Lane 0: copy rows j in `mask` (bit j) from src[j] to dst[j] (R bytes each, 16-B aligned),
 // returning when every store has been issued (its completion is awaited by ring_drain or the
@@ -317,7 +340,8 @@ __device__ __forceinline__ void ring_copy(RowRing& r, const void* const* src, vo
       // the stage's last store (number nl - ST) must have read it; later stores may still read
       if (r.nl >= r.ST) bulk_wait_read(r.ns + r.ST - 1 - r.nl);
       mbar_expect_tx(&r.bar[s], r.R);
-      bulk_g2s(r.buf + (size_t)s * r.R, src[j], r.R, &r.bar[s]);
+      if (r.hint) bulk_g2s_hint(r.buf + (size_t)s * r.R, src[j], r.R, &r.bar[s], r.pol);
+      else bulk_g2s(r.buf + (size_t)s * r.R, src[j], r.R, &r.bar[s]);
       r.pend[s] = j;
       ++r.nl;
       ++issued;
@@ -325,7 +349,8 @@ __device__ __forceinline__ void ring_copy(RowRing& r, const void* const* src, vo
     const uint32_t s = r.ns % r.ST;
     mbar_wait_parity(&r.bar[s], (r.phase >> s) & 1u);
     r.phase ^= 1u << s;
-    bulk_s2g(dst[r.pend[s]], r.buf + (size_t)s * r.R, r.R);
+    if (r.hint) bulk_s2g_hint(dst[r.pend[s]], r.buf + (size_t)s * r.R, r.R, r.pol);
+    else bulk_s2g(dst[r.pend[s]], r.buf + (size_t)s * r.R, r.R);
     bulk_commit();
     ++r.ns;
     ++stored;

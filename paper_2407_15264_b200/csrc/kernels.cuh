@@ -1098,6 +1098,7 @@ struct PullArgs {
   Scratch* scr;  // per-phase chunk counters
   uint32_t G;
   uint32_t ST;  // TMA ring stages per warp (TMA = 1)
+  uint32_t l2ef;  // rows moved with the L2 evict_first policy (RowRing::hint)
   uint32_t tail_chunk, tail_rounds;
 };
 // TMA = 1: rows move (local or peer) HBM -> shared -> `out` with TMA bulk copies through each
@@ -1123,6 +1124,7 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
     ring.bar = s_bar[wib];
     ring.pend = s_pend[wib];
     ring.ST = a.ST;
+    ring.hint = a.l2ef;
     ring.R = nvec * 16;
     if (lane == 0) ring_init(ring);
     __syncwarp();
@@ -1217,6 +1219,7 @@ struct ServeArgs {
   uint32_t ahead;       // keep one 32-request chunk in reserve before the tail phase
   const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
+  uint32_t l2ef;  // rows moved with the L2 evict_first policy (RowRing::hint)
   // S9, closed by the last CTA
   unsigned long long* hist;
   unsigned long long* cum;
@@ -1299,6 +1302,7 @@ __global__ void k_serve(ServeArgs a) {
     ring.bar = s_bar[wib];
     ring.pend = s_pend[wib];
     ring.ST = a.ST;
+    ring.hint = a.l2ef;
     ring.R = nvec * 16;
     if (lane == 0) ring_init(ring);
     __syncwarp();
