@@ -280,7 +280,12 @@ struct DedupArgs {
   Scratch* scr;
   uint32_t A;
 };
-// One request: first occurrence of its node (returns 1) -> into the set's bucket, probed.
+// One request: first occurrence of its node (returns 1) is probed against its set's A tags; a
+// hit writes node_loc and the way's last use (= t: hits are protected, R10, and k_set reads the
+// protection from last_use), a miss goes into the set's bucket (the bucket holds the batch's
+// MISSES only: k_set works on those and on the resident lines).
+// The tag loads are issued with the stamp exchange (speculatively for a repeated occurrence, one
+// extra 128-B read), so a hit costs two dependent round trips: IDs, then stamp + tags.
 // G = 1: request position pos joins node q's list (head[q] = stamp<<32 | pos, nxt[pos] = previous)
 // — the positions a fill of q delivers its row to (k_serve). A hit is delivered through node_loc,
 // so the FIRST occurrence of a hit node never needs to be on the list (the common case skips the
@@ -289,24 +294,31 @@ __device__ __forceinline__ void list_join(const DedupArgs& a, uint32_t q, uint32
   const unsigned long long old = atomicExch(&a.head[q], ((unsigned long long)stamp << 32) | pos);
   a.nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
 }
+// 16-byte load that the compiler may neither drop nor sink into the branch that uses it
+__device__ __forceinline__ uint4 ld16_issue(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, uint32_t stamp,
                                               uint32_t t, uint32_t* nhit) {
   const uint32_t q = v / a.G;
+  const uint32_t s = q % a.S;
+  const uint32_t* tg = a.tags + (size_t)s * a.A;
+  const bool vec = (a.A & 3u) == 0;  // a set's tags are whole 16-B words (A = 4, 8, ..., 32)
+  uint4 w[8];
+  if (vec) {
+    const uint4* t4 = reinterpret_cast<const uint4*>(tg);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = 4u * i < a.A ? ld16_issue(t4 + i) : make_uint4(kInvalid, kInvalid, kInvalid, kInvalid);
+  }
   const bool first = atomicExch(&a.mark[q], stamp) != stamp;
   if (!first) {
     if (a.head) list_join(a, q, pos, stamp);
     return 0;
   }
-  const uint32_t s = q % a.S;
-  // the bucket slot and the probe of the set's A ways are independent: one round trip
-  const uint32_t slot = atomicAdd(&a.set_cnt[s], 1u);
-  const uint32_t* tg = a.tags + (size_t)s * a.A;
   int way = -1;
-  if (a.A == 32) {
-    const uint4* t4 = reinterpret_cast<const uint4*>(tg);
-    uint4 w[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w[i] = t4[i];
+  if (vec) {
 #pragma unroll
     for (int i = 7; i >= 0; --i) {
       if (w[i].w == v) way = 4 * i + 3;
@@ -318,12 +330,13 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
     for (uint32_t k = 0; k < a.A; ++k)
       if (tg[k] == v) way = (int)k;
   }
-  a.bucket[(size_t)s * a.BC + slot] = v;
   if (way >= 0) {
     a.node_loc[q] = s * a.A + (uint32_t)way;
     a.last_use[s * a.A + (uint32_t)way] = t;
     ++*nhit;
   } else {
+    const uint32_t slot = atomicAdd(&a.set_cnt[s], 1u);
+    a.bucket[(size_t)s * a.BC + slot] = v;
     if (a.head) list_join(a, q, pos, stamp);  // a fill will deliver this row
     if (a.slow_stamp[s] != stamp && atomicExch(&a.slow_stamp[s], stamp) != stamp)
       a.slow_list[atomicAdd(&a.scr->nslow, 1u)] = s;  // first miss of the set: k_set processes it
@@ -644,11 +657,10 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
   }
 
   // A set whose nodes all hit was fully handled by k_dedup's probe (node_loc, last use, hit
-  // count): its counter is only reset here (sets scanned 32 per warp iteration, lane = set).
-  // The sets with a miss (k_dedup's slow list) are processed by one warp each.
+  // count) and has an empty bucket. The sets with a miss (k_dedup's slow list) are processed by
+  // one warp each: the bucket holds the set's misses, and its hits are the resident lines whose
+  // last use is t (written by the probe).
   const uint32_t gwarp = blockIdx.x * nwb + wib, nwarps = gridDim.x * nwb;
-  for (uint32_t sl = gwarp * 32 + lane; sl < p.S; sl += nwarps * 32)
-    if (p.set_cnt[sl] && p.slow_stamp[sl] != stamp_) p.set_cnt[sl] = 0;  // ready for the next batch
   const uint32_t nslow = p.scr->nslow;
   for (uint32_t i = gwarp; i < nslow; i += nwarps) {
     const uint32_t s = p.slow_list[i];
@@ -686,34 +698,27 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
     __syncwarp();
     warp_bitonic_sort(sv, (int)Pm);  // nodes ascending (R10: misses installed in node order)
 
-    // ---- probe (S4): tag compare, then the PVP staging directory
-    uint32_t protm = 0;
+    // ---- probe (S4): the hits were found by k_dedup's tag probe, which set their ways' last
+    // use to t (protected, R10); the bucket's misses are looked up in the PVP staging directory
+    const uint32_t protm = __ballot_sync(0xffffffffu, lane < A && tg != kInvalid && lu == t_);
     const uint32_t mr = (m + 31) & ~31u;
     for (uint32_t j = lane; j < mr; j += 32) {
       if (j < m) {
         const uint32_t v = sv[j], q = v / G;
-        int way = -1;
-        for (uint32_t w = 0; w < A; ++w)
-          if (stag[w] == v) way = (int)w;
-        uint32_t kind, inM;
-        if (way >= 0) {  // (node_loc and the hit count were written by k_dedup's probe)
-          kind = kHit;
-          protm |= 1u << way;
-        } else if (p.vst_stamp[q] == stamp_) {
+        uint32_t kind;
+        if (p.vst_stamp[q] == stamp_) {
           kind = kVHit;
           ++ctr[C_VHIT];
         } else {
           kind = kStorage;
           ++ctr[C_STOR];
         }
-        inM = kind != kHit && (kind == kStorage || p.reinsert);
-        sk[j] = kind | ((uint32_t)(way & 0xff) << 2) | (inM << 10);
+        const uint32_t inM = kind == kStorage || p.reinsert;
+        sk[j] = kind | (inM << 10);
       }
     }
-    protm = __reduce_or_sync(0xffffffffu, protm);
     __syncwarp();
     const uint32_t nH = __popc(protm);
-    if ((protm >> lane) & 1u) p.last_use[s * A + lane] = t_;  // hits are protected, last use = t
 
     // ---- M = misses to insert, ascending node order
     uint32_t nM = 0;
