@@ -274,7 +274,7 @@ int lsmgnn_graph_replay(void* stream);
 int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope);
 
 /* Per-iteration records for iterations [first, first+count) (kept on the device in a
- * ring; the last 4095 iterations are available). Synchronous. */
+ * ring; the last 4094 iterations are available). Synchronous. */
 int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count);
 
 /* Debug/inspection (tests): copy a piece of this home's cache state to host memory after

@@ -41,21 +41,21 @@ struct Cand {
 };
 
 // Per-batch scratch counters (u32, device).
+// (unique nodes and requests are counted straight into the iteration's record by k_dedup)
 struct Scratch {
-  uint32_t nuniq;      // unique nodes at this home
-  uint32_t nfill;      // FillEnt entries
-  uint32_t ncand;      // victim candidates
-  uint32_t nbypass;    // bypass-staging rows used
+  uint32_t nfill[2];   // FillEnt entries, by iteration parity (k_set of t + 1 may run while k_serve
+                       // of t still reads its list: k_dedup/k_set `early`)
+  uint32_t ncand;      // victim candidates (PVP: never early)
+  uint32_t nbypass[2]; // bypass-staging rows used, by iteration parity
   uint32_t bad_ids;    // sticky count of node IDs >= N (ERANGE)
-  uint32_t nreq;       // requests routed to this home
   uint32_t staged[2];  // rows the PVP staged, by iteration parity
   uint32_t pvp_done;   // grid-completion counter of the PVP kernel
   uint32_t pull_next;  // k_serve: next request index handed to a delivering warp
   uint32_t serve_done; // k_serve: CTAs finished (the last one closes the record)
   uint32_t io_done;    // k_io_export: CTAs finished (the last one publishes the list)
-  uint32_t nslow;      // sets with a miss this batch (k_dedup's slow list)
+  uint32_t nslow[2];   // sets with a miss (k_dedup's slow list), by iteration parity: k_dedup(t+1)
+                       // may count while gather t closes (k_dedup `early`)
   uint32_t pull_phase_next[2];  // k_pull: next request index per phase
-  uint32_t pad[1];
 };
 
 // Per-iteration values, resident on the device. k_begin / k_win_begin write them (from host
@@ -76,7 +76,12 @@ struct IterState {
   const int64_t* wids;
   int64_t wn;
   uint32_t wslot;             // wk mod (W+1): ring slot and mask bit
-  uint32_t done;              // grid-completion counter (k_mask_clear)
+  // G = 1 window feeds: CTAs of k_route_local that finished their work (monotonic; the host
+  // counts the CTAs it launched, and an early k_set waits for that many, kernels.cuh k_set)
+  unsigned long long feed_ctas_done;
+  // G = 1 direct gathers: CTAs of k_dedup that finished (monotonic, counted the same way)
+  unsigned long long dedup_ctas_done;
+  unsigned long long set_ctas_done;  // ... and of early k_set launches
 };
 
 // Programmatic dependent launch (PDL): a kernel launched with programmatic stream
@@ -193,6 +198,13 @@ __device__ __forceinline__ int next_reuse_d_seq(const uint32_t* row, int p0, int
   pos = first_bit_in(row, 0, end2);
   if (pos >= 0) return (Wp1 - p0) + pos + 1;
   return 0;
+}
+
+// Acquire load of a 64-bit device counter (spin-waits on flags another kernel publishes).
+__device__ __forceinline__ uint64_t ld_acquire_u64(const void* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // 16-byte vector copies.

@@ -22,6 +22,21 @@
 
 namespace lsm {
 
+// Build-time timeline probe (nvcc -DLSMGNN_TRACE, experiments only, never in the product build):
+// per kernel and iteration parity, the earliest CTA start and the latest CTA end (%globaltimer).
+#ifdef LSMGNN_TRACE
+__device__ unsigned long long g_trace[8][2][2];
+__device__ __forceinline__ unsigned long long trace_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE_AT(k, par, e) \
+  do { if (threadIdx.x == 0) { if (e) atomicMax(&g_trace[k][par][1], trace_now()); else atomicMin(&g_trace[k][par][0], trace_now()); } } while (0)
+#else
+#define TRACE_AT(k, par, e) do { } while (0)
+#endif
+
 // ------------------------------------------------------------------------------ S9
 // Start gather t: publish the iteration's values (IterState), zero its record and the per-batch
 // scratch counters. t_host >= 0: t and the batch come from the
@@ -98,11 +113,11 @@ struct EndArgs {
   uint32_t R;
   volatile uint32_t* bad_mirror;
 };
-__device__ __forceinline__ void end_record(IterState* it, unsigned long long* hist, unsigned long long* cum,
+__device__ __forceinline__ void end_record(uint64_t t, IterState* it, unsigned long long* hist, unsigned long long* cum,
                                            Scratch* scr, uint32_t R, volatile uint32_t* bad_mirror);
 __global__ void k_end(EndArgs a) {
   pdl_prologue();
-  end_record(a.it, a.hist, a.cum, a.scr, a.R, a.bad_mirror);
+  end_record(a.it->t, a.it, a.hist, a.cum, a.scr, a.R, a.bad_mirror);
 }
 
 // Start the window feed of one batch (iteration wk): k_host >= 0 from the host, else (graph
@@ -145,8 +160,8 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
 // k_serve(t) could trigger this launch), and the caller's IDs were produced before gather(t) (a
 // kernel or copy of the caller's in between is not a programmatic predecessor: no early start).
 // So it runs alongside k_serve(t) on the SMs k_serve leaves free, and waits for k_serve(t) only
-// at its END: the launch completes after k_serve(t) did, so the programmatic wait of k_dedup(t+1)
-// still covers gather t.
+// at its END (in one CTA): the launch completes after k_serve(t) did, so the programmatic wait of
+// k_dedup(t+1) still covers gather t, and so does any later work the caller puts on the stream.
 __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host, uint32_t Wp1,
                               uint64_t N, uint32_t* __restrict__ ring, uint64_t stride, uint32_t* __restrict__ ring_len,
                               Scratch* scr, uint32_t* __restrict__ mask, uint32_t MW, uint32_t wait_prev) {
@@ -165,6 +180,7 @@ __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_
     slot = it->wslot;
   }
   uint32_t* __restrict__ list = ring + (size_t)slot * stride;
+  TRACE_AT(4, (uint32_t)(k_host & 1), 0);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t x = ids[i];
     if (x >= 0 && (uint64_t)x < N) {
@@ -180,7 +196,21 @@ __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_
     // (feeds of consecutive iterations may overlap: the latest one wins)
     if (k_host >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&it->wk_next), (unsigned long long)k_host + 1);
   }
-  if (!wait_prev && k_host >= 0) asm volatile("griddepcontrol.wait;" ::: "memory");  // complete after k_serve(t)
+  // complete after k_serve(t): one CTA waits, the others exit and free their SM slots (for the
+  // early k_dedup of gather t + 1)
+  TRACE_AT(4, (uint32_t)(k_host & 1), 1);
+  // early feed (behind a G = 1 gather): this CTA's list entries and bits are written — count it
+  // (an early k_set waits for the count of the early feeds the host launched; a feed that is not
+  // early is followed by a gather that is not early either)
+  if (!wait_prev && k_host >= 0) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&it->feed_ctas_done, 1ull);
+    }
+  }
+  if (!wait_prev && k_host >= 0 && blockIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------ S1 (G > 1)
@@ -249,8 +279,9 @@ __global__ void k_route_publish(const uint32_t* route_cnt, PublishArgs a) {
 // gather(t) reads iterations t+1..t+W only, and gather(t-1), the last reader of those bits,
 // has completed; the feed of t+1+W (which rewrites the slot) is ordered after this kernel.
 struct DedupArgs;
-__device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, uint32_t stamp,
-                                              uint32_t t, uint32_t* nhit);
+struct DedupPar;
+__device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, const DedupPar& pp,
+                                              uint32_t stamp, uint32_t t, uint32_t* nhit);
 struct DedupArgs {
   const uint32_t* inbox;
   const uint32_t* inbox_cnt;
@@ -258,8 +289,8 @@ struct DedupArgs {
   uint32_t* mark;
   uint32_t* bucket;
   uint32_t* set_cnt;
-  unsigned long long* head;  // G = 1: request lists of the fused delivery
-  uint32_t* nxt;
+  unsigned long long* head;  // G = 1: request lists of the fused delivery (two parities of Q entries)
+  uint32_t* nxt;             // (two parities of cap entries)
   uint32_t direct;
   uint64_t N;
   // window slot of iteration t: its list and the reuse mask (bit t mod (W+1) is cleared)
@@ -275,10 +306,18 @@ struct DedupArgs {
   const uint32_t* tags;
   uint32_t* last_use;
   uint32_t* node_loc;
+  uint64_t loc_stride;  // G = 1: node_loc has one table per iteration parity (Q apart); G > 1: 0
   uint32_t* slow_stamp;
-  uint32_t* slow_list;  // the sets with a miss this batch (count scr->nslow)
-  Scratch* scr;
+  uint32_t* slow_list;  // the sets with a miss this batch (count scr->nslow[t & 1])
   uint32_t A;
+};
+// The tables of iteration t's parity: with `early` (below) k_dedup(t+1) runs while k_serve(t)
+// still reads node_loc, the request lists and its counters of parity t & 1.
+struct DedupPar {
+  uint32_t* node_loc;
+  unsigned long long* head;
+  uint32_t* nxt;
+  uint32_t* nslow;
 };
 // One request: first occurrence of its node (returns 1) is probed against its set's A tags; a
 // hit writes node_loc and the way's last use (= t: hits are protected, R10, and k_set reads the
@@ -290,9 +329,9 @@ struct DedupArgs {
 // — the positions a fill of q delivers its row to (k_serve). A hit is delivered through node_loc,
 // so the FIRST occurrence of a hit node never needs to be on the list (the common case skips the
 // atomic); later occurrences join it before they know whether the node hit (harmless).
-__device__ __forceinline__ void list_join(const DedupArgs& a, uint32_t q, uint32_t pos, uint32_t stamp) {
-  const unsigned long long old = atomicExch(&a.head[q], ((unsigned long long)stamp << 32) | pos);
-  a.nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
+__device__ __forceinline__ void list_join(const DedupPar& pp, uint32_t q, uint32_t pos, uint32_t stamp) {
+  const unsigned long long old = atomicExch(&pp.head[q], ((unsigned long long)stamp << 32) | pos);
+  pp.nxt[pos] = (uint32_t)(old >> 32) == stamp ? (uint32_t)old : kInvalid;
 }
 // 16-byte load that the compiler may neither drop nor sink into the branch that uses it
 __device__ __forceinline__ uint4 ld16_issue(const uint4* p) {
@@ -300,8 +339,8 @@ __device__ __forceinline__ uint4 ld16_issue(const uint4* p) {
   asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
-__device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, uint32_t stamp,
-                                              uint32_t t, uint32_t* nhit) {
+__device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, const DedupPar& pp,
+                                              uint32_t stamp, uint32_t t, uint32_t* nhit) {
   const uint32_t q = v / a.G;
   const uint32_t s = q % a.S;
   const uint32_t* tg = a.tags + (size_t)s * a.A;
@@ -314,7 +353,7 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
   }
   const bool first = atomicExch(&a.mark[q], stamp) != stamp;
   if (!first) {
-    if (a.head) list_join(a, q, pos, stamp);
+    if (pp.head) list_join(pp, q, pos, stamp);
     return 0;
   }
   int way = -1;
@@ -331,22 +370,34 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
       if (tg[k] == v) way = (int)k;
   }
   if (way >= 0) {
-    a.node_loc[q] = s * a.A + (uint32_t)way;
+    pp.node_loc[q] = s * a.A + (uint32_t)way;
     a.last_use[s * a.A + (uint32_t)way] = t;
     ++*nhit;
   } else {
     const uint32_t slot = atomicAdd(&a.set_cnt[s], 1u);
     a.bucket[(size_t)s * a.BC + slot] = v;
-    if (a.head) list_join(a, q, pos, stamp);  // a fill will deliver this row
+    if (pp.head) list_join(pp, q, pos, stamp);  // a fill will deliver this row
     if (a.slow_stamp[s] != stamp && atomicExch(&a.slow_stamp[s], stamp) != stamp)
-      a.slow_list[atomicAdd(&a.scr->nslow, 1u)] = s;  // first miss of the set: k_set processes it
+      a.slow_list[atomicAdd(pp.nslow, 1u)] = s;  // first miss of the set: k_set processes it
   }
   return 1;
 }
-__global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long long* hist, BeginArgs ba,
-                        uint32_t fused_begin) {
+// early = 1 (the host sets it for a direct G = 1 gather whose programmatic predecessor on the
+// stream is the k_serve of gather t - 1, or the early window feed that followed it): no wait at
+// the start. Everything this launch reads is final once k_serve(t-1) has started — the cache
+// state (k_set(t-1) completed before k_serve(t-1) could trigger), the caller's IDs (produced
+// before gather(t-1) or by a non-programmatic predecessor), the window slot of t — and what it
+// writes is not read by k_serve(t-1): node_loc, the request lists and the slow-set counter are
+// parity-indexed, the record of t is its own, and k_serve(t-1) copied IterState before it let
+// this launch start. So the dedup and hit probe of t run alongside the delivery of t-1 and so
+// does k_set(t) behind it (it waits only for the window feeds issued before gather t, and writes
+// nothing k_serve(t-1) reads: fill list, counters and node_loc are parity-indexed); k_serve(t)
+// then waits for k_serve(t-1)'s published t_next before it fills any slot.
+__global__ void __launch_bounds__(256, 4) k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long long* hist, BeginArgs ba,
+                        uint32_t fused_begin, uint32_t early) {
   // (every thread reaches the __syncthreads below: no early exit before it)
-  pdl_prologue();
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   uint64_t t64;
   const int64_t* ids_b;
   int64_t n_b;
@@ -364,6 +415,13 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
   const uint32_t stamp = (uint32_t)(t64 + 1);
   unsigned long long* rec = hist + (size_t)(t64 % kHist) * F_NFIELDS;
   const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t par = (uint32_t)(t64 & 1);
+  DedupPar pp;
+  pp.node_loc = a.node_loc + par * a.loc_stride;
+  pp.head = a.head ? a.head + (size_t)par * a.Q : nullptr;
+  pp.nxt = a.nxt ? a.nxt + (size_t)par * a.cap : nullptr;
+  pp.nslow = &scr->nslow[par];
+  TRACE_AT(0, par, 0);
   {  // S10: clear the bits of iteration t (its window list is in ring slot t mod (W+1))
     const uint32_t slot = (uint32_t)(t64 % a.Wp1);
     const uint32_t* __restrict__ list = a.ring + (size_t)slot * a.ring_stride;
@@ -387,7 +445,7 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
       const int64_t x = ids[i];
       if (x >= 0 && (uint64_t)x < a.N) {
-        nfirst += dedup_one((uint32_t)x, (uint32_t)i, a, stamp, t, &nhit);
+        nfirst += dedup_one((uint32_t)x, (uint32_t)i, a, pp, stamp, t, &nhit);
         ++nreq;
       } else {
         atomicAdd(&scr->bad_ids, 1u);
@@ -398,7 +456,7 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
       const uint32_t n = a.inbox_cnt[r];
       const uint32_t* in = a.inbox + (size_t)r * a.cap;
       for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        nfirst += dedup_one(in[i], i, a, stamp, t, &nhit);
+        nfirst += dedup_one(in[i], i, a, pp, stamp, t, &nhit);
         ++nreq;
         if (r != a.me) ++npeer;
       }
@@ -421,10 +479,21 @@ __global__ void k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long 
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (s_cnt[0]) atomicAdd(&scr->nreq, s_cnt[0]);
-    if (s_cnt[1]) atomicAdd(&scr->nuniq, s_cnt[1]);
+    if (s_cnt[0]) atomicAdd(&rec[F_REQ], (unsigned long long)s_cnt[0]);
+    if (s_cnt[1]) atomicAdd(&rec[F_UNIQUE], (unsigned long long)s_cnt[1]);
     if (s_cnt[2]) atomicAdd(&rec[F_HIT], (unsigned long long)s_cnt[2]);
     if (s_cnt[3]) atomicAdd(&rec[F_PEER], (unsigned long long)s_cnt[3]);
+  }
+  TRACE_AT(0, par, 1);
+  // early: this CTA's stores are done — count it (the early k_set of this gather waits for the
+  // count of the early k_dedup CTAs the host launched)
+  if (early) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&it->dedup_ctas_done, 1ull);
+    }
   }
 }
 
@@ -551,13 +620,17 @@ struct SetParams {
   const uint8_t* score;
   const uint32_t* mask;
   uint32_t* node_loc;
+  uint64_t loc_stride;  // G = 1: one node_loc table per iteration parity (Q apart); G > 1: 0
   const uint32_t* vst_stamp;
   const uint32_t* vst_idx;
-  FillEnt* fills;
+  FillEnt* fills;        // two parities of fstride entries
+  uint64_t fstride;
+  uint64_t dedup_wait;   // early: k_dedup CTAs (cumulative) that must have finished; 0 = not early
+  uint64_t feed_wait;    // early: window-feed CTAs (cumulative) that must have finished
   Cand* cands;
   uint32_t* qcnt;        // per-queue candidate counts (pvp = 1), zero on entry
   Scratch* scr;
-  const IterState* it;       // t, stamp, p0, staging parity, record of this iteration
+  IterState* it;             // t, stamp, p0, staging parity, record of this iteration (early: done counter)
   unsigned long long* hist;
   uint32_t S, A, G, W, T, MW;
   uint32_t policy, pvp, reinsert;
@@ -618,7 +691,21 @@ __device__ __forceinline__ uint64_t policy_key(const SetParams& p, uint32_t v, u
 }
 
 __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
-  pdl_prologue();
+  // early (dedup_wait > 0; kernels.cuh k_dedup): this launch may run while k_serve of the
+  // previous gather still delivers. A programmatic wait would also wait for that k_serve (stream
+  // work completes in order), so it is replaced by two counters: the CTAs of this gather's
+  // k_dedup that finished (their IterState, buckets and node_loc are then visible), and the CTAs
+  // of every window feed issued before this gather (the reuse bits it reads). Everything written
+  // here is parity-indexed or not read by k_serve.
+  if (p.dedup_wait) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0) {
+      while (ld_acquire_u64(&p.it->dedup_ctas_done) < p.dedup_wait) __nanosleep(64);
+      while (ld_acquire_u64(&p.it->feed_ctas_done) < p.feed_wait) __nanosleep(64);
+    }
+  } else {
+    pdl_prologue();
+  }
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_ctr[C_N];
   const uint32_t lane = lane_id();
@@ -638,6 +725,12 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
   // per-iteration values (device-resident, written by k_begin)
   const uint32_t t_ = (uint32_t)p.it->t, stamp_ = p.it->stamp, p0_ = p.it->p0, stage_base_ = p.it->stage_base;
   unsigned long long* rec_ = p.hist + (size_t)p.it->rec_idx * F_NFIELDS;
+  const uint32_t par_ = p.it->par;
+  uint32_t* const node_loc_ = p.node_loc + par_ * p.loc_stride;  // this iteration's parity (k_dedup)
+  FillEnt* const fills_ = p.fills + (size_t)par_ * p.fstride;
+  uint32_t* const nfill_ = &p.scr->nfill[par_];
+  uint32_t* const nbypass_ = &p.scr->nbypass[par_];
+  TRACE_AT(2, par_, 0);
   const bool upd = p.it->upd != 0;  // exact information for incoming misses
 
   uint32_t ctr[C_N];
@@ -646,7 +739,7 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
   const uint32_t A = p.A, G = p.G;
 
   if (p.stg_nodes) {  // pvp_unused (§8(b)): staged rows whose node this batch did not request
-    const uint32_t par = p.it->par;
+    const uint32_t par = par_;
     const uint32_t* stg = p.stg_nodes + (size_t)par * p.C;
     const uint32_t ns = p.scr->staged[par];
     uint32_t unused = 0;
@@ -661,7 +754,7 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
   // one warp each: the bucket holds the set's misses, and its hits are the resident lines whose
   // last use is t (written by the probe).
   const uint32_t gwarp = blockIdx.x * nwb + wib, nwarps = gridDim.x * nwb;
-  const uint32_t nslow = p.scr->nslow;
+  const uint32_t nslow = p.scr->nslow[par_];
   for (uint32_t i = gwarp; i < nslow; i += nwarps) {
     const uint32_t s = p.slow_list[i];
     uint32_t m = lane == 0 ? p.set_cnt[s] : 0u;
@@ -857,7 +950,7 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
           ++ctr[C_ENR];
         }
       }
-      const uint32_t fidx = warp_reserve(&p.scr->nfill, act ? 1u : 0u);
+      const uint32_t fidx = warp_reserve(nfill_, act ? 1u : 0u);
       const uint32_t cidx = warp_reserve(&p.scr->ncand, is_cand ? 1u : 0u);
       if (act) {
         const uint32_t slot = s * A + way;
@@ -866,8 +959,8 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
         f.dst = slot;
         f.victim = kInvalid;
         f.node = v;
-        p.fills[fidx] = f;
-        p.node_loc[q] = slot | p.deliver;
+        fills_[fidx] = f;
+        node_loc_[q] = slot | p.deliver;
         p.tags[slot] = v;
         p.last_use[slot] = t_;
         if (p.period > 1) p.line_info[slot] = kInfoFresh;
@@ -895,19 +988,19 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
         const uint32_t kind = info & 3u;
         const bool inM = (info >> 10) & 1u, byp = (info >> 11) & 1u;
         v = sv[j];
-        if (kind == kVHit && (!inM || byp)) p.node_loc[v / G] = stage_base_ + p.vst_idx[v / G];
+        if (kind == kVHit && (!inM || byp)) node_loc_[v / G] = stage_base_ + p.vst_idx[v / G];
         bs = kind == kStorage && byp;
       }
-      const uint32_t b = warp_reserve(&p.scr->nbypass, bs ? 1u : 0u);
-      const uint32_t fidx = warp_reserve(&p.scr->nfill, bs ? 1u : 0u);
+      const uint32_t b = warp_reserve(nbypass_, bs ? 1u : 0u);
+      const uint32_t fidx = warp_reserve(nfill_, bs ? 1u : 0u);
       if (bs) {
         FillEnt f;
         f.src = kHostBit | (v / G);
         f.dst = p.bypass_base + b;
         f.victim = kInvalid;
         f.node = v;
-        p.fills[fidx] = f;
-        p.node_loc[v / G] = (p.bypass_base + b) | p.deliver;
+        fills_[fidx] = f;
+        node_loc_[v / G] = (p.bypass_base + b) | p.deliver;
       }
     }
     __syncwarp();
@@ -921,6 +1014,15 @@ __global__ void __launch_bounds__(256, 4) k_set(SetParams p) {
   }
   __syncthreads();
   if (threadIdx.x < C_N && s_ctr[threadIdx.x]) atomicAdd(&rec_[kCtrField[threadIdx.x]], s_ctr[threadIdx.x]);
+  TRACE_AT(2, par_, 1);
+  if (p.dedup_wait) {  // early: count this CTA done (the early k_serve of this gather waits for it)
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&p.it->set_ctas_done, 1ull);
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------ S5: admission
@@ -942,7 +1044,7 @@ __global__ void k_qscatter(const Cand* __restrict__ cands, const Scratch* scr, u
 __global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, const uint32_t* __restrict__ qoff,
                                                const uint32_t* __restrict__ qb, uint32_t* __restrict__ qlen,
                                                uint32_t* __restrict__ qnode, uint32_t* __restrict__ qreuse,
-                                               FillEnt* __restrict__ fills, uint32_t C, const IterState* it,
+                                               FillEnt* __restrict__ fills, uint64_t fstride, uint32_t C, const IterState* it,
                                                unsigned long long* rec_hist) {
   pdl_prologue();
   __shared__ uint32_t hist[256];
@@ -994,7 +1096,7 @@ __global__ void __launch_bounds__(256) k_admit(const Cand* __restrict__ cands, c
       const uint32_t slot = len0 + atomicAdd(&s_taken, 1u);
       qnode[(size_t)k * C + slot] = c.x;
       qreuse[(size_t)k * C + slot] = c.reuse;
-      fills[c.fill].victim = k * C + slot;
+      fills[(size_t)it->par * fstride + c.fill].victim = k * C + slot;
       ++adm;
     }
   }
@@ -1030,10 +1132,11 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const volatile uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(volatile uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__global__ void k_io_export(const FillEnt* __restrict__ fills, Scratch* scr, const IterState* it,
+__global__ void k_io_export(const FillEnt* __restrict__ fills_base, uint64_t fstride, Scratch* scr, const IterState* it,
                             IoShared* io, uint32_t* io_src) {
   pdl_prologue();
-  const uint32_t n = scr->nfill;
+  const uint32_t n = scr->nfill[it->par];
+  const FillEnt* __restrict__ fills = fills_base + (size_t)it->par * fstride;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const uint32_t src = fills[e].src;
     io_src[e] = (src & kHostBit) ? (src & ~kHostBit) : kInvalid;
@@ -1068,11 +1171,12 @@ __device__ __forceinline__ void io_wait(const uint32_t* ready, uint32_t e, uint3
 // (eviction D2H), then the new row from the backing table (zero-copy over PCIe,
 // P:249 "directly fetched by GPU threads") or from PVP staging into the slot.
 template <int UNROLL>
-__global__ void k_fill(const FillEnt* __restrict__ fills, const Scratch* scr, uint4* __restrict__ pool,
+__global__ void k_fill(const FillEnt* __restrict__ fills_base, uint64_t fstride, const Scratch* scr, uint4* __restrict__ pool,
                        const uint4* __restrict__ table, uint4* __restrict__ hostq, uint32_t nvec,
                        uint32_t bounce, const uint32_t* io_ready, const IterState* it) {
   pdl_prologue();
-  const uint32_t n = scr->nfill;
+  const uint32_t n = scr->nfill[it->par];
+  const FillEnt* __restrict__ fills = fills_base + (size_t)it->par * fstride;
   const uint32_t stamp = it->stamp;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1105,6 +1209,7 @@ struct PullArgs {
   uint32_t ST;  // TMA ring stages per warp (TMA = 1)
   uint32_t l2ef;  // rows moved with the L2 evict_first policy (RowRing::hint)
   uint32_t tail_chunk, tail_rounds;
+  uint64_t loc_stride;  // G = 1 (LSMGNN_G1_PULL): node_loc table of the iteration's parity
 };
 // TMA = 1: rows move (local or peer) HBM -> shared -> `out` with TMA bulk copies through each
 // warp's ring of ST stages (the source of a peer row is its IPC mapping: over NVLink on
@@ -1119,6 +1224,7 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
   __shared__ void* s_dst[8][32];
   const int64_t* __restrict__ ids = it->ids;
   const int64_t n = it->n;
+  const uint64_t loc_off = (uint64_t)it->par * a.loc_stride;
   const int lane = (int)lane_id();
   const uint32_t wib = threadIdx.x >> 5;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1155,7 +1261,7 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
       if (x >= 0 && (uint64_t)x < N) {
         const uint32_t v = (uint32_t)x;
         g = v % a.G;
-        loc = a.node_loc[g][v / a.G];
+        loc = a.node_loc[g][loc_off + v / a.G];
         valid = true;
       }
     }
@@ -1206,17 +1312,24 @@ __global__ void k_pull(const IterState* it, uint64_t N, PullArgs a, uint4* __res
 // by shared memory, not registers. TMA = 0: 16-byte vector loads/stores (pinned host `out`).
 // The last CTA to finish closes the iteration's record (S9, end_record).
 struct ServeArgs {
-  const FillEnt* fills;
+  const FillEnt* fills;  // two parities of fstride entries
+  uint64_t fstride;
+  uint64_t set_wait;     // early: k_set CTAs (cumulative) that must have finished; 0 = not early
+  int64_t t_host;        // direct call: the iteration and its batch (graph replay: -1, from IterState)
+  const int64_t* ids_host;
+  int64_t n_host;
   Scratch* scr;
   uint4* pool;
   const uint4* table;
   uint4* hostq;
   uint32_t nvec;
-  const unsigned long long* head;
-  const uint32_t* nxt;
+  const unsigned long long* head;  // request lists, one table per iteration parity:
+  const uint32_t* nxt;             // head Q entries apart, nxt cap entries apart
+  uint64_t Q, cap;
   IterState* it;
   uint64_t N;
   const uint32_t* node_loc;
+  uint64_t loc_stride;  // node_loc tables Q apart (parity)
   uint4* out;
   uint32_t bounce;
   uint32_t tail_chunk;  // delivery chunk size near the end of the batch (guided; 32 = fixed)
@@ -1234,16 +1347,13 @@ struct ServeArgs {
 // S9: close iteration t's record — algorithmic bytes per tier, cumulative sums; the staging
 // count of the next parity is reset so that a missing PVP call stages nothing; the ERANGE
 // counter is mirrored to pinned host memory; it->t_next = t + 1. One warp (lane = field).
-__device__ __forceinline__ void end_record(IterState* it, unsigned long long* hist, unsigned long long* cum,
+__device__ __forceinline__ void end_record(uint64_t t, IterState* it, unsigned long long* hist, unsigned long long* cum,
                                            Scratch* scr, uint32_t R, volatile uint32_t* bad_mirror) {
   const uint32_t f = lane_id();
-  const uint64_t t = it->t;
-  unsigned long long* rec = hist + (size_t)it->rec_idx * F_NFIELDS;
+  unsigned long long* rec = hist + (size_t)(t % kHist) * F_NFIELDS;
   if (f == 0) {
     rec[F_PREF] = scr->staged[t & 1];  // rows the PVP staged for t (its copy completed before gather t)
-    rec[F_UNIQUE] = scr->nuniq;
-    rec[F_REQ] = scr->nreq;
-    rec[F_BOUT] = (unsigned long long)scr->nreq * R;
+    rec[F_BOUT] = rec[F_REQ] * R;
     rec[F_BNVL] = rec[F_PEER] * R;
     rec[F_BH2D] = rec[F_STOR] * R;
     rec[F_BPVP] = rec[F_PREF] * R;
@@ -1261,19 +1371,20 @@ __device__ __forceinline__ void end_record(IterState* it, unsigned long long* hi
     *bad_mirror = scr->bad_ids;
   }
   __syncwarp();
-  // prepare gather t + 1: its record and the per-batch scratch counters start at zero
-  unsigned long long* nrec = hist + (size_t)((t + 1) % kHist) * F_NFIELDS;
+  // prepare gather t + 2 (k_dedup / k_set of t + 1 may already be counting into the record of
+  // t + 1 and the parity counters of t + 1; those were zeroed here by gather t - 1): the record
+  // of t + 2 and the parity counters of t (= those of t + 2) start at zero; the counters only
+  // k_serve / k_pull of t + 1 use (they start after gather t completed) are reset for t + 1
+  unsigned long long* nrec = hist + (size_t)((t + 2) % kHist) * F_NFIELDS;
   if (f < F_NFIELDS) nrec[f] = 0;
   if (f == 0) {
-    scr->nuniq = 0;
-    scr->nfill = 0;
+    scr->nfill[t & 1] = 0;
     scr->ncand = 0;
-    scr->nbypass = 0;
-    scr->nreq = 0;
+    scr->nbypass[t & 1] = 0;
     scr->pull_next = 0;
     scr->pull_phase_next[0] = 0;
     scr->pull_phase_next[1] = 0;
-    scr->nslow = 0;
+    scr->nslow[t & 1] = 0;
   }
   __syncwarp();
   if (f == 0) {  // last: gather t is complete (k_dedup of t + 1 may be waiting for this, below)
@@ -1284,17 +1395,54 @@ __device__ __forceinline__ void end_record(IterState* it, unsigned long long* hi
 
 template <int UNROLL, int OUT, int TMA>
 __global__ void k_serve(ServeArgs a) {
-  pdl_prologue();
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t s_bar[8][kMaxStages];
   __shared__ uint32_t s_pend[8][kMaxStages];
   __shared__ const void* s_src[8][32];
   __shared__ void* s_dst[8][32];
   __shared__ uint32_t s_last;
+  __shared__ uint64_t s_t;
+  __shared__ const int64_t* s_ids;
+  __shared__ int64_t s_n;
+  // Early (set_wait > 0, kernels.cuh k_dedup): no programmatic wait (it would also wait for the
+  // in-flight chain behind the previous k_serve); this gather's k_set is awaited through its
+  // finished-CTA count, and the previous gather — it must be complete before this one fills
+  // slots — through the t_next its last CTA publishes (end_record).
+  // A direct call takes the iteration's values from its arguments (an early k_dedup of the next
+  // gather may republish IterState while this launch runs); a graph replay reads IterState (the
+  // next gather of a replay is never early).
+  if (a.set_wait) {  // early
+    if (threadIdx.x == 0) {
+      while (ld_acquire_u64(&a.it->set_ctas_done) < a.set_wait) __nanosleep(64);
+      while (ld_acquire_u64(&a.it->t_next) < (uint64_t)a.t_host) __nanosleep(64);
+    }
+    __syncthreads();
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.t_host >= 0) {
+    if (threadIdx.x == 0) {
+      s_t = (uint64_t)a.t_host;
+      s_ids = a.ids_host;
+      s_n = a.n_host;
+    }
+  } else if (threadIdx.x == 0) {
+    s_t = a.it->t;
+    s_ids = a.it->ids;
+    s_n = a.it->n;
+  }
+  __syncthreads();
   constexpr uint32_t kChunk = 32;
-  const uint32_t stamp = a.it->stamp;
-  const int64_t* __restrict__ ids = a.it->ids;
-  const int64_t n = a.it->n;
+  const uint64_t t_it = s_t;
+  const uint32_t stamp = (uint32_t)(t_it + 1);
+  const int64_t* __restrict__ ids = s_ids;
+  const int64_t n = s_n;
+  const uint32_t par = (uint32_t)(t_it & 1);
+  TRACE_AT(3, par, 0);
+  const unsigned long long* __restrict__ head = a.head + (size_t)par * a.Q;
+  const uint32_t* __restrict__ nxt = a.nxt + (size_t)par * a.cap;
+  const uint32_t* __restrict__ node_loc = a.node_loc + par * a.loc_stride;
   const uint32_t nvec = a.nvec;
   const uint32_t wib = threadIdx.x >> 5;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1313,9 +1461,10 @@ __global__ void k_serve(ServeArgs a) {
     __syncwarp();
   }
   if (gw >= npull) {  // ---- fill warps
-    const uint32_t nf = a.scr->nfill;
+    const uint32_t nf = a.scr->nfill[par];
+    const FillEnt* __restrict__ fills = a.fills + (size_t)par * a.fstride;
     for (uint32_t e = gw - npull; e < nf; e += nw - npull) {
-      const FillEnt f = a.fills[e];
+      const FillEnt f = fills[e];
       uint4* slot = a.pool + (size_t)f.dst * nvec;
       if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(a.hostq + (size_t)f.victim * nvec, slot, nvec);
       const bool from_host = (f.src & kHostBit) != 0;
@@ -1323,7 +1472,7 @@ __global__ void k_serve(ServeArgs a) {
       // host row: the backing table's row q, or (file tier) bounce-buffer row e
       const uint4* src = from_host ? a.table + (size_t)(a.bounce ? e : (f.src & ~kHostBit)) * nvec
                                    : a.pool + (size_t)f.src * nvec;
-      const unsigned long long h = a.head[f.node];
+      const unsigned long long h = head[f.node];
       const uint32_t first = (uint32_t)(h >> 32) == stamp ? (uint32_t)h : kInvalid;
       for (uint32_t base = 0; base < nvec; base += 32 * UNROLL) {
         uint4 v[UNROLL];
@@ -1337,7 +1486,7 @@ __global__ void k_serve(ServeArgs a) {
           const uint32_t k = base + lane + 32 * u;
           if (k < nvec) st16<kDev>(slot + k, v[u]);
         }
-        for (uint32_t pos = first; pos != kInvalid; pos = a.nxt[pos]) {
+        for (uint32_t pos = first; pos != kInvalid; pos = nxt[pos]) {
           uint4* dst = a.out + (size_t)pos * nvec;  // list positions are request indices
 #pragma unroll
           for (int u = 0; u < UNROLL; ++u) {
@@ -1377,7 +1526,7 @@ __global__ void k_serve(ServeArgs a) {
     }
   };
   auto loc_of = [&](int64_t x) -> uint32_t {  // -2: past the batch (nothing to copy)
-    return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : a.node_loc[(uint32_t)x];
+    return x == -2 ? kDelivered : (x < 0 || (uint64_t)x >= a.N) ? kInvalid : node_loc[(uint32_t)x];
   };
   // Chunks are handed out by a counter (load balance: the hit rows finish together, and a
   // storage-bound batch keeps the delivery-only warps busy while the fills run), with guided
@@ -1429,6 +1578,7 @@ __global__ void k_serve(ServeArgs a) {
   }
   if (TMA && lane == 0) ring_drain();
   // ---- S9: the last CTA to finish closes the record
+  TRACE_AT(3, par, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1438,7 +1588,7 @@ __global__ void k_serve(ServeArgs a) {
   if (s_last && wib == 0) {
     __threadfence();
     if (lane == 0) a.scr->serve_done = 0;
-    end_record(a.it, a.hist, a.cum, a.scr, nvec * 16, a.bad_mirror);
+    end_record(t_it, a.it, a.hist, a.cum, a.scr, nvec * 16, a.bad_mirror);
   }
 }
 

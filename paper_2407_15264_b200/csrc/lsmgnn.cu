@@ -140,6 +140,7 @@ struct Ctx {
   uint64_t N = 0;
   uint32_t R = 0, nvec = 0, A = 0, W = 0, T = 0, MW = 0, Wp1 = 0;
   uint64_t L = 0, S = 0, Q = 0, C = 0, cap = 0, ucap = 0, bcap = 0;
+  uint64_t loc_stride = 0;  // node_loc tables per iteration parity (G = 1), Q apart
   uint64_t BC = 0, BCp = 0;  // per-set bucket capacity (distinct nodes of a set per batch); its pow2
   // window ring slot capacity: G = 1 cap; G > 1 min(G, 2)·cap — twice a home's expected share of
   // the G ranks' batches (a fuller slot is swept instead of listed, k_win_gather / k_dedup)
@@ -222,8 +223,15 @@ struct Ctx {
   // the library's last launch on tail_st ended a G = 1 gather (k_serve / k_end): a window feed
   // right behind it may start early (k_route_local, wait_prev = 0)
   bool tail_gather = false;
+  // ... or an early window feed (k_route_local, wait_prev = 0) right behind such a gather: the
+  // next gather's k_dedup may then start alongside that k_serve (k_dedup `early`)
+  bool tail_feed = false;
   cudaStream_t tail_st = nullptr;
   bool feed_early = true;  // LSMGNN_FEED_EARLY=0 turns the early feed start off (A/B)
+  bool dedup_early = true;  // LSMGNN_DEDUP_EARLY=0 turns the early k_dedup / k_set start off (A/B)
+  uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
+  uint64_t set_ctas_issued = 0;    // CTAs of early k_set launches (it->set_ctas_done)
+  uint64_t feed_ctas_issued = 0;  // CTAs of early k_route_local launches (it->feed_ctas_done counts them done)
   // LSMGNN_G1_PULL=1 (G = 1, profiling aid): the G > 1 serve path — k_fill, then k_pull phase 0
   // (rows in place) and phase 1 (rows filled this batch), then k_end — instead of the fused
   // k_serve; the pull kernels can then be profiled on one process (local HBM instead of peers)
@@ -597,6 +605,7 @@ int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaS
   cfg.attrs = at;
   cfg.numAttrs = g.pdl ? 1 : 0;
   g.tail_gather = false;  // (launch_gather sets it again after its last kernel)
+  g.tail_feed = false;    // (launch_window sets it again after an early feed)
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
   if (e != cudaSuccess) return set_err(LSMGNN_ECUDA, "kernel launch: %s", cudaGetErrorString(e));
   return 0;
@@ -629,6 +638,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   // ---- S3 dedup + set grouping
   prof_begin(1, st);
   const int64_t maxreq = (int64_t)g.cap * G;
+  bool early = false;
   {
     DedupArgs da{};
     da.inbox = inbox;
@@ -656,13 +666,18 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.tags = g.tags;
     da.last_use = g.last_use;
     da.node_loc = loc_of(g.arena);
+    da.loc_stride = g.loc_stride;
     da.slow_stamp = g.slow_stamp;
     da.slow_list = g.slow_list;
-    da.scr = g.scr;
     da.A = g.A;
-    KLAUNCH(k_dedup, grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4), 256, 0, st, da,
-            g.it, g.scr, g.hist, ba, G == 1 ? 1u : 0u);
+    // early start alongside the k_serve of the previous gather (kernels.cuh k_dedup): a direct
+    // G = 1 call whose programmatic predecessor on st is that k_serve or the early feed behind it
+    early = g.dedup_early && g.pdl && G == 1 && !g.g1_pull && !graph && ba.t_host >= 0 && g.C == 0 &&
+            g.file_fd < 0 && g.tail_st == st && (g.tail_gather || g.tail_feed);
+    const int dgrid = grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4);
+    KLAUNCH(k_dedup, dgrid, 256, 0, st, da, g.it, g.scr, g.hist, ba, G == 1 ? 1u : 0u, early ? 1u : 0u);
     LAUNCHED();
+    if (early) g.dedup_ctas_issued += (uint64_t)dgrid;  // (an early k_dedup counts them done)
   }
   if (ev_dedup) CK(cudaEventRecord(ev_dedup, st));  // the window feed of t+1+W may follow from here
   prof_end(1, st);
@@ -684,9 +699,11 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   sp.score = g.score;
   sp.mask = g.mask;
   sp.node_loc = loc_of(g.arena);
+  sp.loc_stride = g.loc_stride;
   sp.vst_stamp = g.vst_stamp;
   sp.vst_idx = g.vst_idx;
   sp.fills = g.fills;
+  sp.fstride = g.ucap;
   sp.cands = g.cands;
   sp.qcnt = g.qcnt;
   sp.scr = g.scr;
@@ -711,6 +728,8 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
   sp.deliver = kDelivered;
   sp.period = (uint32_t)std::max(1, g.opt.update_period);
   sp.line_info = g.line_info;
+  sp.dedup_wait = early ? g.dedup_ctas_issued : 0;
+  sp.feed_wait = early ? g.feed_ctas_issued : 0;
   if (sp.period > 1) {  // the periodic window scan; k_snapshot exits when t mod P != 0
     KLAUNCH(k_snapshot, grid_for((int64_t)g.L, 256, 4), 256, 0, st, g.tags, (uint32_t)g.L, (uint32_t)G, g.mask, g.MW, g.W,
                                                                 g.it, g.line_info);
@@ -721,6 +740,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
         std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(4, g.geom_per_sm));
     KLAUNCH(k_set, (int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st, sp);
     LAUNCHED();
+    if (early) g.set_ctas_issued += (uint64_t)blocks;  // (an early k_set counts them done)
   }
   prof_end(2, st);
   // ---- S5 victim admission (PVP)
@@ -732,7 +752,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     LAUNCHED();
     KLAUNCH(k_qscatter, qg, 256, 0, st, g.cands, g.scr, g.W, g.qoff, g.qcnt, g.qb);
     LAUNCHED();
-    KLAUNCH(k_admit, g.W, 256, 0, st, g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint32_t)g.C, g.it,
+    KLAUNCH(k_admit, g.W, 256, 0, st, g.cands, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse, g.fills, (uint64_t)g.ucap, (uint32_t)g.C, g.it,
                                  g.hist);
     LAUNCHED();
     prof_end(3, st);
@@ -752,6 +772,11 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     if (bounce && (rc_io = io_export(st))) return rc_io;
     ServeArgs sa{};
     sa.fills = g.fills;
+    sa.fstride = g.ucap;
+    sa.set_wait = early ? g.set_ctas_issued : 0;
+    sa.t_host = ba.t_host;
+    sa.ids_host = ba.ids_host;
+    sa.n_host = ba.n_host;
     sa.scr = g.scr;
     sa.pool = pool;
     sa.table = tab;
@@ -759,6 +784,9 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.nvec = g.nvec;
     sa.head = g.head;
     sa.nxt = g.nxt;
+    sa.Q = g.Q;
+    sa.cap = g.cap;
+    sa.loc_stride = g.loc_stride;
     sa.it = g.it;
     sa.N = g.N;
     sa.node_loc = loc_of(g.arena);
@@ -800,6 +828,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
       pa.node_loc[h] = loc_of(g.peer_arena[h]);
     }
     pa.G = (uint32_t)G;
+    pa.loc_stride = g.loc_stride;
     pa.scr = g.scr;
     pa.tail_chunk = (uint32_t)g.serve_tail;
     pa.tail_rounds = (uint32_t)g.serve_tail_rounds;
@@ -832,9 +861,9 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     // (profiles/r01_pcie_microbench.txt) and leaves room on every SM for pull phase 0
     const int blocks = g.sms * std::min(2, g.geom_per_sm);
     if (wide)
-      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce, g.io_ready_dev, g.it);
+      k_fill<8><<<blocks, 256, 0, st>>>(g.fills, g.ucap, g.scr, pool, tab, hq, g.nvec, bounce, g.io_ready_dev, g.it);
     else
-      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.scr, pool, tab, hq, g.nvec, bounce, g.io_ready_dev, g.it);
+      k_fill<2><<<blocks, 256, 0, st>>>(g.fills, g.ucap, g.scr, pool, tab, hq, g.nvec, bounce, g.io_ready_dev, g.it);
     LAUNCHED();
     if (bounce && (rc_io = read_storage_rows(stamp_host, st))) return rc_io;
     prof_end(4, st);
@@ -892,6 +921,8 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
       KLAUNCH(k_route_local, grid_for(std::max<int64_t>(n, 1), 256), 256, 0, st, g.it, k_host, ids, n, g.Wp1, g.N,
               g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, wait_prev);
       LAUNCHED();
+      if (!wait_prev) g.feed_ctas_issued += (uint64_t)grid_for(std::max<int64_t>(n, 1), 256);  // (counted done)
+      if (!wait_prev) g.tail_feed = true;  // (tail_st unchanged: the same stream)
     }
     return 0;
   }
@@ -1086,7 +1117,7 @@ int attach_file(const char* path, uint64_t rows) {
 // File tier, step 1 (stream-ordered, before the fill kernel): publish this batch's fill list to
 // pinned host memory (k_io_export).
 int io_export(cudaStream_t st) {
-  KLAUNCH(k_io_export, grid_for((int64_t)g.ucap, 256, 2), 256, 0, st, (const FillEnt*)g.fills, g.scr,
+  KLAUNCH(k_io_export, grid_for((int64_t)g.ucap, 256, 2), 256, 0, st, (const FillEnt*)g.fills, (uint64_t)g.ucap, g.scr,
           (const IterState*)g.it, g.io_dev, g.io_src_dev);
   LAUNCHED();
   return 0;
@@ -1207,7 +1238,10 @@ int plan_layout(Ctx& c, int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype,
   c.off_wcnt = o;  o = align_up(o + G * sizeof(uint32_t), 256);
   c.off_inbox = o; o = align_up(o + (size_t)G * c.cap * sizeof(uint32_t), 256);
   c.off_win = o;   o = align_up(o + (G > 1 ? (size_t)G * c.cap * sizeof(uint32_t) : 0), 256);
-  c.off_loc = o;   o = align_up(o + c.Q * sizeof(uint32_t), 4096);
+  // node_loc: at G = 1 one table per iteration parity (k_dedup of t + 1 writes its own while
+  // k_serve of t reads the other, kernels.cuh k_dedup `early`); at G > 1 peers read the one table
+  c.loc_stride = G == 1 ? c.Q : 0;
+  c.off_loc = o;   o = align_up(o + (G == 1 ? 2 : 1) * c.Q * sizeof(uint32_t), 4096);
   c.off_pool = o;  o = align_up(o + c.pool_rows * (size_t)c.R, 4096);
   c.arena_bytes = o;
   return 0;
@@ -1330,12 +1364,12 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     DA(g.line_info, g.L);
     CK(cudaMemset(g.line_info, 0xFF, g.L * sizeof(uint32_t)));
   }
-  if (G == 1) {
-    DA(g.head, g.Q);
-    DA(g.nxt, g.cap);
+  if (G == 1) {  // request lists of the fused delivery, one per iteration parity
+    DA(g.head, 2 * g.Q);
+    DA(g.nxt, 2 * g.cap);
   }
   DA(g.score, g.Q);
-  DA(g.fills, g.ucap);
+  DA(g.fills, 2 * g.ucap);  // one fill list per iteration parity
   DA(g.cands, g.ucap);
   DA(g.scr, 1);
   DA(g.it, 1);
@@ -1402,6 +1436,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (const char* e = std::getenv("LSMGNN_SERVE_TAIL_ROUNDS")) g.serve_tail_rounds = std::max(0, std::min(64, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_SERVE_AHEAD")) g.serve_ahead = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_L2_EVICT_FIRST")) g.l2_evict_first = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_DEDUP_EARLY")) g.dedup_early = std::atoi(e) != 0;
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));
@@ -1610,6 +1645,22 @@ int lsmgnn_gather_host(const int64_t* host_ids, int64_t n, void* host_out, void*
   return check_sticky();
 }
 
+#ifdef LSMGNN_TRACE
+// (experiments only) reset = 1: clear the timeline probe; else copy it out: [8][2][2] u64
+int lsmgnn_debug_trace(unsigned long long* out, int32_t reset) {
+  unsigned long long h[8][2][2];
+  if (reset) {
+    for (auto& k : h)
+      for (auto& p : k) p[0] = ~0ull, p[1] = 0;
+    CK(cudaMemcpyToSymbol(g_trace, h, sizeof h));
+  } else {
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyFromSymbol(out, g_trace, sizeof h));
+  }
+  return 0;
+}
+#endif
+
 int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
   if (!out_host || (scope != 0 && scope != 1)) return set_err(LSMGNN_EINVAL, "bad args");
@@ -1628,8 +1679,8 @@ int lsmgnn_stats(lsmgnn_stats_t* out_host, int32_t scope) {
 
 int lsmgnn_stats_history(lsmgnn_stats_t* out_host, int64_t first, int64_t count) {
   if (!g.inited) return set_err(LSMGNN_ESTATE, "not initialised");
-  // the last kHist - 1 iterations (the slot of the next one is already zeroed)
-  if (count < 0 || first < 0 || first + count > g.t_next || (g.t_next - first) > (int64_t)kHist - 1)
+  // the last kHist - 2 iterations (the slots of the next two are already zeroed: end_record)
+  if (count < 0 || first < 0 || first + count > g.t_next || (g.t_next - first) > (int64_t)kHist - 2)
     return set_err(LSMGNN_EINVAL, "history range [%lld,+%lld) unavailable", (long long)first, (long long)count);
   CK(cudaDeviceSynchronize());
   // the ring [first, first+count) is at most two contiguous pieces

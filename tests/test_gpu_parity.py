@@ -280,8 +280,8 @@ def test_bf16_rows():
 
 
 def test_long_run_history_wrap():
-    """6,000 iterations (the on-device history keeps the last 4,095): the cumulative counters
-    and the last 4,095 per-iteration records still equal the oracle's (stamps, rings, wraps)."""
+    """6,000 iterations (the on-device history keeps the last 4,094): the cumulative counters
+    and the last 4,094 per-iteration records still equal the oracle's (stamps, rings, wraps)."""
     import torch
     from paper_2407_15264_b200 import LsmGnn
     from .harness import table_for
@@ -301,7 +301,9 @@ def test_long_run_history_wrap():
         c.gather(ids[t], out)
         c.prefetch([ids[t + 1 + W]], first_iter=t + 1 + W)
     torch.cuda.synchronize()
-    compare(c.history(K - 4095, 4095), ho[K - 4095:], "history tail")
+    compare(c.history(K - 4094, 4094), ho[K - 4094:], "history tail")
+    with pytest.raises(Exception):
+        c.history(K - 4095, 4095)  # the two slots ahead are already zeroed (end_record)
     cum = c.stats(1)
     from paper_2407_15264_b200 import STATS_FIELDS
     for i, f in enumerate(STATS_FIELDS[1:], 1):
