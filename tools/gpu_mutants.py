@@ -17,7 +17,7 @@ CSRC = os.path.join(ROOT, "paper_2407_15264_b200", "csrc")
 # (name, original, mutated, what it breaks) — kernels.cuh unless the name starts with "dc_"
 # (device_common.cuh). Round 2 replaced the patterns of the rewritten kernels and added mutants
 # for the new mechanisms (the hit probe in k_dedup, the slow-set list, the TMA rings, guided
-# delivery chunks, the pipelined file tier).
+# delivery chunks, the pipelined file tier, the overlap of consecutive gathers).
 MUTANTS = [
     ("threshold_strict", "((uint32_t)d <= T ? kNear : kFar)", "((uint32_t)d < T ? kNear : kFar)", "R4 Near iff d <= T"),
     ("no_level_swap", "if (cls == kNoReuse) return pvp ? 1 : 0;\n  if (cls == kFar) return pvp ? 0 : 1;",
@@ -29,7 +29,7 @@ MUTANTS = [
      "R17 queue t+1 after gather(t)"),
     ("mask_never_cleared", "const uint32_t m = ~(1u << (slot & 31));", "const uint32_t m = ~0u;",
      "S10 bits of iteration t cleared (in k_dedup)"),
-    ("deliver_first_only", "for (uint32_t pos = first; pos != kInvalid; pos = a.nxt[pos]) {",
+    ("deliver_first_only", "for (uint32_t pos = first; pos != kInvalid; pos = nxt[pos]) {",
      "for (uint32_t pos = first; pos != kInvalid; pos = kInvalid) {", "S8 every requester of a node"),
     ("no_victim_d2h", "      if (f.victim != kInvalid) warp_copy_row<UNROLL, kDev, kHost>(a.hostq + (size_t)f.victim * nvec, slot, nvec);\n",
      "", "S6 victim row D2H before the slot is overwritten"),
@@ -39,23 +39,40 @@ MUTANTS = [
     ("pull_phase1_skips", "const uint32_t need = __ballot_sync(0xffffffffu, valid && (((loc & kDelivered) != 0) == (PHASE == 1)));",
      "const uint32_t need = __ballot_sync(0xffffffffu, valid && !(loc & kDelivered));", "G > 1 filled rows pulled after served"),
     ("probe_no_last_use", "    a.last_use[s * a.A + (uint32_t)way] = t;\n    ++*nhit;", "    ++*nhit;",
-     "R10/R20 a hit's last use is t (k_dedup probe)"),
-    ("slow_set_dropped", "      a.slow_list[atomicAdd(&a.scr->nslow, 1u)] = s;  // first miss of the set: k_set processes it",
+     "R10/R20 a hit's last use is t (k_dedup probe; k_set protects the ways used at t)"),
+    ("slow_set_dropped", "      a.slow_list[atomicAdd(pp.nslow, 1u)] = s;  // first miss of the set: k_set processes it",
      "      (void)s;", "S4/S5 every set with a miss is replaced"),
-    ("miss_not_listed", "    if (a.head) list_join(a, q, pos, stamp);  // a fill will deliver this row",
+    ("miss_not_listed", "    if (pp.head) list_join(pp, q, pos, stamp);  // a fill will deliver this row",
      "", "S8 a filled node's first requester receives the row"),
-    ("fast_set_cnt_kept", "    if (p.set_cnt[sl] && p.slow_stamp[sl] != stamp_) p.set_cnt[sl] = 0;  // ready for the next batch",
-     "    ;", "S3 the all-hit sets' buckets start empty next batch"),
-    ("hit_counted_twice", "        if (way >= 0) {  // (node_loc and the hit count were written by k_dedup's probe)\n          kind = kHit;",
-     "        if (way >= 0) {\n          kind = kHit;\n          ++ctr[C_HIT];", "S9 hits counted once"),
+    ("hit_into_bucket", "  if (way >= 0) {\n    pp.node_loc[q] = s * a.A + (uint32_t)way;",
+     "  if (way >= 0) {\n    a.bucket[(size_t)s * a.BC + atomicAdd(&a.set_cnt[s], 1u)] = v;\n    pp.node_loc[q] = s * a.A + (uint32_t)way;",
+     "S3/S4 the buckets hold the misses only (a hit re-installed would be counted twice)"),
+    ("protect_none", "const uint32_t protm = __ballot_sync(0xffffffffu, lane < A && tg != kInvalid && lu == t_);",
+     "const uint32_t protm = 0u;", "R10 hits of the batch are protected from eviction"),
+    # the overlap of consecutive gathers (k_dedup / k_set `early`)
+    ("set_no_dedup_wait", "      while (ld_acquire_u64(&p.it->dedup_ctas_done) < p.dedup_wait) __nanosleep(64);\n", "",
+     "an early k_set starts after its gather's k_dedup finished"),
+    ("set_no_feed_wait", "      while (ld_acquire_u64(&p.it->feed_ctas_done) < p.feed_wait) __nanosleep(64);\n", "",
+     "an early k_set reads the window bits after the feeds issued before its gather"),
+    ("serve_no_prev_wait", "      while (ld_acquire_u64(&a.it->t_next) < (uint64_t)a.t_host) __nanosleep(64);\n", "",
+     "an early k_serve fills slots only after the previous gather completed"),
+    ("loc_no_parity", "  pp.node_loc = a.node_loc + par * a.loc_stride;", "  pp.node_loc = a.node_loc;",
+     "node_loc of gather t+1 does not overwrite the table k_serve(t) reads"),
+    ("lists_no_parity", "  pp.head = a.head ? a.head + (size_t)par * a.Q : nullptr;", "  pp.head = a.head;",
+     "request lists of gather t+1 do not overwrite those k_serve(t) walks"),
+    ("fills_no_parity", "  FillEnt* const fills_ = p.fills + (size_t)par_ * p.fstride;", "  FillEnt* const fills_ = p.fills;",
+     "the fill list of gather t+1 does not overwrite the one k_serve(t) reads"),
+    ("record_zeroed_early", "  unsigned long long* nrec = hist + (size_t)((t + 2) % kHist) * F_NFIELDS;",
+     "  unsigned long long* nrec = hist + (size_t)((t + 1) % kHist) * F_NFIELDS;",
+     "the record of t+1 (already being counted by an early k_dedup) is not zeroed by gather t"),
     ("pvp_unused_inverted", "      unused += p.mark[stg[j] / G] != stamp_;", "      unused += p.mark[stg[j] / G] == stamp_;",
      "R28 pvp_unused = staged rows not requested"),
     ("file_no_wait", "      if (from_host && a.bounce) io_wait(a.io_ready, e, stamp);  // file tier: row e read yet?\n",
      "", "N2 a fill reads its bounce row only after the host released its chunk"),
     ("dc_ring_no_read_wait", "      if (r.nl >= r.ST) bulk_wait_read(r.ns + r.ST - 1 - r.nl);\n", "",
      "a stage is reloaded only after its store has read it (TMA rings)"),
-    ("dc_ring_store_wrong_row", "    bulk_s2g(dst[r.pend[s]], r.buf + (size_t)s * r.R, r.R);",
-     "    bulk_s2g(dst[r.pend[(s + 1) % r.ST]], r.buf + (size_t)s * r.R, r.R);", "each stage stored to its own row"),
+    ("dc_ring_store_wrong_row", "    else bulk_s2g(dst[r.pend[s]], r.buf + (size_t)s * r.R, r.R);",
+     "    else bulk_s2g(dst[r.pend[(s + 1) % r.ST]], r.buf + (size_t)s * r.R, r.R);", "each stage stored to its own row"),
 ]
 
 

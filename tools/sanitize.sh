@@ -21,6 +21,11 @@ done
 timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_storage_file.py -q -x \
   -k "small_rows" > $out/sanitize_memcheck_file.log 2>&1
 echo "G=1 file tier memcheck rc=$? : $(grep -E 'ERROR SUMMARY' $out/sanitize_memcheck_file.log | tail -1) $(grep -Eo '[0-9]+ passed' $out/sanitize_memcheck_file.log)" >> $out/sanitize_summary.txt
+# consecutive gathers issued without host synchronisation (parity-indexed tables, done counters;
+# the sanitizer serialises the kernels, so this checks the parity offsets and bounds)
+timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_gpu_overlap.py -q -x \
+  -k "overlapped" > $out/sanitize_memcheck_overlap.log 2>&1
+echo "G=1 overlapped gathers memcheck rc=$? : $(grep -E 'ERROR SUMMARY' $out/sanitize_memcheck_overlap.log | tail -1) $(grep -Eo '[0-9]+ passed' $out/sanitize_memcheck_overlap.log)" >> $out/sanitize_summary.txt
 # G = 2: each rank runs under its own compute-sanitizer (torch.distributed env set by hand, so
 # the ranks themselves are instrumented), both pull orders; the ranks' outputs are
 # checked (rows bad = 0)
