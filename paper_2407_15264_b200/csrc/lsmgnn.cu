@@ -229,6 +229,7 @@ struct Ctx {
   cudaStream_t tail_st = nullptr;
   bool feed_early = true;  // LSMGNN_FEED_EARLY=0 turns the early feed start off (A/B)
   bool dedup_early = true;  // LSMGNN_DEDUP_EARLY=0 turns the early k_dedup / k_set start off (A/B)
+  int early_dedup_per_sm = 4;
   uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
   uint64_t set_ctas_issued = 0;    // CTAs of early k_set launches (it->set_ctas_done)
   uint64_t feed_ctas_issued = 0;  // CTAs of early k_route_local launches (it->feed_ctas_done counts them done)
@@ -672,9 +673,14 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.A = g.A;
     // early start alongside the k_serve of the previous gather (kernels.cuh k_dedup): a direct
     // G = 1 call whose programmatic predecessor on st is that k_serve or the early feed behind it
+    // (not with the periodic window scan: k_snapshot sits between k_dedup and k_set, and an early
+    // k_set does not wait for it)
     early = g.dedup_early && g.pdl && G == 1 && !g.g1_pull && !graph && ba.t_host >= 0 && g.C == 0 &&
-            g.file_fd < 0 && g.tail_st == st && (g.tail_gather || g.tail_feed);
-    const int dgrid = grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256, 4);
+            g.file_fd < 0 && g.opt.update_period <= 1 && g.tail_st == st && (g.tail_gather || g.tail_feed);
+    // (an early k_dedup shares the SMs with the previous k_serve: LSMGNN_EARLY_DEDUP_PER_SM caps its
+    // CTAs per SM, A/B)
+    const int dgrid = grid_for(std::min<int64_t>(maxreq, std::max<int64_t>(n_bound, 1) * G), 256,
+                               early ? g.early_dedup_per_sm : 4);
     KLAUNCH(k_dedup, dgrid, 256, 0, st, da, g.it, g.scr, g.hist, ba, G == 1 ? 1u : 0u, early ? 1u : 0u);
     LAUNCHED();
     if (early) g.dedup_ctas_issued += (uint64_t)dgrid;  // (an early k_dedup counts them done)
@@ -1437,6 +1443,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (const char* e = std::getenv("LSMGNN_SERVE_AHEAD")) g.serve_ahead = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_L2_EVICT_FIRST")) g.l2_evict_first = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_DEDUP_EARLY")) g.dedup_early = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_EARLY_DEDUP_PER_SM")) g.early_dedup_per_sm = std::max(1, std::min(8, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
     CK(cudaStreamCreateWithFlags(&g.pull_st, cudaStreamNonBlocking));

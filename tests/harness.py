@@ -29,10 +29,13 @@ def table_for(N: int, D: int, seed_f: int = 5, pinned: bool = False, home: int =
 
 def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0, reinsert=1, table=None,
             check_rows="full", max_batch_ids=None, rank=0, world=1, group=None, seed_f=5, keep_outs=False, P=1,
-            state_cb=None, storage_file=None, two_streams=False):
+            state_cb=None, storage_file=None, two_streams=False, overlap=False):
     """Run trace[t][rank] through the library. Returns (history [K, 24] uint64, outs or None, bad_rows).
 
-    check_rows: "full" compares every row with the closed form F(v); "none" skips it."""
+    check_rows: "full" compares every row with the closed form F(v); "none" skips it.
+    overlap: no host synchronisation between the gathers (each into its own `out`, all rows
+    checked at the end), so consecutive gathers can run concurrently (kernels.cuh k_dedup
+    `early`); otherwise each `out` is read back right after its gather."""
     import torch
     from paper_2407_15264_b200 import LsmGnn
     K = len(trace)
@@ -56,19 +59,30 @@ def run_gpu(trace, *, N, D, L, A, scores, policy="hybrid", pvp=0, W=8, T=0, V=0,
         torch.cuda.synchronize()
     c.prefetch([ids_d[k] if k < K else empty for k in range(1, W + 1)], first_iter=1, stream=sb)
     outs = []
+    pending = []
     bad = 0
+
+    def check(t, out):
+        nonlocal bad
+        host = out[: ids_d[t].numel()].cpu().numpy()
+        nb, _ = synth.check_rows(host.view(np.uint32).reshape(-1, D), mine[t], D, seed_f)
+        bad += nb
+        if keep_outs:
+            outs.append(host)
+
     for t in range(K):
         out = torch.empty((max(1, ids_d[t].numel()), R), dtype=torch.uint8, device=dev)
         c.gather(ids_d[t], out)
         k = t + 1 + W
         c.prefetch([ids_d[k] if k < K else empty], first_iter=k, stream=sb)
         if check_rows == "full" and ids_d[t].numel():
-            host = out[: ids_d[t].numel()].cpu().numpy()
-            nb, _ = synth.check_rows(host.view(np.uint32).reshape(-1, D), mine[t], D, seed_f)
-            bad += nb
-            if keep_outs:
-                outs.append(host)
+            if overlap:
+                pending.append((t, out))
+            else:
+                check(t, out)
     torch.cuda.synchronize()
+    for t, out in pending:
+        check(t, out)
     hist = c.history(0, K)
     if state_cb is not None:  # inspect the final cache state before the home is freed
         state_cb(c)

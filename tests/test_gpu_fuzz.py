@@ -52,3 +52,19 @@ def test_fuzz_parity(seed):
     gt = state["tags"].astype(np.int64)
     gt[gt == 0xFFFFFFFF] = -1
     assert np.array_equal(gt, ot.reshape(-1)) and np.array_equal(state["lu"].astype(np.int64), olu.reshape(-1))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("LSMGNN_FUZZ_OVERLAP", "20"))))
+def test_fuzz_parity_overlapped(seed):
+    """The same random configurations without a victim buffer (the condition for consecutive
+    gathers to overlap) and without any host synchronisation between the gathers."""
+    from oracle import Oracle, run_trace
+    cfg, tr, sc = random_case(500 + seed)
+    cfg["pvp"] = 0
+    cfg["V"] = 0  # no victim buffer: the overlap is off whenever one exists
+    hg, _, bad = run_gpu(tr, scores=sc, max_batch_ids=max(1, max(len(x[0]) for x in tr)), overlap=True, **cfg)
+    o = Oracle(1, cfg["N"], 4 * cfg["D"], cfg["L"], cfg["A"], sc, policy=cfg["policy"], pvp=0, W=cfg["W"],
+               T=cfg["T"], V=cfg["V"], reinsert=cfg["reinsert"], P=cfg["P"])
+    ho = run_trace(o, tr)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho, f"overlapped fuzz {seed}: {cfg}")
