@@ -229,7 +229,7 @@ struct Ctx {
   cudaStream_t tail_st = nullptr;
   bool feed_early = true;  // LSMGNN_FEED_EARLY=0 turns the early feed start off (A/B)
   bool dedup_early = true;  // LSMGNN_DEDUP_EARLY=0 turns the early k_dedup / k_set start off (A/B)
-  int early_dedup_per_sm = 4;
+  int early_dedup_per_sm = 2;  // (A/B ab_perSM: 1 0.2044, 2 0.2043, 4 0.2065 ms/step direct)
   uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
   uint64_t set_ctas_issued = 0;    // CTAs of early k_set launches (it->set_ctas_done)
   uint64_t feed_ctas_issued = 0;  // CTAs of early k_route_local launches (it->feed_ctas_done counts them done)

@@ -82,3 +82,21 @@ def test_overlap_toggle_identical(monkeypatch):
     h0, bad0 = _run(tr, K, N=N, D=D, L=L, A=A, sc=sc, W=W, shared_out=False)
     assert bad1 == 0 and bad0 == 0
     compare(h1, h0, "early vs serialised")
+
+
+def test_overlap_slow_feed():
+    """Tiny gathers behind huge window feeds: the early k_set of gather t+1 would start while the
+    feed of t+1+W still sets reuse bits unless it waits for the feeds issued before it (their
+    finished-CTA count). Eviction classes and victims depend on those bits (hybrid, W = 4)."""
+    N, D, A, W, K = 1_000_000, 4, 8, 4, 40
+    L = 16384
+    rng = np.random.default_rng(21)
+    tr = []
+    for t in range(K + W + 1):
+        n = 1_500_000 if t % 3 == 0 else 96
+        tr.append([rng.integers(0, N, n).astype(np.int64)])
+    sc = rng.integers(0, 256, N).astype(np.uint8)
+    hg, bad = _run(tr, K, N=N, D=D, L=L, A=A, sc=sc, W=W, shared_out=False)
+    ho = run_oracle(tr, G=1, N=N, D=D, L=L, A=A, scores=sc, policy="hybrid", pvp=0, W=W)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho[:K], "overlap slow feed")
