@@ -307,6 +307,7 @@ struct DedupArgs {
   uint32_t* last_use;
   uint32_t* node_loc;
   uint64_t loc_stride;  // G = 1: node_loc has one table per iteration parity (Q apart); G > 1: 0
+  uint32_t* req_loc;    // G = 1: per-request locations, one table per iteration parity (cap apart)
   uint32_t* slow_stamp;
   uint32_t* slow_list;  // the sets with a miss this batch (count scr->nslow[t & 1])
   uint32_t A;
@@ -318,7 +319,9 @@ struct DedupPar {
   unsigned long long* head;
   uint32_t* nxt;
   uint32_t* nslow;
+  uint32_t* req_loc;  // G = 1: per request position, the slot of a first-occurrence hit, else kPending
 };
+constexpr uint32_t kPending = 0xFFFFFFFEu;  // req_loc: look the location up in node_loc (k_serve)
 // One request: first occurrence of its node (returns 1) is probed against its set's A tags; a
 // hit writes node_loc and the way's last use (= t: hits are protected, R10, and k_set reads the
 // protection from last_use), a miss goes into the set's bucket (the bucket holds the batch's
@@ -354,6 +357,7 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
   const bool first = atomicExch(&a.mark[q], stamp) != stamp;
   if (!first) {
     if (pp.head) list_join(pp, q, pos, stamp);
+    if (pp.req_loc) pp.req_loc[pos] = kPending;
     return 0;
   }
   int way = -1;
@@ -371,12 +375,14 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
   }
   if (way >= 0) {
     pp.node_loc[q] = s * a.A + (uint32_t)way;
+    if (pp.req_loc) pp.req_loc[pos] = s * a.A + (uint32_t)way;
     a.last_use[s * a.A + (uint32_t)way] = t;
     ++*nhit;
   } else {
     const uint32_t slot = atomicAdd(&a.set_cnt[s], 1u);
     a.bucket[(size_t)s * a.BC + slot] = v;
     if (pp.head) list_join(pp, q, pos, stamp);  // a fill will deliver this row
+    if (pp.req_loc) pp.req_loc[pos] = kPending;
     if (a.slow_stamp[s] != stamp && atomicExch(&a.slow_stamp[s], stamp) != stamp)
       a.slow_list[atomicAdd(pp.nslow, 1u)] = s;  // first miss of the set: k_set processes it
   }
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(256, 4) k_dedup(DedupArgs a, IterState* it, Sc
   pp.head = a.head ? a.head + (size_t)par * a.Q : nullptr;
   pp.nxt = a.nxt ? a.nxt + (size_t)par * a.cap : nullptr;
   pp.nslow = &scr->nslow[par];
+  pp.req_loc = a.req_loc ? a.req_loc + (size_t)par * a.cap : nullptr;
   TRACE_AT(0, par, 0);
   {  // S10: clear the bits of iteration t (its window list is in ring slot t mod (W+1))
     const uint32_t slot = (uint32_t)(t64 % a.Wp1);
@@ -449,6 +456,7 @@ __global__ void __launch_bounds__(256, 4) k_dedup(DedupArgs a, IterState* it, Sc
         ++nreq;
       } else {
         atomicAdd(&scr->bad_ids, 1u);
+        if (pp.req_loc) pp.req_loc[i] = kInvalid;  // ERANGE: k_serve zero-fills the row
       }
     }
   } else {
@@ -1330,6 +1338,7 @@ struct ServeArgs {
   uint64_t N;
   const uint32_t* node_loc;
   uint64_t loc_stride;  // node_loc tables Q apart (parity)
+  const uint32_t* req_loc;  // k_dedup's per-request locations, tables cap apart (parity)
   uint4* out;
   uint32_t bounce;
   uint32_t tail_chunk;  // delivery chunk size near the end of the batch (guided; 32 = fixed)
@@ -1443,6 +1452,7 @@ __global__ void k_serve(ServeArgs a) {
   const unsigned long long* __restrict__ head = a.head + (size_t)par * a.Q;
   const uint32_t* __restrict__ nxt = a.nxt + (size_t)par * a.cap;
   const uint32_t* __restrict__ node_loc = a.node_loc + par * a.loc_stride;
+  const uint32_t* __restrict__ req_loc = a.req_loc + (size_t)par * a.cap;
   const uint32_t nvec = a.nvec;
   const uint32_t wib = threadIdx.x >> 5;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1567,13 +1577,18 @@ __global__ void k_serve(ServeArgs a) {
       }
     }
   }
-  // (a.ahead = 0, or the tail after the reserved chunks): chunks grabbed one at a time
+  // (a.ahead = 0, or the tail after the reserved chunks): chunks grabbed one at a time. A
+  // chunk's locations come from k_dedup's per-request table in one coalesced load; only the
+  // requests it left pending (repeated occurrences, misses) take the ID -> node_loc round trips.
   uint32_t size = a.ahead ? tail : kChunk;
   for (;;) {
     const uint32_t sz = size;
     const int64_t c0 = __shfl_sync(0xffffffffu, grab(sz), 0);
     if (c0 >= n) break;
-    copy_chunk(c0, loc_of(ids_of(c0, sz)));
+    const bool in = c0 + lane < min(c0 + (int64_t)sz, n);
+    uint32_t loc = in ? req_loc[c0 + lane] : kDelivered;
+    if (__ballot_sync(0xffffffffu, loc == kPending) && loc == kPending) loc = loc_of(ids[c0 + lane]);
+    copy_chunk(c0, loc);
     if (c0 >= tail_from) size = tail;
   }
   if (TMA && lane == 0) ring_drain();

@@ -171,6 +171,7 @@ struct Ctx {
   unsigned long long* head = nullptr;            // G = 1 fused delivery: per-node request list heads
   uint32_t* line_info = nullptr;                 // update period > 1: per-line dynamic information
   uint32_t* nxt = nullptr;   // next request position of the same node
+  uint32_t* req_loc = nullptr;  // per request position: a first-occurrence hit's slot, else kPending
   uint8_t* score = nullptr;
   FillEnt* fills = nullptr;
   Cand* cands = nullptr;
@@ -502,7 +503,7 @@ int free_all() {
   cudaDeviceSynchronize();
   void* ptrs[] = {g.tags, g.last_use, g.rr, g.mask, g.mark, g.vst_stamp, g.vst_idx, g.set_cnt, g.slow_stamp, g.slow_list, g.scan_q,
                   g.bucket, g.ring, g.ring_len, g.qcnt, g.qoff, g.qb, g.qlen, g.qnode, g.qreuse,
-                  g.stg_nodes, g.route_cnt, g.head, g.nxt, g.line_info, g.score, g.fills, g.cands,
+                  g.stg_nodes, g.route_cnt, g.head, g.nxt, g.req_loc, g.line_info, g.score, g.fills, g.cands,
                   g.scr, g.it, g.hist, g.g_sv, g.g_sk, g.g_sidx, g.g_skey,
                   g.cum, g.arena, g.tmp_ids, g.tmp_out};
   for (void* p : ptrs)
@@ -668,6 +669,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.last_use = g.last_use;
     da.node_loc = loc_of(g.arena);
     da.loc_stride = g.loc_stride;
+    da.req_loc = G == 1 ? g.req_loc : nullptr;
     da.slow_stamp = g.slow_stamp;
     da.slow_list = g.slow_list;
     da.A = g.A;
@@ -793,6 +795,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.Q = g.Q;
     sa.cap = g.cap;
     sa.loc_stride = g.loc_stride;
+    sa.req_loc = g.req_loc;
     sa.it = g.it;
     sa.N = g.N;
     sa.node_loc = loc_of(g.arena);
@@ -1370,9 +1373,10 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     DA(g.line_info, g.L);
     CK(cudaMemset(g.line_info, 0xFF, g.L * sizeof(uint32_t)));
   }
-  if (G == 1) {  // request lists of the fused delivery, one per iteration parity
+  if (G == 1) {  // request lists and per-request locations of the fused delivery, one per iteration parity
     DA(g.head, 2 * g.Q);
     DA(g.nxt, 2 * g.cap);
+    DA(g.req_loc, 2 * g.cap);
   }
   DA(g.score, g.Q);
   DA(g.fills, 2 * g.ucap);  // one fill list per iteration parity

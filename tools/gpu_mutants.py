@@ -62,6 +62,9 @@ MUTANTS = [
      "request lists of gather t+1 do not overwrite those k_serve(t) walks"),
     ("fills_no_parity", "  FillEnt* const fills_ = p.fills + (size_t)par_ * p.fstride;", "  FillEnt* const fills_ = p.fills;",
      "the fill list of gather t+1 does not overwrite the one k_serve(t) reads"),
+    ("pending_not_resolved", "if (__ballot_sync(0xffffffffu, loc == kPending) && loc == kPending) loc = loc_of(ids[c0 + lane]);",
+     "if (__ballot_sync(0xffffffffu, loc == kPending) && loc == kPending) loc = kDelivered;",
+     "S8 requests k_dedup left pending (repeats, staged rows) are delivered through node_loc"),
     ("record_zeroed_early", "  unsigned long long* nrec = hist + (size_t)((t + 2) % kHist) * F_NFIELDS;",
      "  unsigned long long* nrec = hist + (size_t)((t + 1) % kHist) * F_NFIELDS;",
      "the record of t+1 (already being counted by an early k_dedup) is not zeroed by gather t"),
