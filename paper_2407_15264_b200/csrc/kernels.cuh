@@ -1344,6 +1344,7 @@ struct ServeArgs {
   uint32_t tail_chunk;  // delivery chunk size near the end of the batch (guided; 32 = fixed)
   uint32_t tail_rounds; // ... once fewer than tail_rounds rounds of 32-request chunks remain
   uint32_t ahead;       // keep one 32-request chunk in reserve before the tail phase
+  uint32_t static_first;  // hit-dominated batch: warp w's first delivery chunk is chunk w
   const uint32_t* io_ready;  // file tier: per-chunk "rows read" flags (pinned host, stamped)
   uint32_t ST;  // TMA ring stages per warp
   uint32_t l2ef;  // rows moved with the L2 evict_first policy (RowRing::hint)
@@ -1580,10 +1581,17 @@ __global__ void k_serve(ServeArgs a) {
   // (a.ahead = 0, or the tail after the reserved chunks): chunks grabbed one at a time. A
   // chunk's locations come from k_dedup's per-request table in one coalesced load; only the
   // requests it left pending (repeated occurrences, misses) take the ID -> node_loc round trips.
+  // When every fill warp has at most one fill (a hit-dominated batch), warp w's first chunk is
+  // chunk w (no counter round trip) and the counter hands out the rest from nw chunks on.
   uint32_t size = a.ahead ? tail : kChunk;
+  const bool first_static = !a.ahead && a.static_first && a.scr->nfill[par] <= nw - npull &&
+                            (int64_t)nw * kChunk <= tail_from;
+  const int64_t cbase = first_static ? (int64_t)nw * kChunk : 0;
+  bool first = first_static;
   for (;;) {
     const uint32_t sz = size;
-    const int64_t c0 = __shfl_sync(0xffffffffu, grab(sz), 0);
+    const int64_t c0 = first ? (int64_t)gw * kChunk : cbase + __shfl_sync(0xffffffffu, grab(sz), 0);
+    first = false;
     if (c0 >= n) break;
     const bool in = c0 + lane < min(c0 + (int64_t)sz, n);
     uint32_t loc = in ? req_loc[c0 + lane] : kDelivered;

@@ -230,6 +230,7 @@ struct Ctx {
   cudaStream_t tail_st = nullptr;
   bool feed_early = true;  // LSMGNN_FEED_EARLY=0 turns the early feed start off (A/B)
   bool dedup_early = true;  // LSMGNN_DEDUP_EARLY=0 turns the early k_dedup / k_set start off (A/B)
+  bool serve_static_first = true;  // LSMGNN_SERVE_STATIC_FIRST=0: every chunk from the counter (A/B)
   int early_dedup_per_sm = 2;  // (A/B ab_perSM: 1 0.2044, 2 0.2043, 4 0.2065 ms/step direct)
   uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
   uint64_t set_ctas_issued = 0;    // CTAs of early k_set launches (it->set_ctas_done)
@@ -805,6 +806,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.tail_chunk = (uint32_t)g.serve_tail;
     sa.tail_rounds = (uint32_t)g.serve_tail_rounds;
     sa.ahead = g.serve_ahead ? 1u : 0u;
+    sa.static_first = g.serve_static_first ? 1u : 0u;
     sa.hist = g.hist;
     sa.cum = g.cum;
     sa.bad_mirror = g.bad_dev;
@@ -1447,6 +1449,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (const char* e = std::getenv("LSMGNN_SERVE_AHEAD")) g.serve_ahead = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_L2_EVICT_FIRST")) g.l2_evict_first = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_DEDUP_EARLY")) g.dedup_early = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_SERVE_STATIC_FIRST")) g.serve_static_first = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_EARLY_DEDUP_PER_SM")) g.early_dedup_per_sm = std::max(1, std::min(8, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {

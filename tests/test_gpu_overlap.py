@@ -100,3 +100,21 @@ def test_overlap_slow_feed():
     ho = run_oracle(tr, G=1, N=N, D=D, L=L, A=A, scores=sc, policy="hybrid", pvp=0, W=W)[:, 0, :]
     assert bad == 0
     compare(hg, ho[:K], "overlap slow feed")
+
+
+@pytest.mark.parametrize("static_first", ["1", "0"])
+def test_hit_dominated_large_batches(monkeypatch, static_first):
+    """Batches of ~10^5 requests that nearly all hit (the bench's hit-path shape at 256-B rows):
+    k_serve hands each warp its first delivery chunk statically when every fill warp has at most
+    one fill (LSMGNN_SERVE_STATIC_FIRST), the rest from the counter; overlapped gathers."""
+    monkeypatch.setenv("LSMGNN_SERVE_STATIC_FIRST", static_first)
+    N, D, A, W, K = 200_000, 64, 32, 8, 30
+    g = synth.plcite(N, 8)
+    tr = synth.make_trace(g, 1, 1024, (10, 5, 5), K + W + 1, seed_s=12)
+    sc = synth.static_scores(g)
+    L = N - N % A
+    hg, bad = _run(tr, K, N=N, D=D, L=L, A=A, sc=sc, W=W, shared_out=False)
+    ho = run_oracle(tr, G=1, N=N, D=D, L=L, A=A, scores=sc, policy="hybrid", pvp=0, W=W)[:, 0, :]
+    assert bad == 0
+    compare(hg, ho[:K], f"hit-dominated static_first={static_first}")
+    assert ho[K // 2:, 4].sum() > 0.9 * ho[K // 2:, 3].sum()  # hits / unique: the hit path
