@@ -329,7 +329,7 @@ struct RowRing {
   uint32_t* pend;  // ST entries: the row index (into dst[]) whose load occupies the stage
   uint32_t ST, R;
   uint32_t nl, ns, phase;  // loads issued, stores issued (lane 0), phase bit per stage
-  uint32_t hint;           // 1: rows moved with the L2 evict_first policy `pol`
+  uint32_t hint;           // 1: rows loaded and stored with the L2 evict_first policy `pol`; 2: stored only
   uint64_t pol;
 };
 __device__ __forceinline__ void ring_init(RowRing& r) {  // lane 0; then __syncwarp
@@ -352,7 +352,7 @@ __device__ __forceinline__ void ring_copy(RowRing& r, const void* const* src, vo
       // the stage's last store (number nl - ST) must have read it; later stores may still read
       if (r.nl >= r.ST) bulk_wait_read(r.ns + r.ST - 1 - r.nl);
       mbar_expect_tx(&r.bar[s], r.R);
-      if (r.hint) bulk_g2s_hint(r.buf + (size_t)s * r.R, src[j], r.R, &r.bar[s], r.pol);
+      if (r.hint == 1) bulk_g2s_hint(r.buf + (size_t)s * r.R, src[j], r.R, &r.bar[s], r.pol);
       else bulk_g2s(r.buf + (size_t)s * r.R, src[j], r.R, &r.bar[s]);
       r.pend[s] = j;
       ++r.nl;

@@ -308,6 +308,7 @@ struct DedupArgs {
   uint32_t* node_loc;
   uint64_t loc_stride;  // G = 1: node_loc has one table per iteration parity (Q apart); G > 1: 0
   uint32_t* req_loc;    // G = 1: per-request locations, one table per iteration parity (cap apart)
+  uint32_t meta_evict_last;  // L2 evict_last policy on the probe's metadata accesses (A/B)
   uint32_t* slow_stamp;
   uint32_t* slow_list;  // the sets with a miss this batch (count scr->nslow[t & 1])
   uint32_t A;
@@ -320,6 +321,8 @@ struct DedupPar {
   uint32_t* nxt;
   uint32_t* nslow;
   uint32_t* req_loc;  // G = 1: per request position, the slot of a first-occurrence hit, else kPending
+  uint32_t hint;      // 1: the probe's metadata accesses carry the L2 policy pol
+  uint64_t pol;
 };
 constexpr uint32_t kPending = 0xFFFFFFFEu;  // req_loc: look the location up in node_loc (k_serve)
 // One request: first occurrence of its node (returns 1) is probed against its set's A tags; a
@@ -342,6 +345,23 @@ __device__ __forceinline__ uint4 ld16_issue(const uint4* p) {
   asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+// ... and the same accesses with an L2 eviction-priority policy (DedupPar::pol, evict_last): the
+// probe's scattered metadata stays in L2 while the previous gather's row stream passes through
+__device__ __forceinline__ uint4 ld16_issue_hint(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t atom_exch_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  uint32_t r;
+  asm volatile("atom.global.exch.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(r) : "l"(p), "r"(v), "l"(pol) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_u32_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const DedupArgs& a, const DedupPar& pp,
                                               uint32_t stamp, uint32_t t, uint32_t* nhit) {
   const uint32_t q = v / a.G;
@@ -352,9 +372,11 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
   if (vec) {
     const uint4* t4 = reinterpret_cast<const uint4*>(tg);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) w[i] = 4u * i < a.A ? ld16_issue(t4 + i) : make_uint4(kInvalid, kInvalid, kInvalid, kInvalid);
+    for (int i = 0; i < 8; ++i)
+      w[i] = 4u * i < a.A ? (pp.hint ? ld16_issue_hint(t4 + i, pp.pol) : ld16_issue(t4 + i))
+                          : make_uint4(kInvalid, kInvalid, kInvalid, kInvalid);
   }
-  const bool first = atomicExch(&a.mark[q], stamp) != stamp;
+  const bool first = (pp.hint ? atom_exch_hint(&a.mark[q], stamp, pp.pol) : atomicExch(&a.mark[q], stamp)) != stamp;
   if (!first) {
     if (pp.head) list_join(pp, q, pos, stamp);
     if (pp.req_loc) pp.req_loc[pos] = kPending;
@@ -374,9 +396,14 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
       if (tg[k] == v) way = (int)k;
   }
   if (way >= 0) {
-    pp.node_loc[q] = s * a.A + (uint32_t)way;
+    if (pp.hint) {
+      st_u32_hint(&pp.node_loc[q], s * a.A + (uint32_t)way, pp.pol);
+      st_u32_hint(&a.last_use[s * a.A + (uint32_t)way], t, pp.pol);
+    } else {
+      pp.node_loc[q] = s * a.A + (uint32_t)way;
+      a.last_use[s * a.A + (uint32_t)way] = t;
+    }
     if (pp.req_loc) pp.req_loc[pos] = s * a.A + (uint32_t)way;
-    a.last_use[s * a.A + (uint32_t)way] = t;
     ++*nhit;
   } else {
     const uint32_t slot = atomicAdd(&a.set_cnt[s], 1u);
@@ -428,6 +455,9 @@ __global__ void __launch_bounds__(256, 4) k_dedup(DedupArgs a, IterState* it, Sc
   pp.nxt = a.nxt ? a.nxt + (size_t)par * a.cap : nullptr;
   pp.nslow = &scr->nslow[par];
   pp.req_loc = a.req_loc ? a.req_loc + (size_t)par * a.cap : nullptr;
+  pp.hint = a.meta_evict_last;
+  pp.pol = 0;
+  if (pp.hint) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pp.pol));
   TRACE_AT(0, par, 0);
   {  // S10: clear the bits of iteration t (its window list is in ring slot t mod (W+1))
     const uint32_t slot = (uint32_t)(t64 % a.Wp1);

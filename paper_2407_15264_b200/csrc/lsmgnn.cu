@@ -230,6 +230,7 @@ struct Ctx {
   cudaStream_t tail_st = nullptr;
   bool feed_early = true;  // LSMGNN_FEED_EARLY=0 turns the early feed start off (A/B)
   bool dedup_early = true;  // LSMGNN_DEDUP_EARLY=0 turns the early k_dedup / k_set start off (A/B)
+  bool meta_evict_last = false;  // LSMGNN_META_EVICT_LAST=1: k_dedup's metadata accesses evict_last in L2 (A/B)
   bool serve_static_first = true;  // LSMGNN_SERVE_STATIC_FIRST=0: every chunk from the counter (A/B)
   int early_dedup_per_sm = 2;  // (A/B ab_perSM: 1 0.2044, 2 0.2043, 4 0.2065 ms/step direct)
   uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
@@ -242,7 +243,7 @@ struct Ctx {
   // k_serve geometry: CTAs per SM and TMA row stages per warp (0 = 16-B vector copies);
   // LSMGNN_SERVE_CPS / LSMGNN_SERVE_ST override (A/B runs)
   int serve_cps = 2, serve_st = 3;
-  bool l2_evict_first = false;  // LSMGNN_L2_EVICT_FIRST=1: ring row copies with the L2 evict_first policy (A/B ab_l2: slower)
+  int l2_evict_first = 0;  // LSMGNN_L2_EVICT_FIRST=1: ring row copies with the L2 evict_first policy (A/B ab_l2: slower); 2: stores only
   int serve_tail = 4;  // LSMGNN_SERVE_TAIL=n: k_serve's delivery chunk size near the batch end (A/B)
   int serve_tail_rounds = 2;  // LSMGNN_SERVE_TAIL_ROUNDS=r: ... once fewer than r rounds of chunks remain
   bool serve_ahead = false;   // LSMGNN_SERVE_AHEAD=1: one chunk in reserve before the tail phase (measured slower)
@@ -671,6 +672,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.node_loc = loc_of(g.arena);
     da.loc_stride = g.loc_stride;
     da.req_loc = G == 1 ? g.req_loc : nullptr;
+    da.meta_evict_last = g.meta_evict_last ? 1u : 0u;
     da.slow_stamp = g.slow_stamp;
     da.slow_list = g.slow_list;
     da.A = g.A;
@@ -812,7 +814,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.bad_mirror = g.bad_dev;
     const bool tma = !out_host && g.serve_st > 0;
     sa.ST = tma ? (uint32_t)g.serve_st : 0u;
-    sa.l2ef = g.l2_evict_first ? 1u : 0u;
+    sa.l2ef = (uint32_t)g.l2_evict_first;
     const size_t smem = tma ? (size_t)8 * g.serve_st * g.R : 0;
     const int blocks = g.sms * std::min(tma ? g.serve_cps : 4, g.geom_per_sm);
 #define SERVE(U, O, T) KLAUNCH((k_serve<U, O, T>), blocks, 256, smem, st, sa)
@@ -845,7 +847,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     pa.tail_rounds = (uint32_t)g.serve_tail_rounds;
     const bool tma = !out_host && g.serve_st > 0;
     pa.ST = tma ? (uint32_t)g.serve_st : 0u;
-    pa.l2ef = g.l2_evict_first ? 1u : 0u;
+    pa.l2ef = (uint32_t)g.l2_evict_first;
     const size_t psmem = tma ? (size_t)8 * g.serve_st * g.R : 0;
     // a warp per 32 requests; with TMA rings, at most serve_cps CTAs per SM fit
     const int pblocks = grid_for(n_bound, 256, tma ? g.serve_cps : 8);
@@ -1447,8 +1449,9 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (const char* e = std::getenv("LSMGNN_SERVE_TAIL")) g.serve_tail = std::max(1, std::min(32, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_SERVE_TAIL_ROUNDS")) g.serve_tail_rounds = std::max(0, std::min(64, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_SERVE_AHEAD")) g.serve_ahead = std::atoi(e) != 0;
-  if (const char* e = std::getenv("LSMGNN_L2_EVICT_FIRST")) g.l2_evict_first = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_L2_EVICT_FIRST")) g.l2_evict_first = std::max(0, std::min(2, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_DEDUP_EARLY")) g.dedup_early = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_META_EVICT_LAST")) g.meta_evict_last = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_SERVE_STATIC_FIRST")) g.serve_static_first = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_EARLY_DEDUP_PER_SM")) g.early_dedup_per_sm = std::max(1, std::min(8, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
