@@ -37,6 +37,20 @@ __device__ __forceinline__ unsigned long long trace_now() {
 #define TRACE_AT(k, par, e) do { } while (0)
 #endif
 
+// Reuse-bitmask updates with an L2 eviction-priority policy (evict_last: the mask rows the window
+// feed sets, k_dedup clears and k_set reads stay in L2 while the row stream passes through)
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void red_or_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void red_and_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("red.global.and.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
 // ------------------------------------------------------------------------------ S9
 // Start gather t: publish the iteration's values (IterState), zero its record and the per-batch
 // scratch counters. t_host >= 0: t and the batch come from the
@@ -164,9 +178,11 @@ __global__ void k_win_begin(IterState* it, int64_t k_host, const int64_t* ids_ho
 // k_dedup(t+1) still covers gather t, and so does any later work the caller puts on the stream.
 __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_host, int64_t n_host, uint32_t Wp1,
                               uint64_t N, uint32_t* __restrict__ ring, uint64_t stride, uint32_t* __restrict__ ring_len,
-                              Scratch* scr, uint32_t* __restrict__ mask, uint32_t MW, uint32_t wait_prev) {
+                              Scratch* scr, uint32_t* __restrict__ mask, uint32_t MW, uint32_t wait_prev,
+                              uint32_t mask_hint) {
   if (wait_prev || k_host < 0) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint64_t mpol = mask_hint ? l2_evict_last_policy() : 0;
   const int64_t* __restrict__ ids;
   int64_t n;
   uint32_t slot;
@@ -185,7 +201,8 @@ __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_
     const int64_t x = ids[i];
     if (x >= 0 && (uint64_t)x < N) {
       list[i] = (uint32_t)x;
-      atomicOr(&mask[(size_t)x * MW + (slot >> 5)], 1u << (slot & 31));  // G = 1: q = v
+      if (mask_hint) red_or_hint(&mask[(size_t)x * MW + (slot >> 5)], 1u << (slot & 31), mpol);  // G = 1: q = v
+      else atomicOr(&mask[(size_t)x * MW + (slot >> 5)], 1u << (slot & 31));
     } else {
       list[i] = kInvalid;
       atomicAdd(&scr->bad_ids, 1u);
@@ -309,6 +326,7 @@ struct DedupArgs {
   uint64_t loc_stride;  // G = 1: node_loc has one table per iteration parity (Q apart); G > 1: 0
   uint32_t* req_loc;    // G = 1: per-request locations, one table per iteration parity (cap apart)
   uint32_t meta_evict_last;  // L2 evict_last policy on the probe's metadata accesses (A/B)
+  uint32_t mask_hint;        // ... and on the window clear's mask updates
   uint32_t* slow_stamp;
   uint32_t* slow_list;  // the sets with a miss this batch (count scr->nslow[t & 1])
   uint32_t A;
@@ -464,13 +482,16 @@ __global__ void __launch_bounds__(256, 4) k_dedup(DedupArgs a, IterState* it, Sc
     const uint32_t* __restrict__ list = a.ring + (size_t)slot * a.ring_stride;
     const uint32_t nl = a.ring_len[slot];
     const uint32_t m = ~(1u << (slot & 31));
+    const uint64_t mpol = a.mask_hint ? l2_evict_last_policy() : 0;
     if (nl == 0xFFFFFFFFu) {  // the slot's list did not fit its ring slot (k_win_gather): sweep
       for (uint64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < a.Q; q += stride)
         atomicAnd(&a.mask[q * a.MW + (slot >> 5)], m);
     } else {
       for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nl; i += stride) {
         const uint32_t v = list[i];
-        if (v != kInvalid) atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
+        if (v == kInvalid) continue;
+        if (a.mask_hint) red_and_hint(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m, mpol);
+        else atomicAnd(&a.mask[(size_t)(v / a.G) * a.MW + (slot >> 5)], m);
       }
     }
   }

@@ -235,6 +235,10 @@ struct Ctx {
   // (A/B ab_l2b: hit path 0.2053 -> 0.1984 ms/step, k_serve 0.935 -> 0.943): on when that metadata
   // (~20 B per home row) fits in half the L2; LSMGNN_META_EVICT_LAST=0/1 overrides
   bool meta_evict_last = false;
+  // ... and the reuse-bitmask updates of the window feed and its clear (A/B ab_mk: hit path
+  // 0.1996 -> 0.1928 ms/step): on when the metadata plus the mask (4·MW B per row) fit half the L2;
+  // LSMGNN_MASK_EVICT_LAST=0/1 overrides
+  bool mask_evict_last = false;
   bool serve_static_first = true;  // LSMGNN_SERVE_STATIC_FIRST=0: every chunk from the counter (A/B)
   int early_dedup_per_sm = 2;  // (A/B ab_perSM: 1 0.2044, 2 0.2043, 4 0.2065 ms/step direct)
   uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
@@ -677,6 +681,7 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     da.loc_stride = g.loc_stride;
     da.req_loc = G == 1 ? g.req_loc : nullptr;
     da.meta_evict_last = g.meta_evict_last ? 1u : 0u;
+    da.mask_hint = g.mask_evict_last ? 1u : 0u;
     da.slow_stamp = g.slow_stamp;
     da.slow_list = g.slow_list;
     da.A = g.A;
@@ -931,12 +936,12 @@ int launch_window(int64_t k_host, const int64_t* ids, int64_t n, const int64_t* 
               (int64_t)g.cap, g.bad_dev_overflow);
       LAUNCHED();
       KLAUNCH(k_route_local, grid_for(n_bound, 256), 256, 0, st, g.it, (int64_t)-1, (const int64_t*)nullptr, (int64_t)0,
-              g.Wp1, g.N, g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, 1u);
+              g.Wp1, g.N, g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, 1u, g.mask_evict_last ? 1u : 0u);
       LAUNCHED();
     } else {  // direct: one launch, the batch as kernel arguments
       const uint32_t wait_prev = (g.feed_early && g.tail_gather && g.tail_st == st) ? 0u : 1u;
       KLAUNCH(k_route_local, grid_for(std::max<int64_t>(n, 1), 256), 256, 0, st, g.it, k_host, ids, n, g.Wp1, g.N,
-              g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, wait_prev);
+              g.ring, stride, g.ring_len, g.scr, g.mask, g.MW, wait_prev, g.mask_evict_last ? 1u : 0u);
       LAUNCHED();
       if (!wait_prev) g.feed_ctas_issued += (uint64_t)grid_for(std::max<int64_t>(n, 1), 256);  // (counted done)
       if (!wait_prev) g.tail_feed = true;  // (tail_st unchanged: the same stream)
@@ -1456,7 +1461,9 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (const char* e = std::getenv("LSMGNN_L2_EVICT_FIRST")) g.l2_evict_first = std::max(0, std::min(2, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_DEDUP_EARLY")) g.dedup_early = std::atoi(e) != 0;
   g.meta_evict_last = g.Q * 20 <= (60ull << 20);
+  g.mask_evict_last = g.Q * (20 + 4ull * g.MW) <= (64ull << 20);
   if (const char* e = std::getenv("LSMGNN_META_EVICT_LAST")) g.meta_evict_last = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_MASK_EVICT_LAST")) g.mask_evict_last = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_SERVE_STATIC_FIRST")) g.serve_static_first = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_EARLY_DEDUP_PER_SM")) g.early_dedup_per_sm = std::max(1, std::min(8, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
