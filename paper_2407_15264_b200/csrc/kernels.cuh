@@ -1408,9 +1408,32 @@ struct ServeArgs {
 // S9: close iteration t's record — algorithmic bytes per tier, cumulative sums; the staging
 // count of the next parity is reset so that a missing PVP call stages nothing; the ERANGE
 // counter is mirrored to pinned host memory; it->t_next = t + 1. One warp (lane = field).
+// What the next gathers need comes first — the counters and the record of t + 2 start at zero,
+// then t_next is published (an early k_serve of t + 1 waits for it) — and the bookkeeping of
+// t's own record and the cumulative sums after it (read only once the stream is synchronised).
 __device__ __forceinline__ void end_record(uint64_t t, IterState* it, unsigned long long* hist, unsigned long long* cum,
                                            Scratch* scr, uint32_t R, volatile uint32_t* bad_mirror) {
   const uint32_t f = lane_id();
+  // prepare gather t + 2 (k_dedup / k_set of t + 1 may already be counting into the record of
+  // t + 1 and the parity counters of t + 1; those were zeroed here by gather t - 1): the record
+  // of t + 2 and the parity counters of t (= those of t + 2) start at zero; the counters only
+  // k_serve / k_pull of t + 1 use (they start after gather t completed) are reset for t + 1
+  unsigned long long* nrec = hist + (size_t)((t + 2) % kHist) * F_NFIELDS;
+  if (f < F_NFIELDS) nrec[f] = 0;
+  if (f == 0) {
+    scr->nfill[t & 1] = 0;
+    scr->ncand = 0;
+    scr->nbypass[t & 1] = 0;
+    scr->pull_next = 0;
+    scr->pull_phase_next[0] = 0;
+    scr->pull_phase_next[1] = 0;
+    scr->nslow[t & 1] = 0;
+  }
+  __syncwarp();
+  if (f == 0) {  // gather t is complete (an early k_serve of t + 1 waits for this)
+    __threadfence();
+    *(volatile uint64_t*)&it->t_next = t + 1;  // direct calls and graph replays may be mixed
+  }
   unsigned long long* rec = hist + (size_t)(t % kHist) * F_NFIELDS;
   if (f == 0) {
     rec[F_PREF] = scr->staged[t & 1];  // rows the PVP staged for t (its copy completed before gather t)
@@ -1430,27 +1453,6 @@ __device__ __forceinline__ void end_record(uint64_t t, IterState* it, unsigned l
     cum[F_ITER] = t;
     scr->staged[(t + 1) & 1] = 0;
     *bad_mirror = scr->bad_ids;
-  }
-  __syncwarp();
-  // prepare gather t + 2 (k_dedup / k_set of t + 1 may already be counting into the record of
-  // t + 1 and the parity counters of t + 1; those were zeroed here by gather t - 1): the record
-  // of t + 2 and the parity counters of t (= those of t + 2) start at zero; the counters only
-  // k_serve / k_pull of t + 1 use (they start after gather t completed) are reset for t + 1
-  unsigned long long* nrec = hist + (size_t)((t + 2) % kHist) * F_NFIELDS;
-  if (f < F_NFIELDS) nrec[f] = 0;
-  if (f == 0) {
-    scr->nfill[t & 1] = 0;
-    scr->ncand = 0;
-    scr->nbypass[t & 1] = 0;
-    scr->pull_next = 0;
-    scr->pull_phase_next[0] = 0;
-    scr->pull_phase_next[1] = 0;
-    scr->nslow[t & 1] = 0;
-  }
-  __syncwarp();
-  if (f == 0) {  // last: gather t is complete (k_dedup of t + 1 may be waiting for this, below)
-    __threadfence();
-    *(volatile uint64_t*)&it->t_next = t + 1;  // direct calls and graph replays may be mixed
   }
 }
 
