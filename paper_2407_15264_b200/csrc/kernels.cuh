@@ -213,8 +213,6 @@ __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_
     // (feeds of consecutive iterations may overlap: the latest one wins)
     if (k_host >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&it->wk_next), (unsigned long long)k_host + 1);
   }
-  // complete after k_serve(t): one CTA waits, the others exit and free their SM slots (for the
-  // early k_dedup of gather t + 1)
   TRACE_AT(4, (uint32_t)(k_host & 1), 1);
   // early feed (behind a G = 1 gather): this CTA's list entries and bits are written — count it
   // (an early k_set waits for the count of the early feeds the host launched; a feed that is not
@@ -227,6 +225,8 @@ __global__ void k_route_local(IterState* it, int64_t k_host, const int64_t* ids_
       atomicAdd(&it->feed_ctas_done, 1ull);
     }
   }
+  // complete after k_serve(t): one CTA waits, the others exit and free their SM slots (for the
+  // early k_dedup of gather t + 1)
   if (!wait_prev && k_host >= 0 && blockIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
@@ -438,12 +438,13 @@ __device__ __forceinline__ uint32_t dedup_one(uint32_t v, uint32_t pos, const De
 // the start. Everything this launch reads is final once k_serve(t-1) has started — the cache
 // state (k_set(t-1) completed before k_serve(t-1) could trigger), the caller's IDs (produced
 // before gather(t-1) or by a non-programmatic predecessor), the window slot of t — and what it
-// writes is not read by k_serve(t-1): node_loc, the request lists and the slow-set counter are
-// parity-indexed, the record of t is its own, and k_serve(t-1) copied IterState before it let
-// this launch start. So the dedup and hit probe of t run alongside the delivery of t-1 and so
-// does k_set(t) behind it (it waits only for the window feeds issued before gather t, and writes
+// writes is not read by k_serve(t-1): node_loc, the request lists, the per-request locations and
+// the slow-set counter are parity-indexed, the record of t is its own, and k_serve(t-1) of a
+// direct call takes its iteration's values from its arguments, not from IterState. So the dedup
+// and hit probe of t run alongside the delivery of t-1 and so does k_set(t) behind it (it waits
+// for this launch's finished-CTA count and the window feeds issued before gather t, and writes
 // nothing k_serve(t-1) reads: fill list, counters and node_loc are parity-indexed); k_serve(t)
-// then waits for k_serve(t-1)'s published t_next before it fills any slot.
+// then waits for k_set(t)'s count and k_serve(t-1)'s published t_next before it fills any slot.
 __global__ void __launch_bounds__(256, 4) k_dedup(DedupArgs a, IterState* it, Scratch* scr, unsigned long long* hist, BeginArgs ba,
                         uint32_t fused_begin, uint32_t early) {
   // (every thread reaches the __syncthreads below: no early exit before it)
