@@ -45,6 +45,19 @@
  *                             starts alongside k_serve and waits for it at its end)
  *   LSMGNN_G1_PULL=1          G = 1 profiling aid: the G > 1 serve path (k_fill, k_pull phases,
  *                             k_end) instead of the fused k_serve; results are identical
+ *   LSMGNN_DEDUP_EARLY=0      consecutive direct G = 1 gathers do not overlap (default: the next
+ *                             gather's k_dedup / k_set run while the previous k_serve delivers,
+ *                             without PVP, file tier or periodic scan; stream order unchanged)
+ *   LSMGNN_EARLY_DEDUP_PER_SM=c  CTAs per SM of an overlapped k_dedup (default 2)
+ *   LSMGNN_SERVE_STATIC_FIRST=0  every delivery chunk from the counter (default: a warp's first
+ *                             chunk is static in hit-dominated batches)
+ *   LSMGNN_META_EVICT_LAST=0|1, LSMGNN_MASK_EVICT_LAST=0|1  L2 evict_last policy on k_dedup's
+ *                             metadata accesses / on the reuse-bitmask updates (default: on
+ *                             when they fit half the L2)
+ *   LSMGNN_L2_EVICT_FIRST=1|2 L2 evict_first policy on the TMA ring row copies (1: loads and
+ *                             stores, 2: stores; default off — measured slower)
+ * Every switch changes timing only: results are bit-identical (tests/test_gpu_overlap.py,
+ * test_serve_geometry).
  */
 #ifndef LSMGNN_H
 #define LSMGNN_H
