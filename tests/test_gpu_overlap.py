@@ -72,16 +72,22 @@ def test_overlapped_gathers_parity(regime, shared_out):
     compare(hg, ho[:K], f"overlap {regime} shared_out={shared_out}")
 
 
-def test_overlap_toggle_identical(monkeypatch):
-    """LSMGNN_DEDUP_EARLY=0 (every kernel waits for its predecessor) gives the same records."""
+@pytest.mark.parametrize("switches", [{"LSMGNN_DEDUP_EARLY": "0"},
+                                      {"LSMGNN_META_EVICT_LAST": "0", "LSMGNN_MASK_EVICT_LAST": "0",
+                                       "LSMGNN_SERVE_STATIC_FIRST": "0"},
+                                      {"LSMGNN_L2_EVICT_FIRST": "1", "LSMGNN_EARLY_DEDUP_PER_SM": "1"}])
+def test_overlap_toggle_identical(monkeypatch, switches):
+    """The timing switches (no overlap: every kernel waits for its predecessor; no L2 policies;
+    other geometries) give the same records and rows as the defaults."""
     N, D, A, W, K = 60000, 64, 32, 6, 30
     L = 12000
     tr, sc = _trace(N, 256, (10, 5, 5), K, W)
     h1, bad1 = _run(tr, K, N=N, D=D, L=L, A=A, sc=sc, W=W, shared_out=False)
-    monkeypatch.setenv("LSMGNN_DEDUP_EARLY", "0")
+    for k, v in switches.items():
+        monkeypatch.setenv(k, v)
     h0, bad0 = _run(tr, K, N=N, D=D, L=L, A=A, sc=sc, W=W, shared_out=False)
     assert bad1 == 0 and bad0 == 0
-    compare(h1, h0, "early vs serialised")
+    compare(h1, h0, f"defaults vs {switches}")
 
 
 def test_overlap_slow_feed():
