@@ -48,7 +48,8 @@
  *   LSMGNN_DEDUP_EARLY=0      consecutive direct G = 1 gathers do not overlap (default: the next
  *                             gather's k_dedup / k_set run while the previous k_serve delivers,
  *                             without PVP, file tier or periodic scan; stream order unchanged)
- *   LSMGNN_EARLY_DEDUP_PER_SM=c  CTAs per SM of an overlapped k_dedup (default 2)
+ *   LSMGNN_EARLY_DEDUP_PER_SM=c, LSMGNN_EARLY_SET_PER_SM=c  CTAs per SM of an overlapped
+ *                             k_dedup / k_set (defaults 2, 2)
  *   LSMGNN_SERVE_STATIC_FIRST=0  every delivery chunk from the counter (default: a warp's first
  *                             chunk is static in hit-dominated batches)
  *   LSMGNN_META_EVICT_LAST=0|1, LSMGNN_MASK_EVICT_LAST=0|1  L2 evict_last policy on k_dedup's

@@ -240,6 +240,7 @@ struct Ctx {
   // LSMGNN_MASK_EVICT_LAST=0/1 overrides
   bool mask_evict_last = false;
   bool serve_static_first = true;  // LSMGNN_SERVE_STATIC_FIRST=0: every chunk from the counter (A/B)
+  int early_set_per_sm = 2;  // (A/B ab_setsm: 1 0.1910, 2 0.1911, 4 0.1927 ms/step direct)
   int early_dedup_per_sm = 2;  // (A/B ab_perSM: 1 0.2044, 2 0.2043, 4 0.2065 ms/step direct)
   uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
   uint64_t set_ctas_issued = 0;    // CTAs of early k_set launches (it->set_ctas_done)
@@ -756,8 +757,10 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     LAUNCHED();
   }
   {
-    const int64_t blocks =
-        std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps, (int64_t)g.sms * std::min(4, g.geom_per_sm));
+    // (an early k_set shares the SMs with the previous k_serve: LSMGNN_EARLY_SET_PER_SM caps its CTAs
+    // per SM, A/B)
+    const int64_t blocks = std::min<int64_t>((g.S + g.set_warps - 1) / g.set_warps,
+                                             (int64_t)g.sms * std::min(early ? g.early_set_per_sm : 4, g.geom_per_sm));
     KLAUNCH(k_set, (int)blocks, 32 * g.set_warps, g.warp_bytes * g.set_warps, st, sp);
     LAUNCHED();
     if (early) g.set_ctas_issued += (uint64_t)blocks;  // (an early k_set counts them done)
@@ -1465,6 +1468,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (const char* e = std::getenv("LSMGNN_META_EVICT_LAST")) g.meta_evict_last = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_MASK_EVICT_LAST")) g.mask_evict_last = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_SERVE_STATIC_FIRST")) g.serve_static_first = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_EARLY_SET_PER_SM")) g.early_set_per_sm = std::max(1, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_EARLY_DEDUP_PER_SM")) g.early_dedup_per_sm = std::max(1, std::min(8, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
   if (G > 1) {
