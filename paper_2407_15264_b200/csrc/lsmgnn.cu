@@ -240,6 +240,7 @@ struct Ctx {
   // LSMGNN_MASK_EVICT_LAST=0/1 overrides
   bool mask_evict_last = false;
   bool serve_static_first = true;  // LSMGNN_SERVE_STATIC_FIRST=0: every chunk from the counter (A/B)
+  bool host_tma = false;  // LSMGNN_HOST_TMA=1: TMA ring delivery into a pinned host `out` (A/B)
   int early_set_per_sm = 2;  // (A/B ab_setsm: 1 0.1910, 2 0.1911, 4 0.1927 ms/step direct)
   int early_dedup_per_sm = 2;  // (A/B ab_perSM: 1 0.2044, 2 0.2043, 4 0.2065 ms/step direct)
   uint64_t dedup_ctas_issued = 0;  // CTAs of early k_dedup launches (it->dedup_ctas_done)
@@ -824,13 +825,16 @@ int launch_gather(const BeginArgs& ba, int64_t n_bound, void* out, bool out_host
     sa.hist = g.hist;
     sa.cum = g.cum;
     sa.bad_mirror = g.bad_dev;
-    const bool tma = !out_host && g.serve_st > 0;
+    // pinned host `out`: LSMGNN_HOST_TMA=1 delivers through the TMA rings too (bulk stores to the
+    // host mapping; A/B)
+    const bool tma = (!out_host || g.host_tma) && g.serve_st > 0;
     sa.ST = tma ? (uint32_t)g.serve_st : 0u;
     sa.l2ef = (uint32_t)g.l2_evict_first;
     const size_t smem = tma ? (size_t)8 * g.serve_st * g.R : 0;
     const int blocks = g.sms * std::min(tma ? g.serve_cps : 4, g.geom_per_sm);
 #define SERVE(U, O, T) KLAUNCH((k_serve<U, O, T>), blocks, 256, smem, st, sa)
-    if (wide && tma) SERVE(8, kDev, 1);
+    if (wide && tma && out_host) SERVE(8, kHost, 1);
+    else if (wide && tma) SERVE(8, kDev, 1);
     else if (wide && !out_host) SERVE(8, kDev, 0);
     else if (wide) SERVE(8, kHost, 0);
     else if (tma) SERVE(2, kDev, 1);
@@ -1448,6 +1452,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
     if (g.serve_st) {
       const int smem = (int)((size_t)8 * g.serve_st * g.R);
       CK(cudaFuncSetAttribute(k_serve<8, kDev, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      CK(cudaFuncSetAttribute(k_serve<8, kHost, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       CK(cudaFuncSetAttribute(k_serve<2, kDev, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       CK(cudaFuncSetAttribute(k_pull<8, kDev, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       CK(cudaFuncSetAttribute(k_pull<8, kDev, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1468,6 +1473,7 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   if (const char* e = std::getenv("LSMGNN_META_EVICT_LAST")) g.meta_evict_last = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_MASK_EVICT_LAST")) g.mask_evict_last = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_SERVE_STATIC_FIRST")) g.serve_static_first = std::atoi(e) != 0;
+  if (const char* e = std::getenv("LSMGNN_HOST_TMA")) g.host_tma = std::atoi(e) != 0;
   if (const char* e = std::getenv("LSMGNN_EARLY_SET_PER_SM")) g.early_set_per_sm = std::max(1, std::min(4, std::atoi(e)));
   if (const char* e = std::getenv("LSMGNN_EARLY_DEDUP_PER_SM")) g.early_dedup_per_sm = std::max(1, std::min(8, std::atoi(e)));
   if (g.g1_pull) g.split_pull = false;
