@@ -1432,8 +1432,10 @@ int lsmgnn_init(int64_t num_nodes, int32_t feat_dim, lsmgnn_dtype dtype, int64_t
   CK(cudaEventCreateWithFlags(&g.ev_pvp, cudaEventDisableTiming));
   CK(cudaFuncSetAttribute(k_set, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(g.warp_bytes * g.set_warps)));
   {  // k_serve / k_pull: the most row loads in flight per SM — (ST - 1) per warp, 8 warps per
-     // CTA, up to 3 CTAs (registers) — within ~192 KB of shared memory per SM
-    const uint64_t budget = 192 * 1024;
+     // CTA, up to 3 CTAs (registers) — within 160 KB of shared memory per SM, which leaves room
+     // for the next gather's k_dedup / k_set beside it (A/B ab_geo2 at 4 KiB rows: 5 stages
+     // 0.1873 ms/step, 6 stages 0.1916, 4 stages 0.1870, 3 stages 0.1913)
+    const uint64_t budget = 160 * 1024;
     g.serve_cps = 1;
     g.serve_st = 0;
     uint64_t best = 0;
