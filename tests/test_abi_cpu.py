@@ -56,3 +56,16 @@ def test_product_does_not_touch_oracle():
     if os.path.exists(so):
         needed = subprocess.run(["readelf", "-d", so], capture_output=True, text=True).stdout
         assert "oracle" not in needed
+
+
+def test_environment_switches_documented():
+    """Every LSMGNN_* environment switch the library reads is documented in include/lsmgnn.h
+    (the one place the header lists them), and every documented one is read."""
+    src = open(os.path.join(ROOT, "paper_2407_15264_b200", "csrc", "lsmgnn.cu")).read()
+    read = set(re.findall(r'getenv\("(LSMGNN_[A-Z0-9_]+)"\)', src))
+    hdr = open(os.path.join(ROOT, "include", "lsmgnn.h")).read()
+    block = hdr[hdr.index("Environment"):hdr.index("#ifndef LSMGNN_H")] if "Environment" in hdr else hdr
+    documented = set(re.findall(r"\b(LSMGNN_[A-Z][A-Z0-9_]*)=", block)) | set(re.findall(r",\s*(LSMGNN_[A-Z0-9_]+)=", block))
+    assert read, "no switches found"
+    assert read <= set(re.findall(r"LSMGNN_[A-Z0-9_]+", hdr)), read - set(re.findall(r"LSMGNN_[A-Z0-9_]+", hdr))
+    assert documented <= read, documented - read
