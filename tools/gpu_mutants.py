@@ -38,14 +38,14 @@ MUTANTS = [
      "R6 stale snapshot is Fresh"),
     ("pull_phase1_skips", "const uint32_t need = __ballot_sync(0xffffffffu, valid && (((loc & kDelivered) != 0) == (PHASE == 1)));",
      "const uint32_t need = __ballot_sync(0xffffffffu, valid && !(loc & kDelivered));", "G > 1 filled rows pulled after served"),
-    ("probe_no_last_use", "    a.last_use[s * a.A + (uint32_t)way] = t;\n    ++*nhit;", "    ++*nhit;",
-     "R10/R20 a hit's last use is t (k_dedup probe; k_set protects the ways used at t)"),
+    ("probe_no_last_use", "      st_u32_hint(&a.last_use[s * a.A + (uint32_t)way], t, pp.pol);\n", "",
+     "R10/R20 a hit's last use is t (k_dedup probe, L2-hinted path; k_set protects the ways used at t)"),
     ("slow_set_dropped", "      a.slow_list[atomicAdd(pp.nslow, 1u)] = s;  // first miss of the set: k_set processes it",
      "      (void)s;", "S4/S5 every set with a miss is replaced"),
     ("miss_not_listed", "    if (pp.head) list_join(pp, q, pos, stamp);  // a fill will deliver this row",
      "", "S8 a filled node's first requester receives the row"),
-    ("hit_into_bucket", "  if (way >= 0) {\n    pp.node_loc[q] = s * a.A + (uint32_t)way;",
-     "  if (way >= 0) {\n    a.bucket[(size_t)s * a.BC + atomicAdd(&a.set_cnt[s], 1u)] = v;\n    pp.node_loc[q] = s * a.A + (uint32_t)way;",
+    ("hit_into_bucket", "  if (way >= 0) {\n    if (pp.hint) {",
+     "  if (way >= 0) {\n    a.bucket[(size_t)s * a.BC + atomicAdd(&a.set_cnt[s], 1u)] = v;\n    if (pp.hint) {",
      "S3/S4 the buckets hold the misses only (a hit re-installed would be counted twice)"),
     ("protect_none", "const uint32_t protm = __ballot_sync(0xffffffffu, lane < A && tg != kInvalid && lu == t_);",
      "const uint32_t protm = 0u;", "R10 hits of the batch are protected from eviction"),

@@ -12,7 +12,7 @@ for m in ab/mut_*.so; do
   cp $m $SO
   timeout 600 python -m pytest tests/test_gpu_overlap.py tests/test_gpu_parity.py tests/test_gpu_storage_file.py -x -q -p no:cacheprovider > $out/$name.log 2>&1
   rc=$?
-  if [ $rc = 0 ]; then
+  if [ $rc = 0 ] && [ -z "${MUT_SKIP_MP:-}" ]; then
     timeout 900 python -m pytest tests/test_gpu_multiproc.py -x -q -p no:cacheprovider -k "parity or edge" >> $out/$name.log 2>&1
     rc=$?
   fi
