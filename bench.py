@@ -768,8 +768,9 @@ def hbm_regime(wl, scores, table, ids_d, args, max_ids, dev, hbm_peak, hbm_src, 
                          "per_launch": {"algorithmic_bytes": int(alg / psteps), "avg_ms": round(serve_ms / psteps, 4),
                                         "units": "2R per request + 2R per fill row"}},
             "what": "cache holds the whole table: the hit path alone (HBM-bound), same trace as the headline; "
-                    "value/ms_per_step from steps without phase events, phases and k_serve's roofline from "
-                    "profiled_steps more steps with events around each phase"}
+                    "value/ms_per_step from steps without phase events (direct calls on one stream: the next "
+                    "gather's dedup and replacement overlap the current delivery), phases and k_serve's roofline "
+                    "from profiled_steps more steps with events around each phase (kernels serialised)"}
 
 
 def pvp_ablation(wl, scores, table, ids_d, lines, args, max_ids, dev, train_ms=10.0, warm=10, steps=20):
